@@ -1,0 +1,202 @@
+/*
+ * dit.h -- C ABI of the B200-native denoise-step library (libdit.so).
+ *
+ * One call of dit_step() is one LegoDiffusion "model-execution node" of the
+ * shared base diffusion model: execute(model_components, **kwargs) ->
+ * {"noise_pred"} (Fig. flux_model_integration) over a
+ * cross-workflow batch of up to B_max same-model nodes (PAPER.md:1152-1154,
+ * :1178-1187), followed by denoise(noise_pred, latents).
+ * The base model is a Flux-Dev-shaped MMDiT (the paper names Flux-Dev,
+ * PAPER.md:154, :1306, but never defines it: DESIGN.md reading C1).
+ *
+ * Conventions
+ *  - Every call returns an int status (DIT_OK = 0).  Every call validates ALL
+ *    arguments before it enqueues any device work, so a failed call has no
+ *    side effects.  dit_last_error() returns a human-readable reason.
+ *  - Asynchronous device faults surface as DIT_ECUDA on the next call.
+ *  - The CALLER owns all device memory (weights, workspace, inputs, outputs);
+ *    the library never allocates device memory itself (NCCL internals aside).
+ *  - A context is bound to one GPU and is not thread-safe: serialise calls.
+ *  - Pointers documented "device" must be device-accessible; "host" pointers
+ *    are read synchronously during the call and may be reused afterwards.
+ *  - bf16 = IEEE bfloat16 stored as uint16; all matrices are row-major.
+ *  - No C++ exceptions cross this boundary.
+ */
+#ifndef DIT_H_
+#define DIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum {
+  DIT_OK = 0,
+  DIT_EINVAL = 1,     /* bad argument / malformed tensor                        */
+  DIT_ENOMEM = 2,     /* workspace too small                                   */
+  DIT_ECUDA = 3,      /* CUDA runtime error (sticky for async faults)          */
+  DIT_EEXIST = 4,     /* adapter id already registered (~DuplicateModelId)     */
+  DIT_ERANK = 5,      /* LoRA rank > cfg.max_rank                              */
+  DIT_ENOSPC = 6,     /* adapter pool full                                     */
+  DIT_ENOENT = 7,     /* unknown adapter id                                    */
+  DIT_EBATCH = 8,     /* B > B_max (~BatchExceedsMax)                          */
+  DIT_ESHAPE = 9,     /* tokens exceed the configured maxima / not shardable   */
+  DIT_EADAPTER = 10,  /* batch references an unregistered adapter              */
+  DIT_EALIAS = 11,    /* latents_out aliases latents_in (immutability) */
+  DIT_EPARALLEL = 12, /* world does not divide H, Nt, Ni (~ParallelismExceedsMax) */
+  DIT_ENCCL = 13,     /* NCCL error                                            */
+  DIT_ENOWEIGHTS = 14 /* dit_step before every base tensor was loaded          */
+};
+
+/* ------------------------------------------------------------------ config */
+/* Model + capacity description (Model.__init__ / load). */
+typedef struct dit_config {
+  int32_t hidden;          /* D (3072)                                            */
+  int32_t heads;           /* H (24); head dim d = D / H in {32, 64, 128}         */
+  int32_t depth_double;    /* L_d double-stream blocks (19)                        */
+  int32_t depth_single;    /* L_s single-stream blocks (38)                        */
+  int32_t in_channels;     /* C packed latent channels (64)                        */
+  int32_t txt_dim;         /* Ct text-embedding width (4096)                       */
+  int32_t pooled_dim;      /* Cp pooled width (768)                                */
+  int32_t mlp_ratio;       /* F = mlp_ratio * D (4)                                */
+  int32_t rope_axes[3];    /* RoPE dims per position axis, sum = d (16, 56, 56)    */
+  float rope_theta;        /* 10000                                                */
+  int32_t guidance_embed;  /* 1 = guidance MLP present (Flux-Dev)                  */
+  int32_t max_batch;       /* B_max requests per dit_step         */
+  int32_t max_img_tokens;  /* largest Ni (global, before sharding)                */
+  int32_t max_txt_tokens;  /* largest Nt (global, before sharding)                */
+  int32_t max_rank;        /* largest LoRA rank (<= 128)                          */
+  int32_t max_adapters;    /* adapter-pool slots (registered adapters)            */
+} dit_config;
+
+typedef struct dit_ctx dit_ctx;
+
+/* Device workspace bytes dit_create() needs for cfg at world size 1 (an upper
+ * bound for any world size).  Returns 0 on an invalid cfg. */
+size_t dit_workspace_bytes(const dit_config* cfg);
+
+/* Create a context on CUDA device `device`, carving activations, the adapter
+ * pool and the batch plan out of the caller-owned `workspace` (device,
+ * >= dit_workspace_bytes(cfg) bytes, 256-B aligned).  *out is set on success.
+ * Errors: DIT_EINVAL, DIT_ENOMEM, DIT_ECUDA. */
+int dit_create(const dit_config* cfg, int device, void* workspace, size_t ws_bytes,
+               dit_ctx** out);
+
+void dit_destroy(dit_ctx* ctx);
+
+/* Last error message of this context (or of the last failed dit_create when
+ * ctx is NULL).  Never NULL. */
+const char* dit_last_error(const dit_ctx* ctx);
+
+/* ----------------------------------------------------------------- weights */
+/* A named tensor handed across the boundary.  dtype: 0 = bf16 (the only one). */
+typedef struct dit_tensor {
+  const char* name;        /* e.g. "double.3.img.qkv.w" (synth.weight_manifest) */
+  const void* ptr;         /* device pointer                                    */
+  int32_t dtype;
+  int32_t rank;            /* 1 or 2                                            */
+  int64_t shape[4];
+} dit_tensor;
+
+/* load(): register the base weights.  Linear weights
+ * are [out][in] row-major (K-major), biases [out]; names and shapes are those
+ * of synth.weight_manifest(cfg).  BORROWED: must outlive the context and stay
+ * unchanged.  May be called several times (later tensors replace earlier).
+ * Errors: DIT_EINVAL (unknown name, wrong shape/dtype, duplicate in one call). */
+int dit_load_weights(dit_ctx* ctx, const dit_tensor* tensors, int n);
+
+/* ------------------------------------------------------------------- LoRA */
+/* add_patch(lora): copy adapter
+ * `adapter_id` into the pool, enqueued on `stream` (a cudaStream_t).
+ * tensors: "<module>.lora_A" [r][in] and "<module>.lora_B" [out][r] for every
+ * adapted linear (synth.lora_targets: double qkv/proj/fc1/fc2 per stream,
+ * single linear1/linear2).  Missing modules are treated as zero (no delta).
+ * Applied unmerged: y += scale * (x A^T) B^T (reading C9).
+ * Caller buffers may be freed once `stream` has synchronised.
+ * Errors: DIT_EEXIST, DIT_ERANK, DIT_ENOSPC, DIT_EINVAL. */
+int lora_register(dit_ctx* ctx, int32_t adapter_id, int32_t rank, float scale,
+                  const dit_tensor* tensors, int n, void* stream);
+
+/* rm_patch: waits for the adapter's last use, frees the slot.
+ * Errors: DIT_ENOENT. */
+int lora_unregister(dit_ctx* ctx, int32_t adapter_id);
+
+/* -------------------------------------------------------------- ControlNet */
+/* Deferred input "controlnet_inputs": register the
+ * residual of request `slot` of the NEXT dit_step for double block `block`:
+ * after that block, h_img[slot] += cn_scale[slot] * scale * residual.
+ * residual: device bf16 [Ni_local][D] row-major (this rank's image shard).
+ * ready: a cudaEvent_t recorded by the producer, or NULL if already
+ * resident.  The step does NOT wait at launch: the wait is enqueued right
+ * before block `block`'s consuming kernel ("returns immediately if the data is
+ * available, or blocks until the data arrives").
+ * BORROWED and immutable until that dit_step completes.
+ * Registrations apply to exactly one dit_step and are then cleared.
+ * Errors: DIT_EINVAL (slot >= B_max, block >= L_d, NULL residual). */
+int controlnet_inject(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
+                      float scale, void* ready_event);
+
+/* ------------------------------------------------------ sequence parallel */
+/* Parallelism descriptor: this context is rank `rank` of
+ * `world` GPUs running one dit_step together with Ulysses sequence
+ * parallelism.  nccl_unique_id: 128-byte ncclUniqueId (host), identical on all
+ * ranks (broadcast by the caller).  Collective: every rank must call it.
+ * world == 1 disables communication.  Shard layout (bit-exact):
+ * rank r owns, of every request, txt rows [r*Nt/P, (r+1)*Nt/P) and img rows
+ * [r*Ni/P, (r+1)*Ni/P); latents / txt / residuals are passed pre-sharded.
+ * Errors: DIT_EPARALLEL (world does not divide H), DIT_ENCCL, DIT_EINVAL. */
+int sp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_id);
+
+/* -------------------------------------------------------------------- step */
+typedef struct dit_batch {
+  int32_t batch;              /* B (1 .. B_max)                                  */
+  int32_t img_h, img_w;       /* packed latent grid; Ni = img_h * img_w (global) */
+  int32_t txt_tokens;         /* Nt (global)                                     */
+  const int32_t* adapter_id;  /* host [B]; -1 = base model                       */
+  const float* sigma;         /* host [B]; this step's sigma per request         */
+  const float* sigma_next;    /* host [B]                                        */
+  const float* guidance;      /* host [B] (Flux-Dev distilled guidance, 3.5)     */
+  const float* cn_scale;      /* host [B] ControlNet conditioning scale; NULL=1  */
+  const float* latents_in;    /* device fp32 [B][Ni/P][C]                        */
+  float* latents_out;         /* device fp32 [B][Ni/P][C]; must NOT alias input  */
+  const void* txt;            /* device bf16 [B][Nt/P][Ct]                       */
+  const void* pooled;         /* device bf16 [B][Cp]                             */
+  float* v_out;               /* device fp32 [B][Ni/P][C] noise_pred; nullable   */
+} dit_batch;
+
+/* execute() + denoise(): one flow-matching Euler step
+ * latents_out = latents_in + (sigma_next - sigma) * v for every request,
+ * asynchronously on `stream` (a cudaStream_t).  All pointers are borrowed.
+ * Errors: DIT_EBATCH, DIT_ESHAPE, DIT_EADAPTER, DIT_EALIAS, DIT_EINVAL,
+ * DIT_ENOWEIGHTS, DIT_ECUDA, DIT_ENCCL. */
+int dit_step(dit_ctx* ctx, const dit_batch* batch, void* stream);
+
+/* Algorithmic tensor FLOPs of one dit_step on `batch` (DESIGN.md §5 formula:
+ * projections 2MNK, attention 4 N^2 D per request-block, LoRA 2r(in+out)). */
+double dit_step_flops(const dit_ctx* ctx, const dit_batch* batch);
+
+/* Number of kernels the last dit_step launched (for bench.py gpu_launches). */
+int dit_last_launch_count(const dit_ctx* ctx);
+
+/* ---------------------------------------------------- test-only exports */
+/* Fill a device bf16 tensor of n elements with the synth counter generator
+ * (synth/__init__.py docstring): w = bf16(offset + (2u-1)*scale). */
+int dit_fill_synthetic(void* dst_bf16, int64_t n, uint64_t seed, uint64_t tensor_id,
+                       float scale, float offset, void* stream);
+
+/* Integer plan artefacts of `batch` (host outputs; bit-exact tests):
+ * row_adapter: int32 [rows] LoRA pool slot of each local row of the
+ *   txt-stream GEMM followed by the img-stream GEMM (-1 = none), rows =
+ *   B*(Nt/P) + B*(Ni/P).  Returns rows written, or -status. */
+int dit_debug_row_adapter(dit_ctx* ctx, const dit_batch* batch, int32_t* out, int cap);
+/* shard_map: int32 [B*(Nt/P + Ni/P)]: global joint token index (txt first,
+ * request-major: b*N + n) of every local row.  Returns rows, or -status. */
+int dit_debug_shard_map(dit_ctx* ctx, const dit_batch* batch, int32_t* out, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIT_H_ */

@@ -1,0 +1,1326 @@
+// dit_api.cpp -- host side of libdit: context, borrowed weights, adapter pool,
+// ControlNet slots, batch plan and the dit_step launch sequence (include/dit.h).
+//
+// dit_step = one LegoDiffusion model-execution node of the shared base model
+// over a cross-workflow batch plus
+// denoise().  Launch sequence per step:
+//   conditioning MLPs (skinny) -> ALL adaLN modulations (one skinny launch)
+//   -> img_in/txt_in (one grouped GEMM, EPI_STORE_H)
+//   -> 19 x double block: LN-mod(2 streams) -> [LoRA shrink] -> QKV GEMM
+//      (EPI_QKV) -> attention -> [shrink] proj (EPI_RESID) -> LN-mod ->
+//      [shrink] fc1 (EPI_GELU) -> [ControlNet wait] [shrink] fc2 (EPI_RESID+CN)
+//   -> 38 x single block: LN-mod -> [shrink] linear1 (EPI_QKV split GELU) ->
+//      attention -> [shrink] linear2 (EPI_RESID)
+//   -> final LN-mod -> final GEMM with the Euler update fused (EPI_FINAL).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/dit.h"
+#include "kernels.h"
+
+using namespace dit;
+typedef uint16_t bf16_t;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Lin {
+  const void* w = nullptr;
+  const void* b = nullptr;
+  int out = 0, in = 0;
+  CUtensorMap tm;  // weight [out][in], box {64, 256}
+};
+
+struct LoraPool {     // one adapted module
+  int in = 0, out = 0;
+  void* A = nullptr;  // bf16 [slots][r_alloc][in]
+  void* B = nullptr;  // bf16 [slots][out][r_alloc]
+  CUtensorMap tmA, tmB;
+};
+
+struct DoubleStream {
+  Lin mod, qkv, proj, fc1, fc2;
+  const void* qn = nullptr;
+  const void* kn = nullptr;
+  int lora[4];  // module index of qkv, proj, fc1, fc2
+};
+struct SingleBlk {
+  Lin mod, l1, l2;
+  const void* qn = nullptr;
+  const void* kn = nullptr;
+  int lora[2];
+};
+
+struct RowSpace {     // LoRA bookkeeping for one GEMM row space (txt, img or joint)
+  int M = 0, rows_per_req = 0, tiles_m = 0;
+  int* row_slot = nullptr;        // device [M]
+  int* tile_slots = nullptr;      // device [tiles_m][slot_cap]
+  int* tile_cnt = nullptr;        // device [tiles_m]
+  int2* shrink_list = nullptr;    // device [n_shrink]
+  int n_shrink = 0;
+  std::vector<int> h_row_slot;    // host copy (debug export)
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct dit_ctx {
+  dit_config cfg;
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  int D, H, d, F, C, Ct, Cp, Ld, Ls;
+  int Nmax, Rmax;
+  int r_alloc;
+  int mod_total;
+  // weights
+  std::map<std::string, dit_tensor> tensors;
+  bool weights_ready = false;
+  Lin img_in, txt_in, t_in, t_out, g_in, g_out, y_in, y_out, fin_mod, fin_lin;
+  std::vector<DoubleStream> dbl[2];  // [stream][block], stream 0 = img, 1 = txt
+  std::vector<SingleBlk> sgl;
+  // adapter pool
+  std::vector<LoraPool> pools;
+  std::map<int, int> adapter_slot;      // adapter id -> pool slot
+  std::vector<float> slot_scale_h;
+  std::vector<cudaEvent_t> slot_last_use;
+  // ControlNet registrations for the next step
+  struct CnReg { const void* ptr; float scale; cudaEvent_t ready; };
+  std::map<std::pair<int, int>, CnReg> cn;   // (slot, block)
+  // SP
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  // workspace carve-outs
+  float* h = nullptr;
+  bf16_t* u = nullptr;
+  bf16_t* q = nullptr;
+  bf16_t* k = nullptr;
+  bf16_t* v = nullptr;
+  bf16_t* o = nullptr;
+  bf16_t* cat = nullptr;
+  bf16_t* sext = nullptr;
+  bf16_t* xb = nullptr;
+  float2* rope = nullptr;
+  float* mod = nullptr;
+  float* vec = nullptr;
+  float* h1 = nullptr;
+  bf16_t* xprep = nullptr;
+  bf16_t* temb = nullptr;
+  SkinnySeg* segs = nullptr;
+  int nsegs = 0, seg_rows = 0;
+  bool segs_dirty = true;
+  // per-step device params
+  float* p_dsig = nullptr;
+  float* p_cn_scale = nullptr;
+  float* p_sigma = nullptr;
+  float* p_guid = nullptr;
+  const void** p_cn_ptr = nullptr;   // [Ld][B_max]
+  float* p_slot_scale = nullptr;     // [max_adapters]
+  float* p_cn_kappa = nullptr;       // [Ld][8] cn_scale_b * inject scale
+  RowSpace rs[3];                    // 0 txt stream, 1 img stream, 2 joint
+  int slot_cap = 1;
+  // plan cache key
+  int plan_B = -1, plan_h = -1, plan_w = -1, plan_nt = -1;
+  std::vector<int> plan_slots;
+  int rope_key[3] = {-1, -1, -1};
+  int last_launches = 0;
+  int launches = 0;
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+};
+
+// ------------------------------------------------------------------ sizes
+namespace {
+
+struct Carve {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  }
+};
+
+int n_lora_modules(const dit_config& c) { return c.depth_double * 2 * 4 + c.depth_single * 2; }
+
+bool cfg_valid(const dit_config* c, std::string* why) {
+  auto bad = [&](const char* s) { if (why) *why = s; return false; };
+  if (!c) return bad("cfg is NULL");
+  if (c->hidden <= 0 || c->heads <= 0 || c->hidden % c->heads) return bad("hidden must be a positive multiple of heads");
+  int d = c->hidden / c->heads;
+  if (d != 32 && d != 64 && d != 128) return bad("head dim must be 32, 64 or 128");
+  if (c->hidden % 64) return bad("hidden must be a multiple of 64");
+  if (c->hidden > 3072 * 1) { if (c->hidden / 4 > 24 * 32) return bad("hidden > 3072 unsupported"); }
+  if (c->rope_axes[0] + c->rope_axes[1] + c->rope_axes[2] != d) return bad("rope axes must sum to head dim");
+  if (c->rope_axes[0] % 2 || c->rope_axes[1] % 2 || c->rope_axes[2] % 2) return bad("rope axes must be even");
+  if (c->depth_double < 0 || c->depth_single < 0) return bad("negative depth");
+  if (c->in_channels <= 0 || c->in_channels % 8) return bad("in_channels must be a positive multiple of 8");
+  if (c->txt_dim <= 0 || c->txt_dim % 8) return bad("txt_dim must be a positive multiple of 8");
+  if (c->pooled_dim <= 0 || c->pooled_dim % 8) return bad("pooled_dim must be a positive multiple of 8");
+  if (c->mlp_ratio <= 0) return bad("mlp_ratio must be positive");
+  if (c->max_batch < 1 || c->max_batch > 8) return bad("max_batch must be in [1, 8]");
+  if (c->max_img_tokens < 1 || c->max_txt_tokens < 1) return bad("token maxima must be positive");
+  if (c->max_rank < 0 || c->max_rank > 128) return bad("max_rank must be in [0, 128]");
+  if (c->max_adapters < 0 || c->max_adapters > 64) return bad("max_adapters must be in [0, 64]");
+  return true;
+}
+
+struct Layout {
+  size_t h, u, q, k, v, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, total;
+  size_t pool_bytes_per_slot;
+};
+
+Layout layout_of(const dit_config& c) {
+  Layout L{};
+  const size_t D = c.hidden, F = (size_t)c.mlp_ratio * c.hidden, d = D / c.heads;
+  const size_t N = (size_t)c.max_img_tokens + c.max_txt_tokens;
+  const size_t R = (size_t)c.max_batch * N;
+  const size_t r_alloc = c.max_rank > 0 ? align_up(c.max_rank, 64) : 0;
+  const size_t mod_total = 12 * D * c.depth_double + 3 * D * c.depth_single + 2 * D;
+  const size_t nseg = 2 * c.depth_double + c.depth_single + 1;
+  const size_t tiles = (R + GEMM_BM - 1) / GEMM_BM + 4;
+  Carve cv;
+  L.h = cv.take(R * D * 4);
+  L.u = cv.take(R * D * 2);
+  L.q = cv.take(R * D * 2);
+  L.k = cv.take(R * D * 2);
+  L.v = cv.take(R * D * 2);
+  L.o = cv.take(R * D * 2);
+  L.cat = cv.take(R * (D + F) * 2);
+  L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
+  L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
+  L.rope = cv.take(N * (d / 2) * 8);
+  L.mod = cv.take(8 * mod_total * 4);
+  L.vec = cv.take(8 * D * 4);
+  L.h1 = cv.take(8 * D * 4);
+  L.xprep = cv.take(8 * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
+  L.temb = cv.take(8 * 256 * 2);
+  L.segs = cv.take((nseg + 6) * sizeof(SkinnySeg));
+  L.params = cv.take(4096 + (size_t)std::max(c.depth_double, 1) * 8 * (sizeof(void*) + 4) + 2048);
+  L.rowspace = cv.take(3 * (R * 4 + tiles * 8 * 4 + tiles * 4 + tiles * 8 * 8) + 3 * 1024);
+  size_t per_slot = 0;
+  if (c.max_adapters > 0 && r_alloc > 0) {
+    auto add = [&](size_t in, size_t out) { per_slot += r_alloc * in * 2 + out * r_alloc * 2; };
+    for (int i = 0; i < c.depth_double * 2; ++i) { add(D, 3 * D); add(D, D); add(D, F); add(F, D); }
+    for (int j = 0; j < c.depth_single; ++j) { add(D, 3 * D + F); add(D + F, D); }
+  }
+  L.pool_bytes_per_slot = per_slot;
+  L.pools = cv.take(per_slot * c.max_adapters + n_lora_modules(c) * 2 * 256);
+  L.total = cv.off;
+  return L;
+}
+
+}  // namespace
+
+extern "C" size_t dit_workspace_bytes(const dit_config* cfg) {
+  if (!cfg_valid(cfg, nullptr)) return 0;
+  return layout_of(*cfg).total;
+}
+
+// ------------------------------------------------------------------ create / destroy
+extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, size_t ws_bytes, dit_ctx** out) {
+  std::string why;
+  if (!out) { g_create_error = "out is NULL"; return DIT_EINVAL; }
+  *out = nullptr;
+  if (!cfg_valid(cfg, &why)) { g_create_error = why; return DIT_EINVAL; }
+  Layout L = layout_of(*cfg);
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
+    g_create_error = "workspace must be a non-NULL 256-byte aligned device pointer";
+    return DIT_EINVAL;
+  }
+  if (ws_bytes < L.total) {
+    g_create_error = "workspace too small: need " + std::to_string(L.total) + " bytes";
+    return DIT_ENOMEM;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) { g_create_error = "cudaSetDevice failed"; return DIT_ECUDA; }
+  dit_ctx* c = new dit_ctx();
+  c->cfg = *cfg;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  c->ws = static_cast<uint8_t*>(workspace);
+  c->ws_bytes = ws_bytes;
+  c->D = cfg->hidden;
+  c->H = cfg->heads;
+  c->d = c->D / c->H;
+  c->F = cfg->mlp_ratio * c->D;
+  c->C = cfg->in_channels;
+  c->Ct = cfg->txt_dim;
+  c->Cp = cfg->pooled_dim;
+  c->Ld = cfg->depth_double;
+  c->Ls = cfg->depth_single;
+  c->Nmax = cfg->max_img_tokens + cfg->max_txt_tokens;
+  c->Rmax = cfg->max_batch * c->Nmax;
+  c->r_alloc = cfg->max_rank > 0 ? (int)align_up(cfg->max_rank, 64) : 64;
+  c->mod_total = 12 * c->D * c->Ld + 3 * c->D * c->Ls + 2 * c->D;
+  uint8_t* w = c->ws;
+  c->h = reinterpret_cast<float*>(w + L.h);
+  c->u = reinterpret_cast<bf16_t*>(w + L.u);
+  c->q = reinterpret_cast<bf16_t*>(w + L.q);
+  c->k = reinterpret_cast<bf16_t*>(w + L.k);
+  c->v = reinterpret_cast<bf16_t*>(w + L.v);
+  c->o = reinterpret_cast<bf16_t*>(w + L.o);
+  c->cat = reinterpret_cast<bf16_t*>(w + L.cat);
+  c->sext = reinterpret_cast<bf16_t*>(w + L.sext);
+  c->xb = reinterpret_cast<bf16_t*>(w + L.xb);
+  c->rope = reinterpret_cast<float2*>(w + L.rope);
+  c->mod = reinterpret_cast<float*>(w + L.mod);
+  c->vec = reinterpret_cast<float*>(w + L.vec);
+  c->h1 = reinterpret_cast<float*>(w + L.h1);
+  c->xprep = reinterpret_cast<bf16_t*>(w + L.xprep);
+  c->temb = reinterpret_cast<bf16_t*>(w + L.temb);
+  c->segs = reinterpret_cast<SkinnySeg*>(w + L.segs);
+  {
+    Carve cv;
+    uint8_t* p = w + L.params;
+    c->p_dsig = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_cn_scale = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_sigma = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_guid = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_slot_scale = reinterpret_cast<float*>(p + cv.take(64 * 4));
+    c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take((size_t)std::max(c->Ld, 1) * 8 * sizeof(void*)));
+    c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take((size_t)std::max(c->Ld, 1) * 8 * 4));
+  }
+  {
+    const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
+    Carve cv;
+    uint8_t* p = w + L.rowspace;
+    for (int s = 0; s < 3; ++s) {
+      c->rs[s].row_slot = reinterpret_cast<int*>(p + cv.take(c->Rmax * 4));
+      c->rs[s].tile_slots = reinterpret_cast<int*>(p + cv.take(tiles * 8 * 4));
+      c->rs[s].tile_cnt = reinterpret_cast<int*>(p + cv.take(tiles * 4));
+      c->rs[s].shrink_list = reinterpret_cast<int2*>(p + cv.take(tiles * 8 * 8));
+    }
+  }
+  c->slot_cap = cfg->max_batch;
+  // adapter pools
+  const int nmod = n_lora_modules(*cfg);
+  c->pools.resize(nmod);
+  {
+    size_t off = L.pools;
+    int mi = 0;
+    const int D = c->D, F = c->F;
+    auto add = [&](int in, int out) {
+      LoraPool& P = c->pools[mi++];
+      P.in = in;
+      P.out = out;
+      if (cfg->max_adapters > 0 && cfg->max_rank > 0) {
+        P.A = w + off;
+        off = align_up(off + (size_t)cfg->max_adapters * c->r_alloc * in * 2, 256);
+        P.B = w + off;
+        off = align_up(off + (size_t)cfg->max_adapters * out * c->r_alloc * 2, 256);
+        // A pool viewed [slots*r_alloc][in]; B pool viewed [slots*out][r_alloc]
+        make_tmap_2d(&P.tmA, P.A, in, (uint64_t)cfg->max_adapters * c->r_alloc, (uint64_t)in * 2, 64, GEMM_BN);
+        make_tmap_2d(&P.tmB, P.B, c->r_alloc, (uint64_t)cfg->max_adapters * out, (uint64_t)c->r_alloc * 2, 64,
+                     GEMM_BN);
+      }
+    };
+    for (int i = 0; i < c->Ld; ++i)
+      for (int s = 0; s < 2; ++s) { add(D, 3 * D); add(D, D); add(D, F); add(F, D); }
+    for (int j = 0; j < c->Ls; ++j) { add(D, 3 * D + F); add(D + F, D); }
+  }
+  c->slot_scale_h.assign(std::max(cfg->max_adapters, 1), 0.f);
+  c->slot_last_use.assign(std::max(cfg->max_adapters, 1), nullptr);
+  for (auto& e : c->slot_last_use) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  c->dbl[0].resize(c->Ld);
+  c->dbl[1].resize(c->Ld);
+  c->sgl.resize(c->Ls);
+  {
+    int mi = 0;
+    for (int i = 0; i < c->Ld; ++i)
+      for (int s = 0; s < 2; ++s)
+        for (int t = 0; t < 4; ++t) c->dbl[s][i].lora[t] = mi++;
+    for (int j = 0; j < c->Ls; ++j)
+      for (int t = 0; t < 2; ++t) c->sgl[j].lora[t] = mi++;
+  }
+  if (cudaGetLastError() != cudaSuccess) {
+    g_create_error = "CUDA error during context creation";
+    delete c;
+    return DIT_ECUDA;
+  }
+  *out = c;
+  return DIT_OK;
+}
+
+extern "C" void dit_destroy(dit_ctx* c) {
+  if (!c) return;
+  for (auto& e : c->slot_last_use)
+    if (e) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+extern "C" const char* dit_last_error(const dit_ctx* c) {
+  if (!c) return g_create_error.c_str();
+  return c->err.c_str();
+}
+
+// ------------------------------------------------------------------ weights
+namespace {
+
+struct Expect {
+  std::string name;
+  int64_t s0, s1;   // s1 = -1 for rank-1
+};
+
+void expected_tensors(const dit_ctx* c, std::vector<Expect>& e) {
+  const int D = c->D, C = c->C, Ct = c->Ct, Cp = c->Cp, F = c->F, d = c->d;
+  auto lin = [&](const std::string& n, int out, int in) {
+    e.push_back({n + ".w", out, in});
+    e.push_back({n + ".b", out, -1});
+  };
+  lin("img_in", D, C);
+  lin("txt_in", D, Ct);
+  lin("time_in.in", D, 256);
+  lin("time_in.out", D, D);
+  if (c->cfg.guidance_embed) { lin("guidance_in.in", D, 256); lin("guidance_in.out", D, D); }
+  lin("vector_in.in", D, Cp);
+  lin("vector_in.out", D, D);
+  for (int i = 0; i < c->Ld; ++i)
+    for (const char* s : {"img", "txt"}) {
+      std::string p = "double." + std::to_string(i) + "." + s + ".";
+      lin(p + "mod", 6 * D, D);
+      lin(p + "qkv", 3 * D, D);
+      e.push_back({p + "q_norm", d, -1});
+      e.push_back({p + "k_norm", d, -1});
+      lin(p + "proj", D, D);
+      lin(p + "fc1", F, D);
+      lin(p + "fc2", D, F);
+    }
+  for (int j = 0; j < c->Ls; ++j) {
+    std::string p = "single." + std::to_string(j) + ".";
+    lin(p + "mod", 3 * D, D);
+    lin(p + "linear1", 3 * D + F, D);
+    e.push_back({p + "q_norm", d, -1});
+    e.push_back({p + "k_norm", d, -1});
+    lin(p + "linear2", D, D + F);
+  }
+  lin("final.mod", 2 * D, D);
+  lin("final.linear", C, D);
+}
+
+bool bind_lin(dit_ctx* c, Lin& L, const std::string& name) {
+  auto w = c->tensors.find(name + ".w");
+  auto b = c->tensors.find(name + ".b");
+  if (w == c->tensors.end() || b == c->tensors.end()) return false;
+  L.w = w->second.ptr;
+  L.b = b->second.ptr;
+  L.out = (int)w->second.shape[0];
+  L.in = (int)w->second.shape[1];
+  return make_tmap_2d(&L.tm, L.w, L.in, L.out, (uint64_t)L.in * 2, 64, GEMM_BN);
+}
+
+int bind_all(dit_ctx* c) {
+  std::vector<Expect> ex;
+  expected_tensors(c, ex);
+  for (auto& e : ex)
+    if (!c->tensors.count(e.name)) return 0;
+  bool ok = true;
+  ok &= bind_lin(c, c->img_in, "img_in");
+  ok &= bind_lin(c, c->txt_in, "txt_in");
+  ok &= bind_lin(c, c->t_in, "time_in.in");
+  ok &= bind_lin(c, c->t_out, "time_in.out");
+  if (c->cfg.guidance_embed) {
+    ok &= bind_lin(c, c->g_in, "guidance_in.in");
+    ok &= bind_lin(c, c->g_out, "guidance_in.out");
+  }
+  ok &= bind_lin(c, c->y_in, "vector_in.in");
+  ok &= bind_lin(c, c->y_out, "vector_in.out");
+  for (int i = 0; i < c->Ld; ++i)
+    for (int s = 0; s < 2; ++s) {
+      std::string p = "double." + std::to_string(i) + (s == 0 ? ".img." : ".txt.");
+      DoubleStream& B = c->dbl[s][i];
+      ok &= bind_lin(c, B.mod, p + "mod");
+      ok &= bind_lin(c, B.qkv, p + "qkv");
+      ok &= bind_lin(c, B.proj, p + "proj");
+      ok &= bind_lin(c, B.fc1, p + "fc1");
+      ok &= bind_lin(c, B.fc2, p + "fc2");
+      B.qn = c->tensors[p + "q_norm"].ptr;
+      B.kn = c->tensors[p + "k_norm"].ptr;
+    }
+  for (int j = 0; j < c->Ls; ++j) {
+    std::string p = "single." + std::to_string(j) + ".";
+    SingleBlk& S = c->sgl[j];
+    ok &= bind_lin(c, S.mod, p + "mod");
+    ok &= bind_lin(c, S.l1, p + "linear1");
+    ok &= bind_lin(c, S.l2, p + "linear2");
+    S.qn = c->tensors[p + "q_norm"].ptr;
+    S.kn = c->tensors[p + "k_norm"].ptr;
+  }
+  ok &= bind_lin(c, c->fin_mod, "final.mod");
+  ok &= bind_lin(c, c->fin_lin, "final.linear");
+  return ok ? 1 : -1;
+}
+
+}  // namespace
+
+extern "C" int dit_load_weights(dit_ctx* c, const dit_tensor* t, int n) {
+  if (!c) return DIT_EINVAL;
+  if (n < 0 || (n > 0 && !t)) return c->fail(DIT_EINVAL, "bad tensor list");
+  std::vector<Expect> ex;
+  expected_tensors(c, ex);
+  std::map<std::string, Expect> want;
+  for (auto& e : ex) want[e.name] = e;
+  std::map<std::string, int> seen;
+  for (int i = 0; i < n; ++i) {
+    if (!t[i].name) return c->fail(DIT_EINVAL, "tensor %d has no name", i);
+    auto it = want.find(t[i].name);
+    if (it == want.end()) return c->fail(DIT_EINVAL, "unknown tensor '%s'", t[i].name);
+    if (seen.count(t[i].name)) return c->fail(DIT_EINVAL, "duplicate tensor '%s'", t[i].name);
+    seen[t[i].name] = 1;
+    if (t[i].dtype != 0) return c->fail(DIT_EINVAL, "tensor '%s': dtype must be bf16 (0)", t[i].name);
+    if (!t[i].ptr || (reinterpret_cast<uintptr_t>(t[i].ptr) & 15))
+      return c->fail(DIT_EINVAL, "tensor '%s': NULL or not 16-byte aligned", t[i].name);
+    const Expect& e = it->second;
+    const bool r1 = e.s1 < 0;
+    if ((r1 && (t[i].rank != 1 || t[i].shape[0] != e.s0)) ||
+        (!r1 && (t[i].rank != 2 || t[i].shape[0] != e.s0 || t[i].shape[1] != e.s1)))
+      return c->fail(DIT_EINVAL, "tensor '%s': wrong shape", t[i].name);
+  }
+  for (int i = 0; i < n; ++i) {
+    dit_tensor copy = t[i];
+    c->tensors[t[i].name] = copy;
+    c->tensors[t[i].name].name = nullptr;
+  }
+  int r = bind_all(c);
+  if (r < 0) return c->fail(DIT_ECUDA, "tensor map encoding failed");
+  c->weights_ready = (r == 1);
+  c->segs_dirty = true;
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ LoRA registry
+extern "C" int lora_register(dit_ctx* c, int32_t adapter_id, int32_t rank, float scale, const dit_tensor* t, int n,
+                             void* stream) {
+  if (!c) return DIT_EINVAL;
+  if (adapter_id < 0) return c->fail(DIT_EINVAL, "adapter id must be >= 0");
+  if (c->adapter_slot.count(adapter_id)) return c->fail(DIT_EEXIST, "adapter %d already registered", adapter_id);
+  if (rank <= 0 || rank > c->cfg.max_rank) return c->fail(DIT_ERANK, "rank %d not in [1, %d]", rank, c->cfg.max_rank);
+  if (!std::isfinite(scale)) return c->fail(DIT_EINVAL, "scale must be finite");
+  if (n < 0 || (n > 0 && !t)) return c->fail(DIT_EINVAL, "bad tensor list");
+  int slot = -1;
+  for (int s = 0; s < c->cfg.max_adapters; ++s) {
+    bool used = false;
+    for (auto& kv : c->adapter_slot)
+      if (kv.second == s) used = true;
+    if (!used) { slot = s; break; }
+  }
+  if (slot < 0) return c->fail(DIT_ENOSPC, "adapter pool full (%d slots)", c->cfg.max_adapters);
+  // module name -> index
+  std::map<std::string, int> modidx;
+  for (int i = 0; i < c->Ld; ++i)
+    for (int s = 0; s < 2; ++s) {
+      const char* names[4] = {"qkv", "proj", "fc1", "fc2"};
+      for (int q = 0; q < 4; ++q)
+        modidx["double." + std::to_string(i) + (s == 0 ? ".img." : ".txt.") + names[q]] = c->dbl[s][i].lora[q];
+    }
+  for (int j = 0; j < c->Ls; ++j) {
+    modidx["single." + std::to_string(j) + ".linear1"] = c->sgl[j].lora[0];
+    modidx["single." + std::to_string(j) + ".linear2"] = c->sgl[j].lora[1];
+  }
+  struct Job { int mod; bool isA; const dit_tensor* t; };
+  std::vector<Job> jobs;
+  std::map<std::string, int> seen;
+  for (int i = 0; i < n; ++i) {
+    if (!t[i].name || !t[i].ptr) return c->fail(DIT_EINVAL, "tensor %d: NULL name or pointer", i);
+    std::string nm = t[i].name;
+    bool isA;
+    std::string mod;
+    if (nm.size() > 7 && nm.compare(nm.size() - 7, 7, ".lora_A") == 0) { isA = true; mod = nm.substr(0, nm.size() - 7); }
+    else if (nm.size() > 7 && nm.compare(nm.size() - 7, 7, ".lora_B") == 0) { isA = false; mod = nm.substr(0, nm.size() - 7); }
+    else return c->fail(DIT_EINVAL, "tensor '%s' is not <module>.lora_A/B", t[i].name);
+    auto it = modidx.find(mod);
+    if (it == modidx.end()) return c->fail(DIT_EINVAL, "'%s' is not an adapted module", mod.c_str());
+    if (seen.count(nm)) return c->fail(DIT_EINVAL, "duplicate tensor '%s'", t[i].name);
+    seen[nm] = 1;
+    const LoraPool& P = c->pools[it->second];
+    if (t[i].dtype != 0 || t[i].rank != 2) return c->fail(DIT_EINVAL, "'%s': must be a rank-2 bf16 tensor", t[i].name);
+    if (isA && (t[i].shape[0] != rank || t[i].shape[1] != P.in))
+      return c->fail(DIT_EINVAL, "'%s': expected [%d][%d]", t[i].name, rank, P.in);
+    if (!isA && (t[i].shape[0] != P.out || t[i].shape[1] != rank))
+      return c->fail(DIT_EINVAL, "'%s': expected [%d][%d]", t[i].name, P.out, rank);
+    jobs.push_back({it->second, isA, &t[i]});
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ra = c->r_alloc;
+  // zero the whole slot of every module, then copy the given matrices
+  for (auto& P : c->pools) {
+    cudaMemsetAsync(static_cast<uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2, 0, (size_t)ra * P.in * 2, s);
+    cudaMemsetAsync(static_cast<uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, 0, (size_t)P.out * ra * 2, s);
+  }
+  for (auto& j : jobs) {
+    LoraPool& P = c->pools[j.mod];
+    if (j.isA) {
+      cudaMemcpyAsync(static_cast<uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2, j.t->ptr, (size_t)rank * P.in * 2,
+                      cudaMemcpyDeviceToDevice, s);
+    } else {
+      cudaMemcpy2DAsync(static_cast<uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, (size_t)ra * 2, j.t->ptr,
+                        (size_t)rank * 2, (size_t)rank * 2, P.out, cudaMemcpyDeviceToDevice, s);
+    }
+  }
+  if (cudaGetLastError() != cudaSuccess) return c->fail(DIT_ECUDA, "adapter copy failed");
+  c->adapter_slot[adapter_id] = slot;
+  c->slot_scale_h[slot] = scale;
+  c->plan_B = -1;  // slot tables may change
+  return DIT_OK;
+}
+
+extern "C" int lora_unregister(dit_ctx* c, int32_t adapter_id) {
+  if (!c) return DIT_EINVAL;
+  auto it = c->adapter_slot.find(adapter_id);
+  if (it == c->adapter_slot.end()) return c->fail(DIT_ENOENT, "adapter %d not registered", adapter_id);
+  cudaEventSynchronize(c->slot_last_use[it->second]);
+  c->adapter_slot.erase(it);
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ ControlNet
+extern "C" int controlnet_inject(dit_ctx* c, int32_t slot, int32_t block, const void* residual, float scale,
+                                 void* ready) {
+  if (!c) return DIT_EINVAL;
+  if (slot < 0 || slot >= c->cfg.max_batch) return c->fail(DIT_EINVAL, "slot %d not in [0, %d)", slot, c->cfg.max_batch);
+  if (block < 0 || block >= c->Ld) return c->fail(DIT_EINVAL, "block %d not in [0, %d)", block, c->Ld);
+  if (!residual || (reinterpret_cast<uintptr_t>(residual) & 15))
+    return c->fail(DIT_EINVAL, "residual must be a non-NULL 16-byte aligned device pointer");
+  if (!std::isfinite(scale)) return c->fail(DIT_EINVAL, "scale must be finite");
+  c->cn[{slot, block}] = {residual, scale, reinterpret_cast<cudaEvent_t>(ready)};
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ SP
+extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
+  if (!c) return DIT_EINVAL;
+  if (world < 1 || rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad world/rank %d/%d", world, rank);
+  if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
+  if (world == 1) {
+    c->world = 1;
+    c->rank = 0;
+    return DIT_OK;
+  }
+  if (!uid) return c->fail(DIT_EINVAL, "nccl unique id is NULL");
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  cudaSetDevice(c->device);
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->comm = comm;
+  c->world = world;
+  c->rank = rank;
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ plan
+namespace {
+
+int build_rowspace(dit_ctx* c, RowSpace& R, int M, int rows_per_req, const std::vector<int>& req_slot,
+                   std::vector<int>& h_tiles, std::vector<int>& h_cnt, std::vector<int2>& h_shrink) {
+  R.M = M;
+  R.rows_per_req = rows_per_req;
+  R.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  R.h_row_slot.assign(M, -1);
+  for (int r = 0; r < M; ++r) R.h_row_slot[r] = req_slot[r / rows_per_req];
+  h_tiles.assign((size_t)R.tiles_m * c->slot_cap, 0);
+  h_cnt.assign(R.tiles_m, 0);
+  h_shrink.clear();
+  for (int m = 0; m < R.tiles_m; ++m) {
+    std::vector<int> sl;
+    for (int r = m * GEMM_BM; r < std::min(M, (m + 1) * GEMM_BM); ++r) {
+      int s = R.h_row_slot[r];
+      if (s >= 0 && std::find(sl.begin(), sl.end(), s) == sl.end()) sl.push_back(s);
+    }
+    std::sort(sl.begin(), sl.end());
+    if ((int)sl.size() > c->slot_cap) return -1;
+    h_cnt[m] = (int)sl.size();
+    for (size_t i = 0; i < sl.size(); ++i) {
+      h_tiles[(size_t)m * c->slot_cap + i] = sl[i];
+      h_shrink.push_back(make_int2(m, sl[i]));
+    }
+  }
+  R.n_shrink = (int)h_shrink.size();
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ GEMM helpers
+namespace {
+
+GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const Lin& W, const EpiParams& epi) {
+  GemmProblem P;
+  memset(&P, 0, sizeof(P));
+  make_tmap_2d(&P.tmA, A, K, M, (uint64_t)lda * 2, 64, GEMM_BM);
+  P.tmB = W.tm;
+  P.M = M;
+  P.N = W.out;
+  P.K = K;
+  P.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  P.tiles_n = (P.N + GEMM_BN - 1) / GEMM_BN;
+  P.num_tiles = P.tiles_m * P.tiles_n;
+  P.epi = epi;
+  P.slot_cap = c->slot_cap;
+  return P;
+}
+
+void add_lora_ext(dit_ctx* c, GemmProblem& P, const RowSpace& R, int module) {
+  if (R.n_shrink == 0 || c->pools.empty() || !c->pools[module].A) return;
+  const int nslots = std::max(c->cfg.max_adapters, 1);
+  make_tmap_2d(&P.tmAx, c->sext, (uint64_t)nslots * c->r_alloc, P.M, (uint64_t)nslots * c->r_alloc * 2, 64, GEMM_BM);
+  P.tmBx = c->pools[module].tmB;
+  P.tile_slots = R.tile_slots;
+  P.tile_slot_cnt = R.tile_cnt;
+  P.ext_kblocks = c->r_alloc / 64;
+  P.epi.r_alloc = c->r_alloc;
+}
+
+GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, const RowSpace& R, int module) {
+  GemmProblem P;
+  memset(&P, 0, sizeof(P));
+  const LoraPool& L = c->pools[module];
+  const int nslots = std::max(c->cfg.max_adapters, 1);
+  make_tmap_2d(&P.tmA, A, K, M, (uint64_t)lda * 2, 64, GEMM_BM);
+  P.tmB = L.tmA;
+  P.M = M;
+  P.N = c->r_alloc;
+  P.K = K;
+  P.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  P.tiles_n = 1;
+  P.num_tiles = R.n_shrink;
+  P.shrink = 1;
+  P.shrink_list = R.shrink_list;
+  P.epi.kind = EPI_SHRINK;
+  P.epi.out = c->sext;
+  P.epi.ld_out = nslots * c->r_alloc;
+  P.epi.row_slot = R.row_slot;
+  P.epi.slot_scale = c->p_slot_scale;
+  P.epi.r_alloc = c->r_alloc;
+  P.epi.rows_per_req = R.rows_per_req;
+  P.epi.joint_n = 1;
+  return P;
+}
+
+int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  int t = 0;
+  int k = 0;
+  for (int i = 0; i < np; ++i) {
+    if (probs[i].num_tiles <= 0 || probs[i].M <= 0) continue;
+    a.p[k] = probs[i];
+    a.p[k].tile_begin = t;
+    t += probs[i].num_tiles;
+    ++k;
+  }
+  a.num_problems = k;
+  a.total_tiles = t;
+  if (t == 0) return DIT_OK;
+  cudaError_t e = gemm_launch(a, c->num_sms, s);
+  c->launches++;
+  if (e != cudaSuccess) return c->fail(DIT_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
+  return DIT_OK;
+}
+
+// LoRA shrink for up to two (A, rowspace, module) triples, as one launch.
+int run_shrink(dit_ctx* c, int np, const void* const* A, const int* M, const int* K, const int* lda,
+               const RowSpace* const* R, const int* module, cudaStream_t s) {
+  GemmProblem p[2];
+  int k = 0;
+  for (int i = 0; i < np; ++i)
+    if (R[i]->n_shrink > 0 && c->pools[module[i]].A) p[k++] = shrink_problem(c, A[i], M[i], K[i], lda[i], *R[i], module[i]);
+  if (k == 0) return DIT_OK;
+  return run_gemm(c, p, k, s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ step
+extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
+  if (!c || !b) return 0.0;
+  const double B = b->batch, Ni = (double)b->img_h * b->img_w, Nt = b->txt_tokens, N = Ni + Nt;
+  const double D = c->D, F = c->F, C = c->C, Ct = c->Ct;
+  double f = 0;
+  // embedders (the conditioning MLPs are included as 2MNK with M = B)
+  f += 2 * B * Ni * D * C + 2 * B * Nt * D * Ct;
+  // double blocks: qkv, proj, fc1, fc2 per stream + attention
+  f += c->Ld * (2 * B * N * D * (3 * D) + 2 * B * N * D * D + 2 * 2 * B * N * D * F + 4 * B * N * N * D);
+  // single blocks
+  f += c->Ls * (2 * B * N * D * (3 * D + F) + 2 * B * N * (D + F) * D + 4 * B * N * N * D);
+  // final
+  f += 2 * B * Ni * D * C;
+  // LoRA: 2 r (in + out) per row per adapted linear, rows of adapted requests only
+  for (int i = 0; i < b->batch; ++i) {
+    int aid = b->adapter_id ? b->adapter_id[i] : -1;
+    if (aid < 0) continue;
+    double r = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
+    f += c->Ld * 2 * r * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
+    f += c->Ls * 2 * r * N * ((D + 3 * D + F) + (D + F + D));
+  }
+  return f;
+}
+
+extern "C" int dit_last_launch_count(const dit_ctx* c) { return c ? c->last_launches : 0; }
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    int _r = (x);                                                                    \
+    if (_r != DIT_OK) return _r;                                                     \
+  } while (0)
+#define CKC(x)                                                                       \
+  do {                                                                               \
+    cudaError_t _e = (x);                                                            \
+    c->launches++;                                                                   \
+    if (_e != cudaSuccess) return c->fail(DIT_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
+  if (!c) return DIT_EINVAL;
+  if (!b) return c->fail(DIT_EINVAL, "batch is NULL");
+  if (!c->weights_ready) return c->fail(DIT_ENOWEIGHTS, "base weights not (fully) loaded");
+  const int B = b->batch;
+  if (B < 1 || B > c->cfg.max_batch) return c->fail(DIT_EBATCH, "batch %d not in [1, %d]", B, c->cfg.max_batch);
+  if (b->img_h < 1 || b->img_w < 1 || b->txt_tokens < 1) return c->fail(DIT_ESHAPE, "empty token grid");
+  const int Ni = b->img_h * b->img_w, Nt = b->txt_tokens;
+  if (Ni > c->cfg.max_img_tokens || Nt > c->cfg.max_txt_tokens)
+    return c->fail(DIT_ESHAPE, "tokens (%d img, %d txt) exceed the configured maxima", Ni, Nt);
+  const int P = c->world;
+  if (Ni % P || Nt % P) return c->fail(DIT_EPARALLEL, "world %d does not divide Ni=%d / Nt=%d", P, Ni, Nt);
+  if (P > 1) return c->fail(DIT_EPARALLEL, "sequence parallel step not built yet");
+  if (!b->adapter_id || !b->sigma || !b->sigma_next || !b->guidance)
+    return c->fail(DIT_EINVAL, "host arrays adapter_id/sigma/sigma_next/guidance required");
+  if (!b->latents_in || !b->latents_out || !b->txt || !b->pooled) return c->fail(DIT_EINVAL, "NULL device pointer");
+  const size_t lat_bytes = (size_t)B * (Ni / P) * c->C * 4;
+  {
+    const uint8_t* a0 = static_cast<const uint8_t*>((const void*)b->latents_in);
+    const uint8_t* b0 = reinterpret_cast<const uint8_t*>(b->latents_out);
+    if (a0 < b0 + lat_bytes && b0 < a0 + lat_bytes) return c->fail(DIT_EALIAS, "latents_out aliases latents_in");
+  }
+  if ((reinterpret_cast<uintptr_t>(b->txt) & 15)) return c->fail(DIT_EINVAL, "txt must be 16-byte aligned");
+  std::vector<int> req_slot(B, -1);
+  for (int i = 0; i < B; ++i) {
+    const int aid = b->adapter_id[i];
+    if (aid < 0) continue;
+    auto it = c->adapter_slot.find(aid);
+    if (it == c->adapter_slot.end()) return c->fail(DIT_EADAPTER, "request %d uses unregistered adapter %d", i, aid);
+    req_slot[i] = it->second;
+  }
+  for (auto& kv : c->cn)
+    if (kv.first.first >= B) return c->fail(DIT_EINVAL, "ControlNet registered for slot %d >= batch %d", kv.first.first, B);
+
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
+  {
+    cudaError_t pe = cudaGetLastError();
+    if (pe != cudaSuccess) return c->fail(DIT_ECUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
+  }
+  c->launches = 0;
+  const int D = c->D, H = c->H, d = c->d, F = c->F, C = c->C, Ct = c->Ct;
+  const int nt = Nt / P, ni = Ni / P, N = nt + ni;
+  const int Mt = B * nt, Mi = B * ni, Mj = B * N;
+
+  // ---- plan (cached by shape + adapter slots)
+  bool any_lora = false;
+  for (int i = 0; i < B; ++i) any_lora |= req_slot[i] >= 0;
+  if (c->plan_B != B || c->plan_h != b->img_h || c->plan_w != b->img_w || c->plan_nt != Nt || c->plan_slots != req_slot) {
+    std::vector<int> ht, hc;
+    std::vector<int2> hs;
+    const int Ms[3] = {Mt, Mi, Mj}, rpr[3] = {nt, ni, N};
+    for (int r = 0; r < 3; ++r) {
+      if (build_rowspace(c, c->rs[r], Ms[r], rpr[r], req_slot, ht, hc, hs) < 0)
+        return c->fail(DIT_ESHAPE, "too many distinct adapters in one 128-row tile");
+      cudaMemcpyAsync(c->rs[r].row_slot, c->rs[r].h_row_slot.data(), Ms[r] * 4, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(c->rs[r].tile_slots, ht.data(), ht.size() * 4, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(c->rs[r].tile_cnt, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice, s);
+      if (!hs.empty()) cudaMemcpyAsync(c->rs[r].shrink_list, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice, s);
+    }
+    if (!any_lora)
+      for (int r = 0; r < 3; ++r) c->rs[r].n_shrink = 0;
+    c->plan_B = B;
+    c->plan_h = b->img_h;
+    c->plan_w = b->img_w;
+    c->plan_nt = Nt;
+    c->plan_slots = req_slot;
+  }
+  if (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w) {
+    CKC(rope_table_launch(c->rope, nt, ni, c->rank * nt, c->rank * ni, b->img_w, c->cfg.rope_axes[0],
+                          c->cfg.rope_axes[1], c->cfg.rope_axes[2], c->cfg.rope_theta, s));
+    c->rope_key[0] = nt;
+    c->rope_key[1] = ni;
+    c->rope_key[2] = b->img_w;
+  }
+  // ---- per-step parameter block (pageable source: safe to reuse after return)
+  {
+    std::vector<float> pf(8 * 4 + 64, 0.f);
+    for (int i = 0; i < B; ++i) {
+      pf[i] = b->sigma_next[i] - b->sigma[i];
+      pf[8 + i] = b->cn_scale ? b->cn_scale[i] : 1.f;
+      pf[16 + i] = b->sigma[i];
+      pf[24 + i] = b->guidance[i];
+    }
+    cudaMemcpyAsync(c->p_dsig, pf.data(), 8 * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->p_cn_scale, pf.data() + 8, 8 * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->p_sigma, pf.data() + 16, 8 * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->p_guid, pf.data() + 24, 8 * 4, cudaMemcpyHostToDevice, s);
+    std::vector<float> ss(64, 0.f);
+    for (size_t i = 0; i < c->slot_scale_h.size() && i < 64; ++i) ss[i] = c->slot_scale_h[i];
+    cudaMemcpyAsync(c->p_slot_scale, ss.data(), 64 * 4, cudaMemcpyHostToDevice, s);
+    if (c->Ld > 0) {
+      std::vector<const void*> cp((size_t)c->Ld * 8, nullptr);
+      std::vector<float> kap((size_t)c->Ld * 8, 0.f);
+      for (auto& kv : c->cn) {
+        cp[(size_t)kv.first.second * 8 + kv.first.first] = kv.second.ptr;
+        kap[(size_t)kv.first.second * 8 + kv.first.first] =
+            kv.second.scale * (b->cn_scale ? b->cn_scale[kv.first.first] : 1.f);
+      }
+      cudaMemcpyAsync(c->p_cn_ptr, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(c->p_cn_kappa, kap.data(), kap.size() * 4, cudaMemcpyHostToDevice, s);
+    }
+  }
+  if (c->segs_dirty) {
+    std::vector<SkinnySeg> sg;
+    for (int i = 0; i < c->Ld; ++i)
+      for (int st = 0; st < 2; ++st) {
+        const Lin& L = c->dbl[st][i].mod;
+        sg.push_back({L.w, L.b, L.out, (i * 2 + st) * 6 * D});
+      }
+    for (int j = 0; j < c->Ls; ++j) sg.push_back({c->sgl[j].mod.w, c->sgl[j].mod.b, c->sgl[j].mod.out, 12 * D * c->Ld + j * 3 * D});
+    sg.push_back({c->fin_mod.w, c->fin_mod.b, c->fin_mod.out, 12 * D * c->Ld + 3 * D * c->Ls});
+    c->nsegs = (int)sg.size();
+    c->seg_rows = 0;
+    for (auto& x : sg) c->seg_rows += x.rows;
+    // tail: conditioning MLPs (time in/out, guidance in/out, vector in/out)
+    sg.push_back({c->t_in.w, c->t_in.b, D, 0});
+    sg.push_back({c->t_out.w, c->t_out.b, D, 0});
+    sg.push_back({c->g_in.w, c->g_in.b, D, 0});
+    sg.push_back({c->g_out.w, c->g_out.b, D, 0});
+    sg.push_back({c->y_in.w, c->y_in.b, D, 0});
+    sg.push_back({c->y_out.w, c->y_out.b, D, 0});
+    cudaMemcpyAsync(c->segs, sg.data(), sg.size() * sizeof(SkinnySeg), cudaMemcpyHostToDevice, s);
+    c->segs_dirty = false;
+  }
+  const int mod_off_single = 12 * D * c->Ld;
+  const int mod_off_final = mod_off_single + 3 * D * c->Ls;
+
+  // ---- conditioning vec (tail segments nsegs+0..5) and all modulations (one launch)
+  SkinnySeg* cs = c->segs + c->nsegs;
+  CKC(temb_launch(c->p_sigma, B, c->temb, s));
+  CKC(skinny_launch(c->temb, 256, cs + 0, 1, D, c->h1, D, B, 0, s));
+  CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
+  CKC(skinny_launch(c->xprep, D, cs + 1, 1, D, c->vec, D, B, 0, s));
+  if (c->cfg.guidance_embed) {
+    CKC(temb_launch(c->p_guid, B, c->temb, s));
+    CKC(skinny_launch(c->temb, 256, cs + 2, 1, D, c->h1, D, B, 0, s));
+    CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
+    CKC(skinny_launch(c->xprep, D, cs + 3, 1, D, c->vec, D, B, 1, s));
+  }
+  cudaMemsetAsync(c->xprep, 0, (size_t)8 * c->Cp * 2, s);
+  cudaMemcpyAsync(c->xprep, b->pooled, (size_t)B * c->Cp * 2, cudaMemcpyDeviceToDevice, s);
+  CKC(skinny_launch(c->xprep, c->Cp, cs + 4, 1, D, c->h1, D, B, 0, s));
+  CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
+  CKC(skinny_launch(c->xprep, D, cs + 5, 1, D, c->vec, D, B, 1, s));
+  CKC(prep_x_launch(c->vec, B, D, 1, c->xprep, s));
+  CKC(skinny_launch(c->xprep, D, c->segs, c->nsegs, c->seg_rows, c->mod, c->mod_total, B, 0, s));
+
+  // ---- embeddings into the fp32 residual stream h [B][N][D] (txt rows first)
+  CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)Mi * C, s));
+  {
+    EpiParams ei;
+    memset(&ei, 0, sizeof(ei));
+    ei.kind = EPI_STORE_H;
+    ei.h = c->h;
+    ei.D = D;
+    ei.joint_n = N;
+    EpiParams et = ei;
+    ei.bias = c->img_in.b;
+    ei.rows_per_req = ni;
+    ei.joint_off = nt;
+    et.bias = c->txt_in.b;
+    et.rows_per_req = nt;
+    et.joint_off = 0;
+    GemmProblem p[2] = {base_problem(c, c->xb, Mi, C, C, c->img_in, ei),
+                        base_problem(c, b->txt, Mt, Ct, Ct, c->txt_in, et)};
+    CK(run_gemm(c, p, 2, s));
+  }
+
+  const float scale_log2 = 1.4426950408889634f / std::sqrt((float)d);
+  auto lnmod2 = [&](int modT, int modI, int sh, int sc) -> int {
+    LnModParams lp;
+    memset(&lp, 0, sizeof(lp));
+    lp.h = c->h;
+    lp.D = D;
+    lp.joint_n = N;
+    lp.u = c->u;
+    lp.mod_stride = c->mod_total;
+    lp.nseg = 2;
+    lp.seg_rows[0] = Mt;
+    lp.seg_rows[1] = Mi;
+    lp.seg_rows_per_req[0] = nt;
+    lp.seg_rows_per_req[1] = ni;
+    lp.seg_joint_off[0] = 0;
+    lp.seg_joint_off[1] = nt;
+    lp.seg_shift_off[0] = modT + sh;
+    lp.seg_scale_off[0] = modT + sc;
+    lp.seg_shift_off[1] = modI + sh;
+    lp.seg_scale_off[1] = modI + sc;
+    lp.seg_mod[0] = lp.seg_mod[1] = c->mod;
+    cudaError_t e = lnmod_launch(lp, s);
+    c->launches++;
+    return e == cudaSuccess ? DIT_OK : c->fail(DIT_ECUDA, "lnmod: %s", cudaGetErrorString(e));
+  };
+  auto shrink2 = [&](const void* At, const void* Ai, int K, int lda, int modT, int modI) -> int {
+    if (!any_lora) return DIT_OK;
+    const void* A[2] = {At, Ai};
+    const int M[2] = {Mt, Mi}, Ks[2] = {K, K}, ld[2] = {lda, lda};
+    const RowSpace* R[2] = {&c->rs[0], &c->rs[1]};
+    const int mods[2] = {modT, modI};
+    return run_shrink(c, 2, A, M, Ks, ld, R, mods, s);
+  };
+
+  // ---- double-stream blocks
+  for (int i = 0; i < c->Ld; ++i) {
+    const DoubleStream& I = c->dbl[0][i];
+    const DoubleStream& T = c->dbl[1][i];
+    const int mI = (i * 2 + 0) * 6 * D, mT = (i * 2 + 1) * 6 * D;
+    bf16_t* uT = c->u;
+    bf16_t* uI = c->u + (size_t)Mt * D;
+    CK(lnmod2(mT, mI, 0, D));
+    CK(shrink2(uT, uI, D, D, T.lora[0], I.lora[0]));
+    {
+      EpiParams e;
+      memset(&e, 0, sizeof(e));
+      e.kind = EPI_QKV;
+      e.joint_n = N;
+      e.D = D;
+      e.q = c->q;
+      e.k = c->k;
+      e.v = c->v;
+      e.rope = c->rope;
+      e.qkv_cols = 3 * D;
+      e.heads = H;
+      e.head_dim = d;
+      e.seq_len = N;
+      EpiParams eT = e, eI = e;
+      eT.bias = T.qkv.b;
+      eT.rows_per_req = nt;
+      eT.joint_off = 0;
+      eT.q_gamma = T.qn;
+      eT.k_gamma = T.kn;
+      eI.bias = I.qkv.b;
+      eI.rows_per_req = ni;
+      eI.joint_off = nt;
+      eI.q_gamma = I.qn;
+      eI.k_gamma = I.kn;
+      GemmProblem p[2] = {base_problem(c, uT, Mt, D, D, T.qkv, eT), base_problem(c, uI, Mi, D, D, I.qkv, eI)};
+      if (any_lora) {
+        add_lora_ext(c, p[0], c->rs[0], T.lora[0]);
+        add_lora_ext(c, p[1], c->rs[1], I.lora[0]);
+      }
+      CK(run_gemm(c, p, 2, s));
+    }
+    {
+      AttnParams ap;
+      memset(&ap, 0, sizeof(ap));
+      ap.q = c->q;
+      ap.k = c->k;
+      ap.v = c->v;
+      ap.B = B;
+      ap.H = H;
+      ap.N = N;
+      ap.d = d;
+      ap.scale_log2 = scale_log2;
+      ap.out = c->o;
+      ap.ld_out = D;
+      ap.split = 1;
+      ap.nt = nt;
+      ap.ni = ni;
+      CKC(attention_launch(ap, s));
+    }
+    bf16_t* oT = c->o;
+    bf16_t* oI = c->o + (size_t)Mt * D;
+    auto resid_pair = [&](const Lin& LT, const Lin& LI, const void* AT, const void* AI, int K, int lda, int goff,
+                          int modT_l, int modI_l, const void* const* cn_ptr) -> int {
+      EpiParams e;
+      memset(&e, 0, sizeof(e));
+      e.kind = EPI_RESID;
+      e.h = c->h;
+      e.D = D;
+      e.joint_n = N;
+      e.mod = c->mod;
+      e.mod_stride = c->mod_total;
+      EpiParams eT = e, eI = e;
+      eT.bias = LT.b;
+      eT.rows_per_req = nt;
+      eT.joint_off = 0;
+      eT.gate_off = mT + goff;
+      eI.bias = LI.b;
+      eI.rows_per_req = ni;
+      eI.joint_off = nt;
+      eI.gate_off = mI + goff;
+      if (cn_ptr) {
+        eI.cn_ptr = cn_ptr;
+        eI.cn_scale = c->p_cn_kappa + (size_t)i * 8;
+      }
+      GemmProblem p[2] = {base_problem(c, AT, Mt, K, lda, LT, eT), base_problem(c, AI, Mi, K, lda, LI, eI)};
+      if (any_lora) {
+        add_lora_ext(c, p[0], c->rs[0], modT_l);
+        add_lora_ext(c, p[1], c->rs[1], modI_l);
+      }
+      return run_gemm(c, p, 2, s);
+    };
+    CK(shrink2(oT, oI, D, D, T.lora[1], I.lora[1]));
+    CK(resid_pair(T.proj, I.proj, oT, oI, D, D, 2 * D, T.lora[1], I.lora[1], nullptr));
+    CK(lnmod2(mT, mI, 3 * D, 4 * D));
+    CK(shrink2(uT, uI, D, D, T.lora[2], I.lora[2]));
+    bf16_t* aT = c->cat;
+    bf16_t* aI = c->cat + (size_t)Mt * F;
+    {
+      EpiParams e;
+      memset(&e, 0, sizeof(e));
+      e.kind = EPI_GELU;
+      e.ld_out = F;
+      e.joint_n = N;
+      EpiParams eT = e, eI = e;
+      eT.bias = T.fc1.b;
+      eT.rows_per_req = nt;
+      eT.out = aT;
+      eI.bias = I.fc1.b;
+      eI.rows_per_req = ni;
+      eI.joint_off = nt;
+      eI.out = aI;
+      GemmProblem p[2] = {base_problem(c, uT, Mt, D, D, T.fc1, eT), base_problem(c, uI, Mi, D, D, I.fc1, eI)};
+      if (any_lora) {
+        add_lora_ext(c, p[0], c->rs[0], T.lora[2]);
+        add_lora_ext(c, p[1], c->rs[1], I.lora[2]);
+      }
+      CK(run_gemm(c, p, 2, s));
+    }
+    // deferred ControlNet input of block i: wait right before its consumer
+    bool has_cn = false;
+    for (auto& kv : c->cn)
+      if (kv.first.second == i) {
+        has_cn = true;
+        if (kv.second.ready) cudaStreamWaitEvent(s, kv.second.ready, 0);
+      }
+    CK(shrink2(aT, aI, F, F, T.lora[3], I.lora[3]));
+    CK(resid_pair(T.fc2, I.fc2, aT, aI, F, F, 5 * D, T.lora[3], I.lora[3],
+                  has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * 8) : nullptr));
+  }
+
+  // ---- single-stream blocks on the joint sequence
+  for (int j = 0; j < c->Ls; ++j) {
+    const SingleBlk& S = c->sgl[j];
+    const int mj = mod_off_single + j * 3 * D;
+    {
+      LnModParams lp;
+      memset(&lp, 0, sizeof(lp));
+      lp.h = c->h;
+      lp.D = D;
+      lp.joint_n = N;
+      lp.u = c->u;
+      lp.mod_stride = c->mod_total;
+      lp.nseg = 1;
+      lp.seg_rows[0] = Mj;
+      lp.seg_rows_per_req[0] = N;
+      lp.seg_joint_off[0] = 0;
+      lp.seg_shift_off[0] = mj;
+      lp.seg_scale_off[0] = mj + D;
+      lp.seg_mod[0] = c->mod;
+      CKC(lnmod_launch(lp, s));
+    }
+    if (any_lora) {
+      const void* A[1] = {c->u};
+      const int M[1] = {Mj}, K[1] = {D}, ld[1] = {D};
+      const RowSpace* R[1] = {&c->rs[2]};
+      const int mods[1] = {S.lora[0]};
+      CK(run_shrink(c, 1, A, M, K, ld, R, mods, s));
+    }
+    {
+      EpiParams e;
+      memset(&e, 0, sizeof(e));
+      e.kind = EPI_QKV;
+      e.bias = S.l1.b;
+      e.rows_per_req = N;
+      e.joint_off = 0;
+      e.joint_n = N;
+      e.D = D;
+      e.q = c->q;
+      e.k = c->k;
+      e.v = c->v;
+      e.q_gamma = S.qn;
+      e.k_gamma = S.kn;
+      e.rope = c->rope;
+      e.qkv_cols = 3 * D;
+      e.heads = H;
+      e.head_dim = d;
+      e.seq_len = N;
+      e.out = c->cat;
+      e.ld_out = D + F;
+      e.out_col0 = D;
+      GemmProblem p = base_problem(c, c->u, Mj, D, D, S.l1, e);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0]);
+      CK(run_gemm(c, &p, 1, s));
+    }
+    {
+      AttnParams ap;
+      memset(&ap, 0, sizeof(ap));
+      ap.q = c->q;
+      ap.k = c->k;
+      ap.v = c->v;
+      ap.B = B;
+      ap.H = H;
+      ap.N = N;
+      ap.d = d;
+      ap.scale_log2 = scale_log2;
+      ap.out = c->cat;
+      ap.ld_out = D + F;
+      ap.split = 0;
+      CKC(attention_launch(ap, s));
+    }
+    if (any_lora) {
+      const void* A[1] = {c->cat};
+      const int M[1] = {Mj}, K[1] = {D + F}, ld[1] = {D + F};
+      const RowSpace* R[1] = {&c->rs[2]};
+      const int mods[1] = {S.lora[1]};
+      CK(run_shrink(c, 1, A, M, K, ld, R, mods, s));
+    }
+    {
+      EpiParams e;
+      memset(&e, 0, sizeof(e));
+      e.kind = EPI_RESID;
+      e.bias = S.l2.b;
+      e.rows_per_req = N;
+      e.joint_off = 0;
+      e.joint_n = N;
+      e.h = c->h;
+      e.D = D;
+      e.mod = c->mod;
+      e.mod_stride = c->mod_total;
+      e.gate_off = mj + 2 * D;
+      GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1]);
+      CK(run_gemm(c, &p, 1, s));
+    }
+  }
+
+  // ---- final layer + Euler update (fused epilogue)
+  {
+    LnModParams lp;
+    memset(&lp, 0, sizeof(lp));
+    lp.h = c->h;
+    lp.D = D;
+    lp.joint_n = N;
+    lp.u = c->u;
+    lp.mod_stride = c->mod_total;
+    lp.nseg = 1;
+    lp.seg_rows[0] = Mi;
+    lp.seg_rows_per_req[0] = ni;
+    lp.seg_joint_off[0] = nt;
+    lp.seg_shift_off[0] = mod_off_final;
+    lp.seg_scale_off[0] = mod_off_final + D;
+    lp.seg_mod[0] = c->mod;
+    CKC(lnmod_launch(lp, s));
+    EpiParams e;
+    memset(&e, 0, sizeof(e));
+    e.kind = EPI_FINAL;
+    e.bias = c->fin_lin.b;
+    e.rows_per_req = ni;
+    e.joint_n = N;
+    e.lat_in = b->latents_in;
+    e.lat_out = b->latents_out;
+    e.v_out = b->v_out;
+    e.dsig = c->p_dsig;
+    GemmProblem p = base_problem(c, c->u, Mi, D, D, c->fin_lin, e);
+    CK(run_gemm(c, &p, 1, s));
+  }
+
+  for (int i = 0; i < B; ++i)
+    if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
+  c->cn.clear();
+  c->last_launches = c->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ test-only exports
+extern "C" int dit_fill_synthetic(void* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset,
+                                  void* stream) {
+  if (!dst || n < 0) return DIT_EINVAL;
+  cudaError_t e = fill_synthetic_launch(dst, n, seed, tid, scale, offset, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
+namespace {
+int debug_prepare(dit_ctx* c, const dit_batch* b, std::vector<int>& req_slot, int& nt, int& ni) {
+  if (!b || b->batch < 1 || b->batch > c->cfg.max_batch) return -DIT_EBATCH;
+  const int P = c->world;
+  const int Ni = b->img_h * b->img_w, Nt = b->txt_tokens;
+  if (Ni <= 0 || Nt <= 0 || Ni % P || Nt % P) return -DIT_EPARALLEL;
+  nt = Nt / P;
+  ni = Ni / P;
+  req_slot.assign(b->batch, -1);
+  for (int i = 0; i < b->batch; ++i) {
+    const int aid = b->adapter_id ? b->adapter_id[i] : -1;
+    if (aid < 0) continue;
+    auto it = c->adapter_slot.find(aid);
+    if (it == c->adapter_slot.end()) return -DIT_EADAPTER;
+    req_slot[i] = it->second;
+  }
+  return 0;
+}
+}  // namespace
+
+extern "C" int dit_debug_row_adapter(dit_ctx* c, const dit_batch* b, int32_t* out, int cap) {
+  if (!c || !out) return -DIT_EINVAL;
+  std::vector<int> rs;
+  int nt, ni;
+  int r = debug_prepare(c, b, rs, nt, ni);
+  if (r < 0) return r;
+  const int B = b->batch;
+  const int rows = B * nt + B * ni;
+  if (cap < rows) return -DIT_EINVAL;
+  int k = 0;
+  for (int x = 0; x < B * nt; ++x) out[k++] = rs[x / nt];
+  for (int x = 0; x < B * ni; ++x) out[k++] = rs[x / ni];
+  return rows;
+}
+
+extern "C" int dit_debug_shard_map(dit_ctx* c, const dit_batch* b, int32_t* out, int cap) {
+  if (!c || !out) return -DIT_EINVAL;
+  std::vector<int> rs;
+  int nt, ni;
+  int r = debug_prepare(c, b, rs, nt, ni);
+  if (r < 0) return r;
+  const int B = b->batch, Nt = b->txt_tokens, N = b->txt_tokens + b->img_h * b->img_w;
+  const int rows = B * (nt + ni);
+  if (cap < rows) return -DIT_EINVAL;
+  int k = 0;
+  for (int bb = 0; bb < B; ++bb) {
+    for (int x = 0; x < nt; ++x) out[k++] = bb * N + c->rank * nt + x;
+    for (int x = 0; x < ni; ++x) out[k++] = bb * N + Nt + c->rank * ni + x;
+  }
+  return rows;
+}

@@ -1,0 +1,253 @@
+// elementwise.cu -- HBM-bound kernels of the step:
+//   * LN-modulate: u = (1 + scale_b) * LN(h) + shift_b, fp32 in, bf16 out,
+//     one warp per row, float4 loads, two-pass mean/variance in registers;
+//   * skinny GEMM for the conditioning MLPs and ALL adaLN modulations in one
+//     launch: out[b][n] = x[b] . W[n] + bias[n] for b < 8 on mma.sync with the
+//     weight rows streamed straight from HBM (16-byte loads, K permuted
+//     consistently between the A (weights) and B (x) fragments);
+//   * small helpers: sinusoid embedding, RoPE table, casts, synthetic fill.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dit {
+
+// ------------------------------------------------------------------ LN-modulate
+constexpr int LN_MAXV = 24;   // float4 per lane: D <= 3072
+
+__global__ void __launch_bounds__(256) lnmod_kernel(const LnModParams p, int total_rows) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp_global >= total_rows) return;
+  int seg = 0, r = warp_global;
+  if (p.nseg > 1 && r >= p.seg_rows[0]) {
+    seg = 1;
+    r -= p.seg_rows[0];
+  }
+  const int rpr = p.seg_rows_per_req[seg];
+  const int b = r / rpr;
+  const int n = r - b * rpr;
+  const int jrow = b * p.joint_n + p.seg_joint_off[seg] + n;
+  const int D = p.D;
+  const int nv = D / 4;
+  const float4* hrow = reinterpret_cast<const float4*>(p.h + (size_t)jrow * D);
+  float4 x[LN_MAXV];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      x[i] = hrow[c];
+      sum += (x[i].x + x[i].y) + (x[i].z + x[i].w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+  const float mean = sum / (float)D;
+  float var = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float a = x[i].x - mean, bb = x[i].y - mean, cc = x[i].z - mean, dd = x[i].w - mean;
+      var += (a * a + bb * bb) + (cc * cc + dd * dd);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffff, var, o);
+  const float rstd = rsqrtf(var / (float)D + 1e-6f);
+  const float* modb = p.seg_mod[seg] + (size_t)b * p.mod_stride;
+  const float4* sh = reinterpret_cast<const float4*>(modb + p.seg_shift_off[seg]);
+  const float4* sc = reinterpret_cast<const float4*>(modb + p.seg_scale_off[seg]);
+  const int out_row = (seg == 1 ? p.seg_rows[0] : 0) + r;
+  uint2* urow = reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(p.u) + (size_t)out_row * D);
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float4 s4 = __ldg(sh + c), c4 = __ldg(sc + c);
+      uint2 o;
+      o.x = pack_bf16((1.f + c4.x) * ((x[i].x - mean) * rstd) + s4.x, (1.f + c4.y) * ((x[i].y - mean) * rstd) + s4.y);
+      o.y = pack_bf16((1.f + c4.z) * ((x[i].z - mean) * rstd) + s4.z, (1.f + c4.w) * ((x[i].w - mean) * rstd) + s4.w);
+      urow[c] = o;
+    }
+  }
+}
+
+cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
+  if (p.D % 4 != 0 || p.D / 4 > LN_MAXV * 32) return cudaErrorInvalidValue;
+  int total = p.seg_rows[0] + (p.nseg > 1 ? p.seg_rows[1] : 0);
+  if (total <= 0) return cudaSuccess;
+  int blocks = (total * 32 + 255) / 256;
+  lnmod_kernel<<<blocks, 256, 0, s>>>(p, total);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ skinny GEMM
+// One warp computes 16 output rows n (all 8 batch columns) over the full K.
+// Per 32-wide K chunk, thread (gid, tig) loads 16 B of W row gid and row gid+8
+// at k = base + 8*tig and 16 B of x row gid at the same k; two m16n8k16 MMAs
+// consume them with logical k slots {2tig,2tig+1,2tig+8,2tig+9} mapped to
+// physical k = base + 8 tig + {0,1,2,3} (first MMA) / {4,5,6,7} (second).
+__global__ void __launch_bounds__(256) skinny_kernel(const bf16* __restrict__ x, int K, const SkinnySeg* __restrict__ segs,
+                                                     int nseg, int total_rows, float* __restrict__ out, int out_stride,
+                                                     int B, int accumulate) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int row0 = warp_global * 16;
+  if (row0 >= total_rows) return;
+  // find segment (rows of a segment are a multiple of 16 except possibly the last tile)
+  int sidx = 0, srow = row0;
+  while (sidx < nseg - 1 && srow >= segs[sidx].rows) {
+    srow -= segs[sidx].rows;
+    ++sidx;
+  }
+  const SkinnySeg sg = segs[sidx];
+  const int gid = lane / 4, tig = lane % 4;
+  const bf16* w0 = reinterpret_cast<const bf16*>(sg.w) + (size_t)min(srow + gid, sg.rows - 1) * K;
+  const bf16* w1 = reinterpret_cast<const bf16*>(sg.w) + (size_t)min(srow + gid + 8, sg.rows - 1) * K;
+  const bf16* xr = x + (size_t)gid * K;
+  float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+  const int Kpad = (K + 31) & ~31;
+#pragma unroll 4
+  for (int k = 8 * tig; k < Kpad; k += 32) {
+    const bool ok = k < K;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    const uint4 a0 = ok ? __ldg(reinterpret_cast<const uint4*>(w0 + k)) : z;
+    const uint4 a1 = ok ? __ldg(reinterpret_cast<const uint4*>(w1 + k)) : z;
+    const uint4 xv = ok ? __ldg(reinterpret_cast<const uint4*>(xr + k)) : z;
+    uint32_t fa[4] = {a0.x, a1.x, a0.y, a1.y};
+    uint32_t fb[2] = {xv.x, xv.y};
+    mma_bf16_16816(acc0, fa, fb);
+    uint32_t fa2[4] = {a0.z, a1.z, a0.w, a1.w};
+    uint32_t fb2[2] = {xv.z, xv.w};
+    mma_bf16_16816(acc1, fa2, fb2);
+  }
+  // C fragment: c0,c1 = (row gid, batch 2tig, 2tig+1), c2,c3 = (row gid+8, ...)
+  const bf16* bias = reinterpret_cast<const bf16*>(sg.bias);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int rr = srow + gid + (e >= 2 ? 8 : 0);
+    const int bb = 2 * tig + (e & 1);
+    if (rr < sg.rows && bb < B) {
+      float v = acc0[e] + acc1[e] + __bfloat162float(bias[rr]);
+      float* o = out + (size_t)bb * out_stride + sg.out_off + rr;
+      if (accumulate) v += *o;
+      *o = v;
+    }
+  }
+}
+
+cudaError_t skinny_launch(const void* x, int K, const SkinnySeg* segs_dev, int nseg, int total_rows, float* out,
+                          int out_stride, int B, int accumulate, cudaStream_t s) {
+  if (K % 8 != 0) return cudaErrorInvalidValue;
+  int warps = (total_rows + 15) / 16;
+  int blocks = (warps * 32 + 255) / 256;
+  skinny_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const bf16*>(x), K, segs_dev, nseg, total_rows, out,
+                                       out_stride, B, accumulate);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ small helpers
+__global__ void prep_x_kernel(const float* x, int B, int K, int silu, bf16* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 8 * K) return;
+  const int b = i / K;
+  float v = 0.f;
+  if (b < B) {
+    v = x[i];
+    if (silu) v = v / (1.f + expf(-v));
+  }
+  out[i] = __float2bfloat16_rn(v);
+}
+cudaError_t prep_x_launch(const float* x, int B, int K, int silu, void* out, cudaStream_t s) {
+  prep_x_kernel<<<(8 * K + 255) / 256, 256, 0, s>>>(x, B, K, silu, reinterpret_cast<bf16*>(out));
+  return cudaGetLastError();
+}
+
+// e(t) = [cos(1000 t w_k), sin(1000 t w_k)], w_k = 10000^(-k/128), k < 128 (fp64 args).
+__global__ void temb_kernel(const float* vals, int B, bf16* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 8 * 256) return;
+  const int b = i / 256, j = i % 256;
+  double v = 0.0;
+  if (b < B) {
+    const int k = j % 128;
+    const double w = exp(-log(10000.0) * (double)k / 128.0);
+    const double a = 1000.0 * (double)vals[b] * w;
+    v = (j < 128) ? cos(a) : sin(a);
+  }
+  out[i] = __float2bfloat16_rn((float)v);
+}
+cudaError_t temb_launch(const float* vals, int B, void* out, cudaStream_t s) {
+  temb_kernel<<<8, 256, 0, s>>>(vals, B, reinterpret_cast<bf16*>(out));
+  return cudaGetLastError();
+}
+
+// RoPE (cos, sin) for local joint rows: rows [0, nt_loc) are txt (position 0),
+// rows [nt_loc, nt_loc + ni_loc) are img tokens ni_off + i -> (0, n / W, n % W).
+__global__ void rope_table_kernel(float2* tab, int nt_loc, int ni_loc, int ni_off, int img_w, int a0, int a1, int a2,
+                                  float theta) {
+  const int half = (a0 + a1 + a2) / 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (nt_loc + ni_loc) * half) return;
+  const int row = i / half, j = i % half;
+  double pos[3] = {0.0, 0.0, 0.0};
+  if (row >= nt_loc) {
+    const int n = ni_off + (row - nt_loc);
+    pos[1] = (double)(n / img_w);
+    pos[2] = (double)(n % img_w);
+  }
+  int axis, jj, da;
+  if (j < a0 / 2) { axis = 0; jj = j; da = a0; }
+  else if (j < (a0 + a1) / 2) { axis = 1; jj = j - a0 / 2; da = a1; }
+  else { axis = 2; jj = j - (a0 + a1) / 2; da = a2; }
+  const double ang = pos[axis] * pow((double)theta, -2.0 * jj / (double)da);
+  tab[i] = make_float2((float)cos(ang), (float)sin(ang));
+}
+cudaError_t rope_table_launch(float2* tab, int nt_loc, int ni_loc, int nt_off, int ni_off, int img_w, int a0, int a1,
+                              int a2, float theta, cudaStream_t s) {
+  (void)nt_off;
+  const int half = (a0 + a1 + a2) / 2;
+  const int n = (nt_loc + ni_loc) * half;
+  rope_table_kernel<<<(n + 255) / 256, 256, 0, s>>>(tab, nt_loc, ni_loc, ni_off, img_w, a0, a1, a2, theta);
+  return cudaGetLastError();
+}
+
+__global__ void cast_bf16_kernel(const float* x, bf16* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(x[i]);
+}
+cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cast_bf16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, reinterpret_cast<bf16*>(out), n);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ synthetic fill (synth/__init__.py)
+DEVI uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void fill_synth_kernel(bf16* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = seed ^ (tid << 40) ^ (uint64_t)i;
+    const float u = (float)(splitmix64(key) >> 40) * 5.9604644775390625e-08f;   // 2^-24, exact
+    const float t = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);
+    float w = __fmul_rn(t, scale);
+    if (offset != 0.0f) w = __fadd_rn(offset, w);
+    dst[i] = __float2bfloat16_rn(w);
+  }
+}
+cudaError_t fill_synthetic_launch(void* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  fill_synth_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<bf16*>(dst), n, seed, tid, scale, offset);
+  return cudaGetLastError();
+}
+
+}  // namespace dit

@@ -1,0 +1,478 @@
+// gemm.cu -- persistent warp-specialised tcgen05 GEMM with fused epilogues.
+//
+// C[M][N] = A[M][K] * B[N][K]^T (+ LoRA K-extension), bf16 in, fp32 in TMEM.
+// Roles (192 threads, 1 CTA per SM):
+//   warp 0      TMA producer: 4-stage smem ring of A 128x64 + B 256x64 tiles
+//               (SWIZZLE_128B), mbarrier full/empty handshake.
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1
+//               kind::f16 M=128 N=256 K=16, commits stage release and
+//               accumulator-ready to mbarriers.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 from a double-buffered TMEM
+//               accumulator (2 x 256 columns) and the fused epilogue of the
+//               step row: bias, QK-RMSNorm + RoPE + head-major
+//               scatter, GELU, gated residual (+ControlNet), Euler, LoRA shrink.
+// Tiles are scheduled statically (tile += gridDim.x) over up to two problems
+// (the img and txt streams of a double block share one launch), rasterised
+// in groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dit {
+
+constexpr int STAGES = 4;
+constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+constexpr int B_BYTES = GEMM_BN * GEMM_BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+size_t gemm_smem_bytes() { return SMEM_BYTES; }
+
+struct TileInfo {
+  int p, m, n, slot, nk_base, nk_total;
+};
+
+DEVI TileInfo decode_tile(const GemmArgs& A, int t) {
+  TileInfo ti;
+  ti.p = (A.num_problems > 1 && t >= A.p[1].tile_begin) ? 1 : 0;
+  const GemmProblem& P = A.p[ti.p];
+  int local = t - P.tile_begin;
+  ti.slot = -1;
+  if (P.shrink) {
+    int2 e = P.shrink_list[local];
+    ti.m = e.x;
+    ti.slot = e.y;
+    ti.n = 0;
+  } else {
+    int per_group = GEMM_GROUP_M * P.tiles_n;
+    int g = local / per_group;
+    int first_m = g * GEMM_GROUP_M;
+    int gm = min(GEMM_GROUP_M, P.tiles_m - first_m);
+    int within = local - g * per_group;
+    ti.m = first_m + within % gm;
+    ti.n = within / gm;
+  }
+  ti.nk_base = (P.K + GEMM_BK - 1) / GEMM_BK;
+  ti.nk_total = ti.nk_base;
+  if (P.ext_kblocks > 0 && !P.shrink) ti.nk_total += P.tile_slot_cnt[ti.m] * P.ext_kblocks;
+  return ti;
+}
+
+DEVI float gelu_tanh_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+
+DEVI void load_bias32(const bf16* bias, int col, int N, float (&bv)[32]) {
+  if (col + 32 <= N) {
+    const uint4* p = reinterpret_cast<const uint4*>(bias + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u = __ldg(p + q);
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bv[q * 8 + 2 * e] = bf16_lo(w[e]);
+        bv[q * 8 + 2 * e + 1] = bf16_hi(w[e]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bv[j] = (col + j < N) ? __bfloat162float(bias[col + j]) : 0.f;
+  }
+}
+
+DEVI void store_bf16_32(bf16* dst, const float (&x)[32], int valid) {
+  if (valid >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint4* p = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16(x[q * 8 + 0], x[q * 8 + 1]);
+      u.y = pack_bf16(x[q * 8 + 2], x[q * 8 + 3]);
+      u.z = pack_bf16(x[q * 8 + 4], x[q * 8 + 5]);
+      u.w = pack_bf16(x[q * 8 + 6], x[q * 8 + 7]);
+      p[q] = u;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < valid) dst[j] = __float2bfloat16_rn(x[j]);
+  }
+}
+
+// Epilogue for one accumulator tile; executed by the 128 epilogue threads.
+DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase, int row_in_tile) {
+  const EpiParams& E = P.epi;
+  const int r = ti.m * GEMM_BM + row_in_tile;
+  const bool row_ok = r < P.M;
+  const int n0 = ti.n * GEMM_BN;
+  const int b = row_ok ? r / E.rows_per_req : 0;
+  const int nloc = row_ok ? r - b * E.rows_per_req : 0;
+  const int jrow = b * E.joint_n + E.joint_off + nloc;
+  const bf16* bias = reinterpret_cast<const bf16*>(E.bias);
+
+  if (E.kind == EPI_QKV) {
+    const int d = E.head_dim;
+    const int D = E.D;
+#pragma unroll 1
+    for (int c0 = 0; c0 < GEMM_BN; c0 += d) {
+      const int col0 = n0 + c0;
+      if (col0 >= P.N) break;
+      if (col0 < E.qkv_cols) {
+        float x[128];
+        const int nch = d / 32;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < nch) {
+            uint32_t rr[32];
+            tmem_ld32(tbase + c0 + 32 * j, rr);
+            tmem_ld_wait();
+            float bv[32];
+            load_bias32(bias, col0 + 32 * j, P.N, bv);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) x[32 * j + e] = __uint_as_float(rr[e]) + bv[e];
+          }
+        }
+        if (!row_ok) continue;
+        const int sec = col0 / D;
+        const int head = (col0 - sec * D) / d;
+        if (sec < 2) {
+          const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
+          float ss = 0.f;
+#pragma unroll
+          for (int j = 0; j < 128; ++j)
+            if (j < d) ss += x[j] * x[j];
+          const float rs = rsqrtf(ss / (float)d + 1e-6f);
+          const float2* cs = E.rope + (size_t)(E.joint_off + nloc) * (d / 2);
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            if (2 * j < d) {
+              float x0 = x[2 * j] * rs * __bfloat162float(g[2 * j]);
+              float x1 = x[2 * j + 1] * rs * __bfloat162float(g[2 * j + 1]);
+              float2 c = __ldg(cs + j);
+              x[2 * j] = c.x * x0 - c.y * x1;
+              x[2 * j + 1] = c.y * x0 + c.x * x1;
+            }
+          }
+        }
+        bf16* dst = reinterpret_cast<bf16*>(sec == 0 ? E.q : (sec == 1 ? E.k : E.v));
+        dst += ((size_t)(b * E.heads + head) * E.seq_len + (E.joint_off + nloc)) * d;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < nch) {
+            float y[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) y[e] = x[32 * j + e];
+            store_bf16_32(dst + 32 * j, y, 32);
+          }
+        }
+      } else {
+        // GELU branch of the single-block linear1 (cols >= 3D)
+        for (int j = 0; j < d; j += 32) {
+          const int col = col0 + j;
+          uint32_t rr[32];
+          tmem_ld32(tbase + c0 + j, rr);
+          tmem_ld_wait();
+          if (col >= P.N || !row_ok) continue;
+          float bv[32], y[32];
+          load_bias32(bias, col, P.N, bv);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) y[e] = gelu_tanh_f(__uint_as_float(rr[e]) + bv[e]);
+          bf16* dst = reinterpret_cast<bf16*>(E.out) + (size_t)r * E.ld_out + E.out_col0 + (col - E.qkv_cols);
+          store_bf16_32(dst, y, min(32, P.N - col));
+        }
+      }
+    }
+    return;
+  }
+
+  if (E.kind == EPI_SHRINK) {
+    const int rs = row_ok ? E.row_slot[r] : -2;
+    const float sc = E.slot_scale[ti.slot];
+    for (int c0 = 0; c0 < E.r_alloc; c0 += 32) {
+      uint32_t rr[32];
+      tmem_ld32(tbase + c0, rr);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      float y[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) y[e] = (rs == ti.slot) ? sc * __uint_as_float(rr[e]) : 0.f;
+      bf16* dst = reinterpret_cast<bf16*>(E.out) + (size_t)r * E.ld_out + ti.slot * E.r_alloc + c0;
+      store_bf16_32(dst, y, 32);
+    }
+    return;
+  }
+
+#pragma unroll 1
+  for (int c0 = 0; c0 < GEMM_BN; c0 += 32) {
+    const int col = n0 + c0;
+    if (col >= P.N) break;
+    uint32_t rr[32];
+    tmem_ld32(tbase + c0, rr);
+    tmem_ld_wait();
+    if (!row_ok) continue;
+    const int valid = min(32, P.N - col);
+    float bv[32], y[32];
+    load_bias32(bias, col, P.N, bv);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr[e]) + bv[e];
+    if (E.kind == EPI_GELU) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) y[e] = gelu_tanh_f(y[e]);
+      store_bf16_32(reinterpret_cast<bf16*>(E.out) + (size_t)r * E.ld_out + E.out_col0 + col, y, valid);
+    } else if (E.kind == EPI_STORE_H) {
+      float* hp = E.h + (size_t)jrow * E.D + col;
+      if (valid == 32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(hp)[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+      } else {
+        for (int e = 0; e < valid; ++e) hp[e] = y[e];
+      }
+    } else if (E.kind == EPI_RESID) {
+      float* hp = E.h + (size_t)jrow * E.D + col;
+      const float* gp = E.mod + (size_t)b * E.mod_stride + E.gate_off + col;
+      const bf16* cn = nullptr;
+      float kap = 0.f;
+      if (E.cn_ptr != nullptr) {
+        cn = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
+        if (cn != nullptr) {
+          kap = E.cn_scale[b];
+          cn += (size_t)nloc * E.D + col;
+        }
+      }
+      if (valid == 32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 h4 = reinterpret_cast<float4*>(hp)[q];
+          float4 g4 = __ldg(reinterpret_cast<const float4*>(gp) + q);
+          h4.x += g4.x * y[4 * q];
+          h4.y += g4.y * y[4 * q + 1];
+          h4.z += g4.z * y[4 * q + 2];
+          h4.w += g4.w * y[4 * q + 3];
+          if (cn != nullptr) {
+            uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
+            h4.x += kap * bf16_lo(c2.x);
+            h4.y += kap * bf16_hi(c2.x);
+            h4.z += kap * bf16_lo(c2.y);
+            h4.w += kap * bf16_hi(c2.y);
+          }
+          reinterpret_cast<float4*>(hp)[q] = h4;
+        }
+      } else {
+        for (int e = 0; e < valid; ++e) {
+          float hv = hp[e] + gp[e] * y[e];
+          if (cn != nullptr) hv += kap * __bfloat162float(cn[e]);
+          hp[e] = hv;
+        }
+      }
+    } else if (E.kind == EPI_FINAL) {
+      const float ds = E.dsig[b];
+      for (int e = 0; e < valid; ++e) {
+        const size_t off = (size_t)r * P.N + col + e;
+        E.lat_out[off] = E.lat_in[off] + ds * y[e];
+        if (E.v_out != nullptr) E.v_out[off] = y[e];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < args.num_problems; ++p) {
+      tma_prefetch_desc(&args.p[p].tmA);
+      tma_prefetch_desc(&args.p[p].tmB);
+      if (args.p[p].ext_kblocks > 0) {
+        tma_prefetch_desc(&args.p[p].tmAx);
+        tma_prefetch_desc(&args.p[p].tmBx);
+      }
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+        const TileInfo ti = decode_tile(args, t);
+        const GemmProblem& P = args.p[ti.p];
+        for (int kb = 0; kb < ti.nk_total; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * B_BYTES;
+          if (kb < ti.nk_base) {
+            tma_load_2d(&P.tmA, &full[stage], a_dst, kb * GEMM_BK, ti.m * GEMM_BM);
+            if (P.shrink)
+              tma_load_2d(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.slot * P.epi.r_alloc);
+            else
+              tma_load_2d(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.n * GEMM_BN);
+          } else {
+            const int e = kb - ti.nk_base;
+            const int si = e / P.ext_kblocks;
+            const int ek = e - si * P.ext_kblocks;
+            const int slot = P.tile_slots[ti.m * P.slot_cap + si];
+            tma_load_2d(&P.tmAx, &full[stage], a_dst, slot * P.epi.r_alloc + ek * GEMM_BK, ti.m * GEMM_BM);
+            tma_load_2d(&P.tmBx, &full[stage], b_dst, ek * GEMM_BK, slot * P.N + ti.n * GEMM_BN);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++iter) {
+        const TileInfo ti = decode_tile(args, t);
+        const int acc = iter & 1;
+        const uint32_t acc_phase = (iter >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
+        for (int kb = 0; kb < ti.nk_total; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            tc_mma_f16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32), idesc,
+                       (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int wq = warp & 3;              // TMEM lane quarter this warp may access
+    const int row_in_tile = wq * 32 + lane;
+    int iter = 0;
+    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++iter) {
+      const TileInfo ti = decode_tile(args, t);
+      const int acc = iter & 1;
+      const uint32_t acc_phase = (iter >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * GEMM_BN;
+      epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                  uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "[libdit] cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu stride=%llu ptr=%p\n",
+            (int)r, (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_stride_bytes, ptr);
+    return false;
+  }
+  return true;
+}
+
+bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                  uint64_t stride2_bytes, uint32_t box0, uint32_t box1) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (args.total_tiles <= 0) return cudaSuccess;
+  int grid = args.total_tiles < num_sms ? args.total_tiles : num_sms;
+  gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(args);
+  return cudaGetLastError();
+}
+
+}  // namespace dit

@@ -1,0 +1,159 @@
+// kernels.h -- internal launch interfaces of libdit (host side; no torch types).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dit {
+
+// ------------------------------------------------------------------ GEMM (tcgen05)
+// Tile 128 x 256 x 64, bf16 in, fp32 accumulate in TMEM, fused epilogues.
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_MAX_PROBLEMS = 2;
+constexpr int GEMM_GROUP_M = 16;   // rasterisation: tiles sweep all N within a group of 16 M-tiles
+
+enum EpiKind : int {
+  EPI_STORE_H = 0,  // h[jrow][c] = acc + bias                (fp32, embeddings)
+  EPI_QKV = 1,      // bias, QK-RMSNorm, RoPE, head-major scatter; cols >= qkv_cols -> GELU to out
+  EPI_GELU = 2,     // out[r][out_col0 + c] = bf16(gelu_tanh(acc + bias))
+  EPI_RESID = 3,    // h[jrow][c] += gate_b[c] * (acc + bias) (+ cn_scale_b * R_b[n][c])
+  EPI_FINAL = 4,    // v = acc + bias; lat_out = lat_in + dsig_b * v
+  EPI_SHRINK = 5,   // S[r][slot*r_alloc + c] = row_slot(r)==slot ? bf16(scale_slot*acc) : 0
+};
+
+struct EpiParams {
+  int kind;
+  const void* bias;          // bf16 [N]
+  // row map: local GEMM row r -> request b = r / rows_per_req, n = r % rows_per_req
+  int rows_per_req;
+  int joint_off;             // stream offset inside the joint (local) sequence
+  int joint_n;               // local joint rows per request
+  // fp32 residual stream h [B][joint_n][D]
+  float* h;
+  int D;
+  const float* mod;          // modulation base [B][mod_stride]
+  int mod_stride;
+  int gate_off;              // column offset of the gate vector inside mod rows
+  // ControlNet residual (EPI_RESID img stream)
+  const void* const* cn_ptr; // device [B] residual pointers (nullptr = none), bf16 [rows_per_req][D]
+  const float* cn_scale;     // device [B]
+  // bf16 outputs
+  void* out;
+  int ld_out;
+  int out_col0;
+  // QKV scatter
+  void* q;
+  void* k;
+  void* v;
+  const void* q_gamma;       // bf16 [d]
+  const void* k_gamma;
+  const float2* rope;        // [joint_n][d/2] (cos, sin)
+  int qkv_cols;              // 3D (columns beyond go to the GELU branch)
+  int heads, head_dim;
+  int seq_len;               // rows per (b, h) of q/k/v (= joint_n)
+  // final layer
+  const float* lat_in;
+  float* lat_out;
+  float* v_out;
+  const float* dsig;         // device [B] sigma_next - sigma
+  // LoRA shrink
+  const int* row_slot;       // device [M] pool slot of each row (-1 none)
+  const float* slot_scale;   // device [max_adapters]
+  int r_alloc;
+};
+
+struct GemmProblem {
+  CUtensorMap tmA;       // A [M][K] bf16, box {64, 128}
+  CUtensorMap tmB;       // B [N][K] bf16, box {64, 256}; or 3D [slot][N][K] for shrink
+  CUtensorMap tmAx;      // LoRA K-extension A: S [M][slots*r_alloc], box {64, 128}
+  CUtensorMap tmBx;      // LoRA K-extension B: pool [slot][N][r_alloc] 3D, box {64, 256, 1}
+  int M, N, K;
+  int tiles_m, tiles_n;
+  int tile_begin;        // first global tile index of this problem
+  int num_tiles;
+  // LoRA: per m-tile list of pool slots (device [tiles_m][slot_cap]) + counts
+  const int* tile_slots;
+  const int* tile_slot_cnt;
+  int slot_cap;
+  int ext_kblocks;       // k-blocks per slot (r_alloc / 64); 0 = no extension
+  int shrink;            // 1: tiles enumerate (m_tile, slot) pairs from shrink_list
+  const int2* shrink_list;  // device [num_tiles] (m_tile, slot)
+  EpiParams epi;
+};
+
+struct GemmArgs {
+  GemmProblem p[GEMM_MAX_PROBLEMS];
+  int num_problems;
+  int total_tiles;
+};
+
+// Encode a 2D/3D bf16 tensor map with SWIZZLE_128B (box inner = 64 elements).
+bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                  uint32_t box_inner, uint32_t box_outer);
+bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                  uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
+
+cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s);
+size_t gemm_smem_bytes();
+
+// ------------------------------------------------------------------ attention
+// q/k/v bf16 [B][H][N][d]; O rows written to out with the stream-split or joint map.
+struct AttnParams {
+  const void* q;
+  const void* k;
+  const void* v;
+  int B, H, N, d;
+  float scale_log2;    // log2(e) / sqrt(d)
+  void* out;           // bf16
+  int ld_out;          // elements per output row
+  int split;           // 1: rows n < Nt -> txt block, else img block (double blocks)
+  int nt;              // txt rows per request (split mode)
+  int ni;              // img rows per request (split mode)
+};
+cudaError_t attention_launch(const AttnParams& p, cudaStream_t s);
+
+// ------------------------------------------------------------------ elementwise / skinny
+// u[r] = (1 + scale_b) * LN(h[jrow(r)]) + shift_b  (bf16 out), rows of up to 2 streams.
+struct LnModParams {
+  const float* h;
+  int D;
+  int joint_n;
+  void* u;                 // bf16 [rows][D]
+  const float* mod;
+  int mod_stride;
+  int nseg;
+  int seg_rows[2];         // rows of each segment (stream)
+  int seg_rows_per_req[2];
+  int seg_joint_off[2];
+  int seg_shift_off[2];    // column offsets of shift / scale inside mod rows
+  int seg_scale_off[2];
+  const float* seg_mod[2]; // per-segment modulation base (may differ per stream)
+};
+cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s);
+
+// out[b][n] (+)= sum_k x[b][k] * W[n][k] + bias[n] for b < 8, with x bf16 [8][K]
+// (zero rows beyond B).  Segment table lets one launch cover many weights.
+struct SkinnySeg {
+  const void* w;       // bf16 [rows][K]
+  const void* bias;    // bf16 [rows]
+  int rows;
+  int out_off;         // column offset into out rows
+};
+cudaError_t skinny_launch(const void* x, int K, const SkinnySeg* segs_dev, int nseg, int total_rows,
+                          float* out, int out_stride, int B, int accumulate, cudaStream_t s);
+
+// x_bf16[b][k] = bf16(act(x[b][k])) (act: 0 none, 1 SiLU), rows >= B zeroed (8 rows).
+cudaError_t prep_x_launch(const float* x, int B, int K, int silu, void* out, cudaStream_t s);
+// sinusoid embedding rows: out[b] = bf16([cos(1000 t w_k), sin(...)]), t = vals[b]; zero rows >= B.
+cudaError_t temb_launch(const float* vals, int B, void* out, cudaStream_t s);
+// rope table [n_rows][d/2] float2 from (Nt, img_w, first global joint row ...).
+cudaError_t rope_table_launch(float2* tab, int nt_loc, int ni_loc, int nt_off, int ni_off, int img_w,
+                              int a0, int a1, int a2, float theta, cudaStream_t s);
+// x fp32 [n] -> bf16
+cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t s);
+cudaError_t fill_synthetic_launch(void* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset,
+                                  cudaStream_t s);
+
+}  // namespace dit
