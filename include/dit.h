@@ -181,6 +181,18 @@ double dit_step_flops(const dit_ctx* ctx, const dit_batch* batch);
 /* Number of kernels the last dit_step launched (for bench.py gpu_launches). */
 int dit_last_launch_count(const dit_ctx* ctx);
 
+/* ------------------------------------------------------ profiling exports */
+/* Per-launch device timing for bench.py's roofline (CUDA events recorded on
+ * the launch stream around every kernel while enabled).  kind: 0 tcgen05
+ * GEMM (all projections, LoRA shrink/expand), 1 attention, 2 LN-modulate,
+ * 3 modulation skinny GEMM, 4 other small kernels.  dit_profile_read
+ * synchronises on the recorded events and returns the summed device time,
+ * the summed ALGORITHMIC flops and the number of launches of that kind since
+ * the last dit_profile_reset. */
+int dit_profile(dit_ctx* ctx, int enable);
+int dit_profile_read(dit_ctx* ctx, int kind, double* total_ms, double* flops, int* launches);
+int dit_profile_reset(dit_ctx* ctx);
+
 /* ---------------------------------------------------- test-only exports */
 /* Fill a device bf16 tensor of n elements with the synth counter generator
  * (synth/__init__.py docstring): w = bf16(offset + (2u-1)*scale). */

@@ -109,11 +109,11 @@ def attention(q: np.ndarray, k: np.ndarray, v: np.ndarray) -> np.ndarray:
     q, k, v: [H, N, d] -> [H, N, d].
     """
     d = q.shape[-1]
-    s = np.einsum("hqd,hkd->hqk", q, k) / math.sqrt(d)
+    s = (q @ k.swapaxes(-1, -2)) / math.sqrt(d)          # [H, Nq, Nk]
     s = s - s.max(axis=-1, keepdims=True)
     p = np.exp(s)
     p = p / p.sum(axis=-1, keepdims=True)
-    return np.einsum("hqk,hkd->hqd", p, v)
+    return p @ v
 
 
 # ----------------------------------------------------------------------------

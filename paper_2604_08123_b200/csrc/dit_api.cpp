@@ -69,6 +69,7 @@ struct RowSpace {     // LoRA bookkeeping for one GEMM row space (txt, img or jo
   int* tile_cnt = nullptr;        // device [tiles_m]
   int2* shrink_list = nullptr;    // device [n_shrink]
   int n_shrink = 0;
+  double rank_rows = 0;           // sum over rows of the adapter rank
   std::vector<int> h_row_slot;    // host copy (debug export)
 };
 
@@ -139,6 +140,14 @@ struct dit_ctx {
   int rope_key[3] = {-1, -1, -1};
   int last_launches = 0;
   int launches = 0;
+  // per-launch profiling (bench.py roofline): events on the launch stream
+  struct ProfRec { int kind; double flops; cudaEvent_t a, b; };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  cudaEvent_t prof_a = nullptr;
+  std::vector<int> slot_rank_h;
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -341,6 +350,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     for (int j = 0; j < c->Ls; ++j) { add(D, 3 * D + F); add(D + F, D); }
   }
   c->slot_scale_h.assign(std::max(cfg->max_adapters, 1), 0.f);
+  c->slot_rank_h.assign(std::max(cfg->max_adapters, 1), 0);
   c->slot_last_use.assign(std::max(cfg->max_adapters, 1), nullptr);
   for (auto& e : c->slot_last_use) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   c->dbl[0].resize(c->Ld);
@@ -365,6 +375,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
 
 extern "C" void dit_destroy(dit_ctx* c) {
   if (!c) return;
+  for (auto& e : c->ev_pool) cudaEventDestroy(e);
   for (auto& e : c->slot_last_use)
     if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -582,6 +593,7 @@ extern "C" int lora_register(dit_ctx* c, int32_t adapter_id, int32_t rank, float
   if (cudaGetLastError() != cudaSuccess) return c->fail(DIT_ECUDA, "adapter copy failed");
   c->adapter_slot[adapter_id] = slot;
   c->slot_scale_h[slot] = scale;
+  c->slot_rank_h[slot] = rank;
   c->plan_B = -1;  // slot tables may change
   return DIT_OK;
 }
@@ -662,6 +674,9 @@ int build_rowspace(dit_ctx* c, RowSpace& R, int M, int rows_per_req, const std::
     }
   }
   R.n_shrink = (int)h_shrink.size();
+  R.rank_rows = 0;
+  for (int r = 0; r < M; ++r)
+    if (R.h_row_slot[r] >= 0) R.rank_rows += c->slot_rank_h[R.h_row_slot[r]];
   return 0;
 }
 
@@ -669,6 +684,36 @@ int build_rowspace(dit_ctx* c, RowSpace& R, int M, int rows_per_req, const std::
 
 // ------------------------------------------------------------------ GEMM helpers
 namespace {
+
+cudaEvent_t prof_event(dit_ctx* c) {
+  if (c->ev_next == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_next++];
+}
+void prof_begin(dit_ctx* c, cudaStream_t s) {
+  if (!c->prof_on) return;
+  c->prof_a = prof_event(c);
+  cudaEventRecord(c->prof_a, s);
+}
+void prof_end(dit_ctx* c, cudaStream_t s, int kind, double flops) {
+  if (!c->prof_on) return;
+  cudaEvent_t b = prof_event(c);
+  cudaEventRecord(b, s);
+  c->prof.push_back({kind, flops, c->prof_a, b});
+}
+
+// Algorithmic FLOPs: 2MNK for the base product; LoRA counts
+// 2 r in (shrink) + 2 r out (expand) per adapted row -- padding excluded.
+double problem_flops(const dit_ctx* c, const GemmProblem& P) {
+  (void)c;
+  if (P.shrink) return 2.0 * P.K * P.rank_rows;
+  double f = 2.0 * P.M * P.N * (double)P.K;
+  if (P.ext_kblocks > 0) f += 2.0 * P.N * P.rank_rows;
+  return f;
+}
 
 GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const Lin& W, const EpiParams& epi) {
   GemmProblem P;
@@ -686,18 +731,20 @@ GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const
   return P;
 }
 
-void add_lora_ext(dit_ctx* c, GemmProblem& P, const RowSpace& R, int module) {
+void add_lora_ext(dit_ctx* c, GemmProblem& P, const RowSpace& R, int module, const void* sext) {
   if (R.n_shrink == 0 || c->pools.empty() || !c->pools[module].A) return;
   const int nslots = std::max(c->cfg.max_adapters, 1);
-  make_tmap_2d(&P.tmAx, c->sext, (uint64_t)nslots * c->r_alloc, P.M, (uint64_t)nslots * c->r_alloc * 2, 64, GEMM_BM);
+  make_tmap_2d(&P.tmAx, sext, (uint64_t)nslots * c->r_alloc, P.M, (uint64_t)nslots * c->r_alloc * 2, 64, GEMM_BM);
   P.tmBx = c->pools[module].tmB;
   P.tile_slots = R.tile_slots;
   P.tile_slot_cnt = R.tile_cnt;
   P.ext_kblocks = c->r_alloc / 64;
   P.epi.r_alloc = c->r_alloc;
+  P.rank_rows = R.rank_rows;
 }
 
-GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, const RowSpace& R, int module) {
+GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, const RowSpace& R, int module,
+                           void* sext) {
   GemmProblem P;
   memset(&P, 0, sizeof(P));
   const LoraPool& L = c->pools[module];
@@ -712,8 +759,9 @@ GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, con
   P.num_tiles = R.n_shrink;
   P.shrink = 1;
   P.shrink_list = R.shrink_list;
+  P.rank_rows = R.rank_rows;
   P.epi.kind = EPI_SHRINK;
-  P.epi.out = c->sext;
+  P.epi.out = sext;
   P.epi.ld_out = nslots * c->r_alloc;
   P.epi.row_slot = R.row_slot;
   P.epi.slot_scale = c->p_slot_scale;
@@ -723,7 +771,11 @@ GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, con
   return P;
 }
 
-int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s) {
+int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s, double flops = -1.0) {
+  if (flops < 0) {
+    flops = 0;
+    for (int i = 0; i < np; ++i) flops += problem_flops(c, probs[i]);
+  }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   int t = 0;
@@ -738,19 +790,29 @@ int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s) {
   a.num_problems = k;
   a.total_tiles = t;
   if (t == 0) return DIT_OK;
+  prof_begin(c, s);
   cudaError_t e = gemm_launch(a, c->num_sms, s);
+  prof_end(c, s, 0, flops);
   c->launches++;
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   return DIT_OK;
 }
 
 // LoRA shrink for up to two (A, rowspace, module) triples, as one launch.
+// S_ext of stream problem i lives at sext_of(c, i): the txt stream's rows first,
+// then the img stream's (a single-block problem uses the start).
+void* sext_of(dit_ctx* c, int stream_rows_before) {
+  const int nslots = std::max(c->cfg.max_adapters, 1);
+  return c->sext + (size_t)stream_rows_before * nslots * c->r_alloc;
+}
+
 int run_shrink(dit_ctx* c, int np, const void* const* A, const int* M, const int* K, const int* lda,
-               const RowSpace* const* R, const int* module, cudaStream_t s) {
+               const RowSpace* const* R, const int* module, const int* row_base, cudaStream_t s) {
   GemmProblem p[2];
   int k = 0;
   for (int i = 0; i < np; ++i)
-    if (R[i]->n_shrink > 0 && c->pools[module[i]].A) p[k++] = shrink_problem(c, A[i], M[i], K[i], lda[i], *R[i], module[i]);
+    if (R[i]->n_shrink > 0 && c->pools[module[i]].A)
+      p[k++] = shrink_problem(c, A[i], M[i], K[i], lda[i], *R[i], module[i], sext_of(c, row_base[i]));
   if (k == 0) return DIT_OK;
   return run_gemm(c, p, k, s);
 }
@@ -789,9 +851,12 @@ extern "C" int dit_last_launch_count(const dit_ctx* c) { return c ? c->last_laun
     int _r = (x);                                                                    \
     if (_r != DIT_OK) return _r;                                                     \
   } while (0)
-#define CKC(x)                                                                       \
+#define CKC(x) CKK(x, 4, 0.0)
+#define CKK(x, kind, flops)                                                          \
   do {                                                                               \
+    prof_begin(c, s);                                                                \
     cudaError_t _e = (x);                                                            \
+    prof_end(c, s, kind, flops);                                                     \
     c->launches++;                                                                   \
     if (_e != cudaSuccess) return c->fail(DIT_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
   } while (0)
@@ -942,7 +1007,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
   CKC(skinny_launch(c->xprep, D, cs + 5, 1, D, c->vec, D, B, 1, s));
   CKC(prep_x_launch(c->vec, B, D, 1, c->xprep, s));
-  CKC(skinny_launch(c->xprep, D, c->segs, c->nsegs, c->seg_rows, c->mod, c->mod_total, B, 0, s));
+  CKK(skinny_launch(c->xprep, D, c->segs, c->nsegs, c->seg_rows, c->mod, c->mod_total, B, 0, s), 3,
+      2.0 * B * (double)c->seg_rows * D);
 
   // ---- embeddings into the fp32 residual stream h [B][N][D] (txt rows first)
   CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)Mi * C, s));
@@ -986,7 +1052,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     lp.seg_shift_off[1] = modI + sh;
     lp.seg_scale_off[1] = modI + sc;
     lp.seg_mod[0] = lp.seg_mod[1] = c->mod;
+    prof_begin(c, s);
     cudaError_t e = lnmod_launch(lp, s);
+    prof_end(c, s, 2, 0.0);
     c->launches++;
     return e == cudaSuccess ? DIT_OK : c->fail(DIT_ECUDA, "lnmod: %s", cudaGetErrorString(e));
   };
@@ -996,7 +1064,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     const int M[2] = {Mt, Mi}, Ks[2] = {K, K}, ld[2] = {lda, lda};
     const RowSpace* R[2] = {&c->rs[0], &c->rs[1]};
     const int mods[2] = {modT, modI};
-    return run_shrink(c, 2, A, M, Ks, ld, R, mods, s);
+    const int base[2] = {0, Mt};
+    return run_shrink(c, 2, A, M, Ks, ld, R, mods, base, s);
   };
 
   // ---- double-stream blocks
@@ -1035,8 +1104,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       eI.k_gamma = I.kn;
       GemmProblem p[2] = {base_problem(c, uT, Mt, D, D, T.qkv, eT), base_problem(c, uI, Mi, D, D, I.qkv, eI)};
       if (any_lora) {
-        add_lora_ext(c, p[0], c->rs[0], T.lora[0]);
-        add_lora_ext(c, p[1], c->rs[1], I.lora[0]);
+        add_lora_ext(c, p[0], c->rs[0], T.lora[0], sext_of(c, 0));
+        add_lora_ext(c, p[1], c->rs[1], I.lora[0], sext_of(c, Mt));
       }
       CK(run_gemm(c, p, 2, s));
     }
@@ -1056,7 +1125,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       ap.split = 1;
       ap.nt = nt;
       ap.ni = ni;
-      CKC(attention_launch(ap, s));
+      CKK(attention_launch(ap, s), 1, 4.0 * B * (double)N * N * D);
     }
     bf16_t* oT = c->o;
     bf16_t* oI = c->o + (size_t)Mt * D;
@@ -1085,8 +1154,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       }
       GemmProblem p[2] = {base_problem(c, AT, Mt, K, lda, LT, eT), base_problem(c, AI, Mi, K, lda, LI, eI)};
       if (any_lora) {
-        add_lora_ext(c, p[0], c->rs[0], modT_l);
-        add_lora_ext(c, p[1], c->rs[1], modI_l);
+        add_lora_ext(c, p[0], c->rs[0], modT_l, sext_of(c, 0));
+        add_lora_ext(c, p[1], c->rs[1], modI_l, sext_of(c, Mt));
       }
       return run_gemm(c, p, 2, s);
     };
@@ -1112,8 +1181,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       eI.out = aI;
       GemmProblem p[2] = {base_problem(c, uT, Mt, D, D, T.fc1, eT), base_problem(c, uI, Mi, D, D, I.fc1, eI)};
       if (any_lora) {
-        add_lora_ext(c, p[0], c->rs[0], T.lora[2]);
-        add_lora_ext(c, p[1], c->rs[1], I.lora[2]);
+        add_lora_ext(c, p[0], c->rs[0], T.lora[2], sext_of(c, 0));
+        add_lora_ext(c, p[1], c->rs[1], I.lora[2], sext_of(c, Mt));
       }
       CK(run_gemm(c, p, 2, s));
     }
@@ -1148,14 +1217,15 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       lp.seg_shift_off[0] = mj;
       lp.seg_scale_off[0] = mj + D;
       lp.seg_mod[0] = c->mod;
-      CKC(lnmod_launch(lp, s));
+      CKK(lnmod_launch(lp, s), 2, 0.0);
     }
     if (any_lora) {
       const void* A[1] = {c->u};
       const int M[1] = {Mj}, K[1] = {D}, ld[1] = {D};
       const RowSpace* R[1] = {&c->rs[2]};
       const int mods[1] = {S.lora[0]};
-      CK(run_shrink(c, 1, A, M, K, ld, R, mods, s));
+      const int base[1] = {0};
+      CK(run_shrink(c, 1, A, M, K, ld, R, mods, base, s));
     }
     {
       EpiParams e;
@@ -1180,7 +1250,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.ld_out = D + F;
       e.out_col0 = D;
       GemmProblem p = base_problem(c, c->u, Mj, D, D, S.l1, e);
-      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0]);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0], sext_of(c, 0));
       CK(run_gemm(c, &p, 1, s));
     }
     {
@@ -1197,14 +1267,15 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       ap.out = c->cat;
       ap.ld_out = D + F;
       ap.split = 0;
-      CKC(attention_launch(ap, s));
+      CKK(attention_launch(ap, s), 1, 4.0 * B * (double)N * N * D);
     }
     if (any_lora) {
       const void* A[1] = {c->cat};
       const int M[1] = {Mj}, K[1] = {D + F}, ld[1] = {D + F};
       const RowSpace* R[1] = {&c->rs[2]};
       const int mods[1] = {S.lora[1]};
-      CK(run_shrink(c, 1, A, M, K, ld, R, mods, s));
+      const int base[1] = {0};
+      CK(run_shrink(c, 1, A, M, K, ld, R, mods, base, s));
     }
     {
       EpiParams e;
@@ -1220,7 +1291,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.mod_stride = c->mod_total;
       e.gate_off = mj + 2 * D;
       GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
-      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1]);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1], sext_of(c, 0));
       CK(run_gemm(c, &p, 1, s));
     }
   }
@@ -1241,7 +1312,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     lp.seg_shift_off[0] = mod_off_final;
     lp.seg_scale_off[0] = mod_off_final + D;
     lp.seg_mod[0] = c->mod;
-    CKC(lnmod_launch(lp, s));
+    CKK(lnmod_launch(lp, s), 2, 0.0);
     EpiParams e;
     memset(&e, 0, sizeof(e));
     e.kind = EPI_FINAL;
@@ -1262,6 +1333,39 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   c->last_launches = c->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ profiling exports
+extern "C" int dit_profile(dit_ctx* c, int enable) {
+  if (!c) return DIT_EINVAL;
+  c->prof_on = enable != 0;
+  return DIT_OK;
+}
+
+extern "C" int dit_profile_read(dit_ctx* c, int kind, double* total_ms, double* flops, int* launches) {
+  if (!c || kind < 0 || kind > 4) return DIT_EINVAL;
+  double ms = 0, fl = 0;
+  int n = 0;
+  for (auto& r : c->prof) {
+    if (r.kind != kind) continue;
+    cudaEventSynchronize(r.b);
+    float e = 0.f;
+    cudaEventElapsedTime(&e, r.a, r.b);
+    ms += e;
+    fl += r.flops;
+    ++n;
+  }
+  if (total_ms) *total_ms = ms;
+  if (flops) *flops = fl;
+  if (launches) *launches = n;
+  return DIT_OK;
+}
+
+extern "C" int dit_profile_reset(dit_ctx* c) {
+  if (!c) return DIT_EINVAL;
+  c->prof.clear();
+  c->ev_next = 0;
   return DIT_OK;
 }
 

@@ -81,6 +81,7 @@ struct GemmProblem {
   int shrink;            // 1: tiles enumerate (m_tile, slot) pairs from shrink_list
   const int2* shrink_list;  // device [num_tiles] (m_tile, slot)
   EpiParams epi;
+  double rank_rows;      // host bookkeeping: sum over LoRA rows of the adapter rank (FLOP count)
 };
 
 struct GemmArgs {

@@ -57,6 +57,10 @@ EXPORTS = {
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
     "dit_last_launch_count": (C.c_int, [C.c_void_p]),
+    "dit_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "dit_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int)]),
+    "dit_profile_reset": (C.c_int, [C.c_void_p]),
     "dit_fill_synthetic": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64, C.c_float, C.c_float,
                                      C.c_void_p]),
     "dit_debug_row_adapter": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
@@ -203,6 +207,17 @@ class DiT:
 
     def last_launch_count(self) -> int:
         return int(self.lib.dit_last_launch_count(self.ctx))
+
+    def profile(self, enable: bool):
+        _check(self.lib.dit_profile(self.ctx, int(enable)), self.ctx)
+
+    def profile_read(self, kind: int):
+        ms, fl, n = C.c_double(), C.c_double(), C.c_int()
+        _check(self.lib.dit_profile_read(self.ctx, kind, C.byref(ms), C.byref(fl), C.byref(n)), self.ctx)
+        return ms.value, fl.value, n.value
+
+    def profile_reset(self):
+        _check(self.lib.dit_profile_reset(self.ctx), self.ctx)
 
     def debug_row_adapter(self, batch: dit_batch, cap: int):
         out = (C.c_int32 * cap)()
