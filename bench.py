@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py -- denoise steps/s of the B200-native shared-base-model step.
+
+Workload (BASELINE.json metric config, configs[2]): Flux-Dev-shaped MMDiT
+(19 double + 38 single blocks, D = 3072, 24 x 128 heads) at 1024^2
+(4096 image + 512 text tokens), a cross-workflow batch of B = 8 requests
+sharing the base model with 4 distinct rank-64 LoRAs (ids a seeded
+permutation of [0,0,1,1,2,2,3,3]) and mixed timesteps.  One "step" = one
+dit_step over the whole batch (every row of SURVEY.md §8(a)).
+
+Contract: python bench.py --gpus N --steps K --warmup W prints ONE JSON line
+on rank 0.  --impl reference times the fp64 CPU oracle (the reference arm of
+this tier) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "denoise steps/s (Flux-Dev 1024², mixed LoRA) at 1/2/4/8 B200; % bf16 peak"
+UNIT = "steps/s"
+WORKLOAD = "Flux-Dev-shaped 19+38 blocks, D=3072, 24x128 heads, 1024^2 (4096 img + 512 txt tokens), " \
+           "B=8 cross-workflow batch, 4 distinct rank-64 LoRAs (ids permuted [0,0,1,1,2,2,3,3]), mixed sigmas"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm": d.get("hbm_gbs", 6650.0), "bf16": d.get("bf16_tflops", 1590.0),
+                "bf16_sus": d.get("bf16_tflops_sustained", 1400.0), "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) timing
+def oracle_sample_times(n_double: int, n_single: int):
+    """Time the fp64 oracle's own block functions at the full workload width/tokens.
+
+    Sample: `n_double` Flux-width double blocks and `n_single` single blocks of ONE
+    request with its rank-64 LoRA, N = 4608 tokens.  Weights are random (timing
+    is value-independent).  Returns (mean t_double, mean t_single) seconds.
+    """
+    import numpy as np
+    import synth
+    from oracle import flux_step as O
+
+    cfg = synth.flux_reduced(1, 1)
+    D, F, H, r = cfg.hidden, cfg.mlp_hidden, cfg.heads, 64
+    rng = np.random.default_rng(0)
+    W = {}
+    for spec in synth.weight_manifest(cfg):
+        if spec.name.startswith(("double.", "single.")):
+            W[spec.name] = rng.standard_normal(spec.shape) * spec.scale + spec.offset
+    mats = {}
+    for mod, fin, fout in synth.lora_targets(cfg):
+        mats[mod] = (rng.standard_normal((r, fin)) * math.sqrt(3 / fin), rng.standard_normal((fout, r)) * 0.1)
+    ad = O.OracleLoRA(1.0, mats)
+    ids = O.position_ids(512, 64, 64)
+    cos, sin = O.rope_cos_sin(ids, cfg.rope_axes, cfg.rope_theta)
+    img = rng.standard_normal((4096, D))
+    txt = rng.standard_normal((512, D))
+    vec = rng.standard_normal(D)
+    td, ts = [], []
+    for _ in range(n_double):
+        t0 = time.perf_counter()
+        O.double_block(W, 0, H, img, txt, vec, cos, sin, ad)
+        td.append(time.perf_counter() - t0)
+    x = np.concatenate([txt, img])
+    for _ in range(n_single):
+        t0 = time.perf_counter()
+        O.single_block(W, 0, H, x, vec, cos, sin, ad)
+        ts.append(time.perf_counter() - t0)
+    return (sum(td) / len(td) if td else None), (sum(ts) / len(ts) if ts else None)
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline(B=8, n_double=1, n_single=1):
+    t0 = time.perf_counter()
+    td, ts = oracle_sample_times(n_double, n_single)
+    t_step = B * (19 * td + 38 * ts)
+    return {
+        "value": 1.0 / t_step, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+        "sample": (f"fp64 numpy oracle, {n_double} double + {n_single} single Flux-width block(s) of one request "
+                   f"(N=4608, rank-64 LoRA) timed ({td:.2f} s / {ts:.2f} s per block); steps/s extrapolated as "
+                   f"1 / (B=8 x (19 t_double + 38 t_single)), embedders/final omitted (<0.1% of FLOPs); "
+                   f"sample wall {time.perf_counter() - t0:.1f} s"),
+    }
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    tds, tss = [], []
+    for i in range(args.warmup + args.steps):
+        dbl = (i % 2 == 0)
+        td, ts = oracle_sample_times(1 if dbl else 0, 0 if dbl else 1)
+        if i >= args.warmup:
+            (tds if dbl else tss).append(td if dbl else ts)
+    if not tds:
+        tds.append(oracle_sample_times(1, 0)[0])
+    if not tss:
+        tss.append(oracle_sample_times(0, 1)[1])
+    td, ts = sum(tds) / len(tds), sum(tss) / len(tss)
+    t_step = 8 * (19 * td + 38 * ts)
+    val = 1.0 / t_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": 8, "seq_len": 4608, "parallelism": "cpu-oracle"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": f"each timed step = one Flux-width block of one request (alternating double/"
+                                   f"single, N=4608, rank-64 LoRA); steps/s = 1/(8 x (19 t_d + 38 t_s))"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2604_08123_b200 import SyntheticDiT
+    from paper_2604_08123_b200.synthetic import _bits_to_bf16_tensor
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = f"cuda:{local}"
+    cfg = synth.FLUX
+    B, H_, W_, NT = 8, 64, 64, 512
+    n_ad, rank_lora = 4, 64
+    model = SyntheticDiT(cfg, max_batch=B, max_img_tokens=H_ * W_, max_txt_tokens=NT, max_rank=rank_lora,
+                         max_adapters=n_ad, device=local)
+    for a in range(n_ad):
+        model.register_synthetic_lora(a, rank=rank_lora, index=a, scale=1.0)
+    batch = synth.make_batch(cfg, B, H_, W_, NT, n_adapters=n_ad, first_request=8 * rank)
+    lat, txt, pooled, out, v = model.device_inputs(batch)
+    lat2 = torch.empty_like(lat)
+    cb = model.make_batch(B, H_, W_, NT, batch.adapter_id, batch.sigma, batch.sigma_next, batch.guidance,
+                          lat, out, txt, pooled, v_out=None, cn_scale=batch.cn_scale)
+    stream = torch.cuda.current_stream()
+    flops = model.step_flops(cb)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        model.dit_step(cb)
+    torch.cuda.synchronize()
+    launches_per_step = model.last_launch_count()
+
+    # ---- device-timed region (inputs resident in HBM; working set 26 GB >> 126 MB L2)
+    model.profile_reset()
+    model.profile(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        model.dit_step(cb)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    model.profile(False)
+    prof = {k: model.profile_read(k) for k in range(5)}
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end-to-end through the public API with host buffers (pinned), H2D + D2H in the timed region
+    h_lat = torch.from_numpy(np.ascontiguousarray(batch.latents)).pin_memory()
+    h_txt = torch.from_numpy(np.ascontiguousarray(batch.txt).view(np.int16)).view(torch.bfloat16).pin_memory()
+    h_pool = torch.from_numpy(np.ascontiguousarray(batch.pooled).view(np.int16)).view(torch.bfloat16).pin_memory()
+    h_out = torch.empty_like(h_lat).pin_memory()
+    e_steps = max(1, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(e_steps):
+        lat.copy_(h_lat, non_blocking=True)
+        txt.copy_(h_txt, non_blocking=True)
+        pooled.copy_(h_pool, non_blocking=True)
+        model.dit_step(cb)
+        h_out.copy_(out, non_blocking=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": world * e_steps / (e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(h_lat.numel() * 4 + h_txt.numel() * 2 + h_pool.numel() * 2),
+           "d2h_bytes_per_step": int(h_out.numel() * 4)}
+
+    if rank != 0:
+        return 0
+    peaks = load_peaks()
+    g_ms, g_fl, g_n = prof[0]
+    a_ms, a_fl, a_n = prof[1]
+    achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    prof_total = sum(p[0] for p in prof.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": H_ * W_ + NT,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "inputs larger than L2 (26 GB weights+adapters streamed per step vs 126 MB L2)"},
+        "tflops_per_step": flops / 1e12,
+        "achieved_tflops": flops / (ms_step / 1e3) / 1e12,
+        "pct_bf16_peak": 100.0 * flops / (ms_step / 1e3) / 1e12 / peaks["bf16"],
+        "roofline": {"bound": "tensor", "kernel": "gemm_kernel (tcgen05 128x256x64, fused epilogues)",
+                     "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                     "frac": (achieved / peaks["bf16_sus"]) if achieved else None, "traffic": traffic,
+                     "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside the long step)",
+                     "launches": g_n, "share_of_step": g_ms / prof_total if prof_total else None},
+        "kernels": {
+            "gemm": {"ms_per_step": g_ms / args.steps, "tflops": achieved, "launches_per_step": g_n / args.steps},
+            "attention": {"ms_per_step": a_ms / args.steps,
+                          "tflops": a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else None},
+            "lnmod": {"ms_per_step": prof[2][0] / args.steps},
+            "modulation_skinny": {"ms_per_step": prof[3][0] / args.steps},
+            "other": {"ms_per_step": prof[4][0] / args.steps},
+        },
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(B)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
