@@ -114,8 +114,12 @@ def oracle_sample_times(n_double: int, n_single: int):
     import synth
     from oracle import flux_step as O
 
+    global _SAMPLE
     cfg = synth.flux_reduced(1, 1)
     D, F, H, r = cfg.hidden, cfg.mlp_hidden, cfg.heads, 64
+    if _SAMPLE is not None:
+        W, ad, cos, sin, img, txt, vec = _SAMPLE
+        return _time_blocks(O, W, ad, cos, sin, img, txt, vec, H, n_double, n_single)
     rng = np.random.default_rng(0)
     W = {}
     for spec in synth.weight_manifest(cfg):
@@ -130,6 +134,15 @@ def oracle_sample_times(n_double: int, n_single: int):
     img = rng.standard_normal((4096, D))
     txt = rng.standard_normal((512, D))
     vec = rng.standard_normal(D)
+    _SAMPLE = (W, ad, cos, sin, img, txt, vec)
+    return _time_blocks(O, W, ad, cos, sin, img, txt, vec, H, n_double, n_single)
+
+
+_SAMPLE = None
+
+
+def _time_blocks(O, W, ad, cos, sin, img, txt, vec, H, n_double, n_single):
+    import numpy as np
     td, ts = [], []
     for _ in range(n_double):
         t0 = time.perf_counter()
