@@ -222,11 +222,15 @@ static cudaError_t launch_hd(const AttnParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s);
+
+// d = 128 (Flux) runs on the tcgen05 kernel (attention_tc.cu); the mma.sync
+// kernel serves the small head dims of the tiny parity configs.
 cudaError_t attention_launch(const AttnParams& p, cudaStream_t s) {
   switch (p.d) {
     case 32: return launch_hd<32>(p, s);
     case 64: return launch_hd<64>(p, s);
-    case 128: return launch_hd<128>(p, s);
+    case 128: return attention_tc_launch(p, s);
     default: return cudaErrorInvalidValue;
   }
 }

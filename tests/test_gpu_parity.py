@@ -119,3 +119,22 @@ def test_batch_invariance_bitwise(torch_cuda):
                                   adapter_id=full.adapter_id[b:b + 1], cn_scale=full.cn_scale[b:b + 1])
         _, v1 = m.step(one)
         np.testing.assert_array_equal(v1[0], v[b])
+
+
+D128 = dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, rope_axes=(16, 56, 56), depth_single=1)
+
+
+@pytest.mark.parametrize("grid,nt", [((10, 15), 40), ((32, 32), 256), ((4, 4), 8)])
+def test_head_dim_128_tcgen05_attention(torch_cuda, grid, nt):
+    """d = 128 routes attention to the tcgen05 kernel: ragged KV tails, many KV tiles, tiny N."""
+    cfg = D128
+    hh, ww = grid
+    m = _model(cfg, 2, hh * ww, nt, rank=8, adapters=1)
+    m.register_synthetic_lora(3, rank=8, index=0)
+    batch = synth.make_batch(cfg, 2, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([-1, 3], dtype=np.int32)
+    lat, v = m.step(batch)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = O.dit_step(cfg, W, batch, {3: oracle_adapter(cfg, 8, 0)[0]})
+    check(v, v_o, "v")
+    check(lat, x_o, "latents")
