@@ -185,7 +185,8 @@ int dit_last_launch_count(const dit_ctx* ctx);
 /* Per-launch device timing for bench.py's roofline (CUDA events recorded on
  * the launch stream around every kernel while enabled).  kind: 0 tcgen05
  * GEMM (all projections, LoRA shrink/expand), 1 attention, 2 LN-modulate,
- * 3 modulation skinny GEMM, 4 other small kernels.  dit_profile_read
+ * 3 modulation skinny GEMM, 4 other small kernels, 5 SP all-to-all (NCCL),
+ * 6 SP layout gather/scatter kernels.  dit_profile_read
  * synchronises on the recorded events and returns the summed device time,
  * the summed ALGORITHMIC flops and the number of launches of that kind since
  * the last dit_profile_reset. */
@@ -198,6 +199,14 @@ int dit_profile_reset(dit_ctx* ctx);
  * (synth/__init__.py docstring): w = bf16(offset + (2u-1)*scale). */
 int dit_fill_synthetic(void* dst_bf16, int64_t n, uint64_t seed, uint64_t tensor_id,
                        float scale, float offset, void* stream);
+
+/* In-process communicator for tests (one host thread per rank, all ranks'
+ * contexts in this process): the SP all-to-all becomes event-ordered device
+ * copies.  Lets the exact sequence-parallel kernels and layouts be exercised
+ * on a single GPU.  sp_init_local is the test analogue of sp_init. */
+void* dit_local_group_create(int32_t world);
+void dit_local_group_destroy(void* group);
+int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 
 /* Integer plan artefacts of `batch` (host outputs; bit-exact tests):
  * row_adapter: int32 [rows] LoRA pool slot of each local row of the

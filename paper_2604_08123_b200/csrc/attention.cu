@@ -198,11 +198,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
     const int r = i / C::CHUNKS, c = i % C::CHUNKS;
     const int n = q0 + r;
     if (n >= N) continue;
-    size_t orow;
-    if (p.split)
-      orow = (n < p.nt) ? (size_t)b * p.nt + n : (size_t)p.B * p.nt + (size_t)b * p.ni + (n - p.nt);
-    else
-      orow = (size_t)b * N + n;
+    const size_t orow = (size_t)attn_out_row(p, b, n);
     const uint4 val = *reinterpret_cast<const uint4*>(sq + swz_off<HD>(r, c));
     *reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD + c * 8) = val;
   }

@@ -251,11 +251,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const int n = q0 + row;
     const float inv = 1.0f / l;
     bf16* out = reinterpret_cast<bf16*>(p.out);
-    size_t orow;
-    if (p.split)
-      orow = (n < p.nt) ? (size_t)b * p.nt + n : (size_t)p.B * p.nt + (size_t)b * p.ni + (n - p.nt);
-    else
-      orow = (size_t)b * N + n;
+    const size_t orow = n < N ? (size_t)attn_out_row(p, b, n) : 0;
     uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {

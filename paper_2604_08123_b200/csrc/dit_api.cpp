@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -77,6 +79,45 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
+// In-process communicator for tests: one host thread per rank, all ranks'
+// contexts in one process (same or peer-accessible devices).  The all-to-all
+// is event-ordered device-to-device copies; host barriers make every rank see
+// the others' send buffers and events.  Test-only (dit_local_group_create).
+struct LocalGroup {
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int count = 0;
+  long gen = 0;
+  std::vector<const void*> send;
+  std::vector<cudaEvent_t> ready, done;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long g = gen;
+    if (++count == world) {
+      count = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+  void a2a(int rank, const void* sendbuf, void* recvbuf, size_t bytes, cudaStream_t s) {
+    cudaEventRecord(ready[rank], s);
+    send[rank] = sendbuf;
+    barrier();
+    for (int r = 0; r < world; ++r) {
+      cudaStreamWaitEvent(s, ready[r], 0);
+      cudaMemcpyAsync(static_cast<uint8_t*>(recvbuf) + (size_t)r * bytes,
+                      static_cast<const uint8_t*>(send[r]) + (size_t)rank * bytes, bytes, cudaMemcpyDeviceToDevice, s);
+    }
+    cudaEventRecord(done[rank], s);
+    barrier();
+    for (int r = 0; r < world; ++r) cudaStreamWaitEvent(s, done[r], 0);
+    barrier();
+  }
+};
+
 struct dit_ctx {
   dit_config cfg;
   int device = 0;
@@ -105,12 +146,12 @@ struct dit_ctx {
   // SP
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  LocalGroup* local_group = nullptr;
+  bf16_t* sp = nullptr;              // [send1 | recv1 | send2 | recv2] at P > 1
+  bf16_t* qkv = nullptr;             // attention layout [3][B][H/P][N][d]
   // workspace carve-outs
   float* h = nullptr;
   bf16_t* u = nullptr;
-  bf16_t* q = nullptr;
-  bf16_t* k = nullptr;
-  bf16_t* v = nullptr;
   bf16_t* o = nullptr;
   bf16_t* cat = nullptr;
   bf16_t* sext = nullptr;
@@ -197,7 +238,7 @@ bool cfg_valid(const dit_config* c, std::string* why) {
 }
 
 struct Layout {
-  size_t h, u, q, k, v, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, total;
+  size_t h, u, qkv, sp, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, total;
   size_t pool_bytes_per_slot;
 };
 
@@ -213,9 +254,8 @@ Layout layout_of(const dit_config& c) {
   Carve cv;
   L.h = cv.take(R * D * 4);
   L.u = cv.take(R * D * 2);
-  L.q = cv.take(R * D * 2);
-  L.k = cv.take(R * D * 2);
-  L.v = cv.take(R * D * 2);
+  L.qkv = cv.take(3 * R * D * 2);
+  L.sp = cv.take(4 * R * D * 2);
   L.o = cv.take(R * D * 2);
   L.cat = cv.take(R * (D + F) * 2);
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
@@ -286,9 +326,8 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   uint8_t* w = c->ws;
   c->h = reinterpret_cast<float*>(w + L.h);
   c->u = reinterpret_cast<bf16_t*>(w + L.u);
-  c->q = reinterpret_cast<bf16_t*>(w + L.q);
-  c->k = reinterpret_cast<bf16_t*>(w + L.k);
-  c->v = reinterpret_cast<bf16_t*>(w + L.v);
+  c->qkv = reinterpret_cast<bf16_t*>(w + L.qkv);
+  c->sp = reinterpret_cast<bf16_t*>(w + L.sp);
   c->o = reinterpret_cast<bf16_t*>(w + L.o);
   c->cat = reinterpret_cast<bf16_t*>(w + L.cat);
   c->sext = reinterpret_cast<bf16_t*>(w + L.sext);
@@ -622,6 +661,41 @@ extern "C" int controlnet_inject(dit_ctx* c, int32_t slot, int32_t block, const 
 }
 
 // ------------------------------------------------------------------ SP
+extern "C" void* dit_local_group_create(int32_t world) {
+  if (world < 1 || world > 64) return nullptr;
+  LocalGroup* g = new LocalGroup();
+  g->world = world;
+  g->send.assign(world, nullptr);
+  g->ready.assign(world, nullptr);
+  g->done.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming);
+  }
+  return g;
+}
+
+extern "C" void dit_local_group_destroy(void* grp) {
+  LocalGroup* g = static_cast<LocalGroup*>(grp);
+  if (!g) return;
+  for (auto e : g->ready) cudaEventDestroy(e);
+  for (auto e : g->done) cudaEventDestroy(e);
+  delete g;
+}
+
+extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
+  if (!c) return DIT_EINVAL;
+  LocalGroup* g = static_cast<LocalGroup*>(grp);
+  if (!g || rank < 0 || rank >= g->world) return c->fail(DIT_EINVAL, "bad local group / rank");
+  if (c->H % g->world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", g->world, c->H);
+  c->local_group = g;
+  c->world = g->world;
+  c->rank = rank;
+  c->plan_B = -1;
+  c->rope_key[0] = -1;
+  return DIT_OK;
+}
+
 extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
   if (!c) return DIT_EINVAL;
   if (world < 1 || rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad world/rank %d/%d", world, rank);
@@ -629,6 +703,8 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   if (world == 1) {
     c->world = 1;
     c->rank = 0;
+    c->local_group = nullptr;
+    c->rope_key[0] = -1;
     return DIT_OK;
   }
   if (!uid) return c->fail(DIT_EINVAL, "nccl unique id is NULL");
@@ -640,9 +716,11 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   if (c->comm) ncclCommDestroy(c->comm);
   c->comm = comm;
+  c->local_group = nullptr;
   c->world = world;
   c->rank = rank;
   c->plan_B = -1;
+  c->rope_key[0] = -1;
   return DIT_OK;
 }
 
@@ -873,7 +951,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     return c->fail(DIT_ESHAPE, "tokens (%d img, %d txt) exceed the configured maxima", Ni, Nt);
   const int P = c->world;
   if (Ni % P || Nt % P) return c->fail(DIT_EPARALLEL, "world %d does not divide Ni=%d / Nt=%d", P, Ni, Nt);
-  if (P > 1) return c->fail(DIT_EPARALLEL, "sequence parallel step not built yet");
+  if (P > 1 && !c->comm && !c->local_group) return c->fail(DIT_EPARALLEL, "sp_init not called");
   if (!b->adapter_id || !b->sigma || !b->sigma_next || !b->guidance)
     return c->fail(DIT_EINVAL, "host arrays adapter_id/sigma/sigma_next/guidance required");
   if (!b->latents_in || !b->latents_out || !b->txt || !b->pooled) return c->fail(DIT_EINVAL, "NULL device pointer");
@@ -1032,6 +1110,62 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   }
 
   const float scale_log2 = 1.4426950408889634f / std::sqrt((float)d);
+  // ---- attention with the Ulysses exchange around it (P > 1): QKV epilogue wrote
+  // [P][3][B][H/P][N_loc][d] -> a2a -> global order -> attention on H/P heads over the
+  // full sequence -> O in [P][B][N_loc][H/P*d] -> a2a -> scatter into the local rows.
+  const int Hl = H / P, Nglob = P * N;
+  auto a2a = [&](const void* snd, void* rcv, size_t count) -> int {
+    prof_begin(c, s);
+    if (c->comm) {
+      ncclResult_t r = ncclAlltoAll(snd, rcv, count, ncclBfloat16, c->comm, s);
+      if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclAlltoAll: %s", ncclGetErrorString(r));
+    } else {
+      c->local_group->a2a(c->rank, snd, rcv, count * 2, s);
+    }
+    prof_end(c, s, 5, 0.0);
+    c->launches++;
+    return DIT_OK;
+  };
+  auto attention_stage = [&](void* out, int ld_out, int split) -> int {
+    const size_t pp1 = (size_t)3 * B * Hl * N * d, pp2 = (size_t)B * N * Hl * d;
+    bf16_t* send1 = c->sp;
+    bf16_t* recv1 = send1 + (size_t)P * pp1;
+    bf16_t* send2 = recv1 + (size_t)P * pp1;
+    bf16_t* recv2 = send2 + (size_t)P * pp2;
+    if (P > 1) {
+      CK(a2a(send1, recv1, pp1));
+      CKK(sp_gather_qkv_launch(recv1, c->qkv, P, B, Hl, nt, ni, d, s), 6, 0.0);
+    }
+    AttnParams ap;
+    memset(&ap, 0, sizeof(ap));
+    const size_t sec = (size_t)B * Hl * Nglob * d;
+    ap.q = c->qkv;
+    ap.k = c->qkv + sec;
+    ap.v = c->qkv + 2 * sec;
+    ap.B = B;
+    ap.H = Hl;
+    ap.N = Nglob;
+    ap.d = d;
+    ap.scale_log2 = scale_log2;
+    ap.nt = nt;
+    ap.ni = ni;
+    ap.Nt = Nt;
+    if (P == 1) {
+      ap.out = out;
+      ap.ld_out = ld_out;
+      ap.split = split;
+    } else {
+      ap.out = send2;
+      ap.ld_out = Hl * d;
+      ap.split = 2;
+    }
+    CKK(attention_launch(ap, s), 1, 4.0 * B * (double)Nglob * Nglob * Hl * d);
+    if (P > 1) {
+      CK(a2a(send2, recv2, pp2));
+      CKK(sp_scatter_o_launch(recv2, out, ld_out, split, P, B, Hl, nt, ni, d, s), 6, 0.0);
+    }
+    return DIT_OK;
+  };
   auto lnmod2 = [&](int modT, int modI, int sh, int sc) -> int {
     LnModParams lp;
     memset(&lp, 0, sizeof(lp));
@@ -1083,9 +1217,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.kind = EPI_QKV;
       e.joint_n = N;
       e.D = D;
-      e.q = c->q;
-      e.k = c->k;
-      e.v = c->v;
+      e.qkv = (P == 1) ? c->qkv : c->sp;
+      e.batch = B;
+      e.sp_world = P;
       e.rope = c->rope;
       e.qkv_cols = 3 * D;
       e.heads = H;
@@ -1109,24 +1243,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       }
       CK(run_gemm(c, p, 2, s));
     }
-    {
-      AttnParams ap;
-      memset(&ap, 0, sizeof(ap));
-      ap.q = c->q;
-      ap.k = c->k;
-      ap.v = c->v;
-      ap.B = B;
-      ap.H = H;
-      ap.N = N;
-      ap.d = d;
-      ap.scale_log2 = scale_log2;
-      ap.out = c->o;
-      ap.ld_out = D;
-      ap.split = 1;
-      ap.nt = nt;
-      ap.ni = ni;
-      CKK(attention_launch(ap, s), 1, 4.0 * B * (double)N * N * D);
-    }
+    CK(attention_stage(c->o, D, 1));
     bf16_t* oT = c->o;
     bf16_t* oI = c->o + (size_t)Mt * D;
     auto resid_pair = [&](const Lin& LT, const Lin& LI, const void* AT, const void* AI, int K, int lda, int goff,
@@ -1236,9 +1353,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.joint_off = 0;
       e.joint_n = N;
       e.D = D;
-      e.q = c->q;
-      e.k = c->k;
-      e.v = c->v;
+      e.qkv = (P == 1) ? c->qkv : c->sp;
+      e.batch = B;
+      e.sp_world = P;
       e.q_gamma = S.qn;
       e.k_gamma = S.kn;
       e.rope = c->rope;
@@ -1253,22 +1370,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0], sext_of(c, 0));
       CK(run_gemm(c, &p, 1, s));
     }
-    {
-      AttnParams ap;
-      memset(&ap, 0, sizeof(ap));
-      ap.q = c->q;
-      ap.k = c->k;
-      ap.v = c->v;
-      ap.B = B;
-      ap.H = H;
-      ap.N = N;
-      ap.d = d;
-      ap.scale_log2 = scale_log2;
-      ap.out = c->cat;
-      ap.ld_out = D + F;
-      ap.split = 0;
-      CKK(attention_launch(ap, s), 1, 4.0 * B * (double)N * N * D);
-    }
+    CK(attention_stage(c->cat, D + F, 0));
     if (any_lora) {
       const void* A[1] = {c->cat};
       const int M[1] = {Mj}, K[1] = {D + F}, ld[1] = {D + F};
@@ -1344,7 +1446,7 @@ extern "C" int dit_profile(dit_ctx* c, int enable) {
 }
 
 extern "C" int dit_profile_read(dit_ctx* c, int kind, double* total_ms, double* flops, int* launches) {
-  if (!c || kind < 0 || kind > 4) return DIT_EINVAL;
+  if (!c || kind < 0 || kind > 6) return DIT_EINVAL;
   double ms = 0, fl = 0;
   int n = 0;
   for (auto& r : c->prof) {

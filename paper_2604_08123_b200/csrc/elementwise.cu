@@ -223,6 +223,61 @@ cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ Ulysses SP layout
+// 16-byte granules; rank r_s's local row i is global joint row
+//   i <  nt : r_s*nt + i            (txt)
+//   i >= nt : P*nt + r_s*ni + i-nt   (img)
+__global__ void sp_gather_qkv_kernel(const uint4* __restrict__ recv, uint4* __restrict__ out, int P, int B, int Hl,
+                                     int nt, int ni, int g_per_row, long long total) {
+  const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gidx >= total) return;
+  const int nloc = nt + ni, N = P * nloc;
+  long long t = gidx;
+  const int g = (int)(t % g_per_row); t /= g_per_row;
+  const int i = (int)(t % nloc); t /= nloc;
+  const int hl = (int)(t % Hl); t /= Hl;
+  const int b = (int)(t % B); t /= B;
+  const int sec = (int)(t % 3); t /= 3;
+  const int rs = (int)t;
+  const int n = (i < nt) ? rs * nt + i : P * nt + rs * ni + (i - nt);
+  out[((((long long)sec * B + b) * Hl + hl) * N + n) * g_per_row + g] = recv[gidx];
+}
+cudaError_t sp_gather_qkv_launch(const void* recv, void* out, int P, int B, int Hl, int nt_loc, int ni_loc, int d,
+                                 cudaStream_t s) {
+  const int gpr = d / 8;
+  const long long total = (long long)P * 3 * B * Hl * (nt_loc + ni_loc) * gpr;
+  if (total == 0) return cudaSuccess;
+  sp_gather_qkv_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(recv),
+                                                                      reinterpret_cast<uint4*>(out), P, B, Hl,
+                                                                      nt_loc, ni_loc, gpr, total);
+  return cudaGetLastError();
+}
+
+__global__ void sp_scatter_o_kernel(const uint4* __restrict__ recv, bf16* __restrict__ out, int ld_out, int split,
+                                    int P, int B, int Hl, int nt, int ni, int d, long long total) {
+  const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gidx >= total) return;
+  const int nloc = nt + ni, gpr = Hl * d / 8;
+  long long t = gidx;
+  const int g = (int)(t % gpr); t /= gpr;
+  const int i = (int)(t % nloc); t /= nloc;
+  const int b = (int)(t % B); t /= B;
+  const int rs = (int)t;
+  long long row;
+  if (split) row = (i < nt) ? (long long)b * nt + i : (long long)B * nt + (long long)b * ni + (i - nt);
+  else row = (long long)b * nloc + i;
+  *reinterpret_cast<uint4*>(out + row * ld_out + (long long)rs * Hl * d + g * 8) = recv[gidx];
+}
+cudaError_t sp_scatter_o_launch(const void* recv, void* out, int ld_out, int split, int P, int B, int Hl, int nt_loc,
+                                int ni_loc, int d, cudaStream_t s) {
+  const long long total = (long long)P * B * (nt_loc + ni_loc) * (Hl * d / 8);
+  if (total == 0) return cudaSuccess;
+  sp_scatter_o_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(recv),
+                                                                     reinterpret_cast<bf16*>(out), ld_out, split, P,
+                                                                     B, Hl, nt_loc, ni_loc, d, total);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ synthetic fill (synth/__init__.py)
 DEVI uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;

@@ -159,8 +159,10 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
             }
           }
         }
-        bf16* dst = reinterpret_cast<bf16*>(sec == 0 ? E.q : (sec == 1 ? E.k : E.v));
-        dst += ((size_t)(b * E.heads + head) * E.seq_len + (E.joint_off + nloc)) * d;
+        const int hl_n = E.heads / E.sp_world;
+        const int dest = head / hl_n, hl = head - dest * hl_n;
+        bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
+                    ((((size_t)(dest * 3 + sec) * E.batch + b) * hl_n + hl) * E.seq_len + (E.joint_off + nloc)) * d;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j < nch) {

@@ -43,10 +43,11 @@ struct EpiParams {
   void* out;
   int ld_out;
   int out_col0;
-  // QKV scatter
-  void* q;
-  void* k;
-  void* v;
+  // QKV scatter into the (SP send) layout [P][3][B][H/P][seq_len][d]; P = 1 is the
+  // attention layout [3][B][H][N][d] itself.
+  void* qkv;
+  int batch;                 // B
+  int sp_world;              // P
   const void* q_gamma;       // bf16 [d]
   const void* k_gamma;
   const float2* rope;        // [joint_n][d/2] (cos, sin)
@@ -105,15 +106,40 @@ struct AttnParams {
   const void* q;
   const void* k;
   const void* v;
-  int B, H, N, d;
+  int B, H, N, d;      // H = heads on this rank, N = full (global) joint sequence
   float scale_log2;    // log2(e) / sqrt(d)
   void* out;           // bf16
   int ld_out;          // elements per output row
-  int split;           // 1: rows n < Nt -> txt block, else img block (double blocks)
-  int nt;              // txt rows per request (split mode)
-  int ni;              // img rows per request (split mode)
+  int split;           // 0 joint rows b*N+n; 1 stream-split (txt rows then img rows); 2 SP send layout
+  int nt;              // txt rows per request (split: global Nt; SP: local nt)
+  int ni;              // img rows per request (split: global Ni; SP: local ni)
+  int Nt;              // global txt rows (SP mode)
 };
+// Output row of query token n (global joint order) of request b; SP mode also
+// returns the destination rank in *dest (rows are then [dest][B][N_loc]).
+__host__ __device__ inline long long attn_out_row(const AttnParams& p, int b, int n) {
+  if (p.split == 1)
+    return (n < p.nt) ? (long long)b * p.nt + n : (long long)p.B * p.nt + (long long)b * p.ni + (n - p.nt);
+  if (p.split == 2) {
+    const int nloc = p.nt + p.ni;
+    int dest, i;
+    if (n < p.Nt) { dest = n / p.nt; i = n - dest * p.nt; }
+    else { dest = (n - p.Nt) / p.ni; i = p.nt + (n - p.Nt) - dest * p.ni; }
+    return ((long long)dest * p.B + b) * nloc + i;
+  }
+  return (long long)b * p.N + n;
+}
 cudaError_t attention_launch(const AttnParams& p, cudaStream_t s);
+
+// ------------------------------------------------------------------ Ulysses SP layout kernels
+// recv [P][3][B][Hl][nloc][d] (chunk r_s = rank r_s's tokens, my heads) ->
+// attention layout [3][B][Hl][N][d], global joint order (txt of all ranks, then img).
+cudaError_t sp_gather_qkv_launch(const void* recv, void* out, int P, int B, int Hl, int nt_loc, int ni_loc, int d,
+                                 cudaStream_t s);
+// recv [P][B][nloc][Hl*d] (chunk r_s = heads of rank r_s for my tokens) -> rows of
+// `out` (split = 1 stream-split rows, 0 joint rows b*nloc+i) at columns r_s*Hl*d.
+cudaError_t sp_scatter_o_launch(const void* recv, void* out, int ld_out, int split, int P, int B, int Hl, int nt_loc,
+                                int ni_loc, int d, cudaStream_t s);
 
 // ------------------------------------------------------------------ elementwise / skinny
 // u[r] = (1 + scale_b) * LN(h[jrow(r)]) + shift_b  (bf16 out), rows of up to 2 streams.

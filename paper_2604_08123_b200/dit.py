@@ -63,6 +63,9 @@ EXPORTS = {
     "dit_profile_reset": (C.c_int, [C.c_void_p]),
     "dit_fill_synthetic": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64, C.c_float, C.c_float,
                                      C.c_void_p]),
+    "dit_local_group_create": (C.c_void_p, [C.c_int32]),
+    "dit_local_group_destroy": (None, [C.c_void_p]),
+    "sp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "dit_debug_row_adapter": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
     "dit_debug_shard_map": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
 }
@@ -181,6 +184,9 @@ class DiT:
     def sp_init(self, world: int, rank: int, nccl_uid: Optional[bytes] = None):
         buf = C.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
         _check(self.lib.sp_init(self.ctx, world, rank, buf), self.ctx)
+
+    def sp_init_local(self, group, rank: int):
+        _check(self.lib.sp_init_local(self.ctx, group, rank), self.ctx)
 
     def make_batch(self, batch_size, img_h, img_w, txt_tokens, adapter_id, sigma, sigma_next, guidance,
                    latents_in, latents_out, txt, pooled, v_out=None, cn_scale=None) -> dit_batch:

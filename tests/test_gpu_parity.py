@@ -138,3 +138,66 @@ def test_head_dim_128_tcgen05_attention(torch_cuda, grid, nt):
     x_o, v_o = O.dit_step(cfg, W, batch, {3: oracle_adapter(cfg, 8, 0)[0]})
     check(v, v_o, "v")
     check(lat, x_o, "latents")
+
+
+def _shard_step(models, batch, P):
+    """Run one dit_step on P in-process ranks (one host thread + stream each); gather v, latents."""
+    import concurrent.futures as cf
+    import torch
+    from paper_2604_08123_b200.synthetic import _bits_to_bf16_tensor
+    B, ni, nt = batch.batch, batch.img_tokens, batch.txt_tokens
+    nil, ntl = ni // P, nt // P
+    outs, vs, keep = [], [], []
+    cbs, streams = [], []
+    for r, m in enumerate(models):
+        lat = torch.from_numpy(np.ascontiguousarray(batch.latents[:, r * nil:(r + 1) * nil])).to(m.dev)
+        txt = _bits_to_bf16_tensor(np.ascontiguousarray(batch.txt[:, r * ntl:(r + 1) * ntl]), m.dev)
+        pooled = _bits_to_bf16_tensor(batch.pooled, m.dev)
+        out, v = torch.empty_like(lat), torch.empty_like(lat)
+        keep += [lat, txt, pooled]
+        outs.append(out)
+        vs.append(v)
+        cbs.append(m.make_batch(B, batch.img_h, batch.img_w, nt, batch.adapter_id, batch.sigma, batch.sigma_next,
+                                batch.guidance, lat, out, txt, pooled, v_out=v, cn_scale=batch.cn_scale))
+        streams.append(torch.cuda.Stream())
+    torch.cuda.synchronize()
+    with cf.ThreadPoolExecutor(P) as ex:
+        list(ex.map(lambda r: models[r].dit_step(cbs[r], stream=streams[r]), range(P)))
+    torch.cuda.synchronize()
+    v = np.concatenate([x.cpu().numpy() for x in vs], axis=1)
+    lat = np.concatenate([x.cpu().numpy() for x in outs], axis=1)
+    return lat, v
+
+
+@pytest.mark.parametrize("P,hidden,heads", [(2, 512, 4), (4, 512, 4), (2, 128, 4), (4, 128, 4)])
+def test_sequence_parallel_local_group(torch_cuda, P, hidden, heads):
+    """Ulysses SP at P ranks (in-process group, one GPU): bitwise equal to P = 1 (pin P10) and oracle parity.
+
+    hidden 512 / 4 heads -> d = 128 (tcgen05 attention); hidden 128 / 4 heads -> d = 32 (mma.sync kernel).
+    """
+    from paper_2604_08123_b200 import dit as D
+    d = hidden // heads
+    cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=hidden, heads=heads, depth_single=1,
+                              rope_axes=(16, 56, 56) if d == 128 else (4, 14, 14))
+    B, hh, ww, nt = 2, 16, 16, 64
+    ref = _model(cfg, B, hh * ww, nt, rank=8, adapters=1)
+    ref.register_synthetic_lora(5, rank=8, index=0)
+    batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([5, -1], dtype=np.int32)
+    lat1, v1 = ref.step(batch)
+    group = D.load_library().dit_local_group_create(P)
+    models = []
+    for r in range(P):
+        m = _model(cfg, B, hh * ww, nt, rank=8, adapters=1)
+        m.register_synthetic_lora(5, rank=8, index=0)
+        m.sp_init_local(group, r)
+        models.append(m)
+    latP, vP = _shard_step(models, batch, P)
+    np.testing.assert_array_equal(vP, v1)
+    np.testing.assert_array_equal(latP, lat1)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = O.dit_step(cfg, W, batch, {5: oracle_adapter(cfg, 8, 0)[0]})
+    check(vP, v_o, "v")
+    for m in models:
+        m.close()
+    D.load_library().dit_local_group_destroy(group)
