@@ -208,6 +208,17 @@ void* dit_local_group_create(int32_t world);
 void dit_local_group_destroy(void* group);
 int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 
+/* ncclGetUniqueId for sp_init (rank 0 calls it, the caller broadcasts the 128 bytes). */
+int dit_nccl_unique_id(void* out128);
+
+/* Host copy of the sequence-parallel index maps the kernels use (bit-exact
+ * layout tests, no GPU needed).  which: 0 shard map (local row -> global joint
+ * row b*N+n), 1 QKV send layout, 2 gather (recv -> attention layout), 3 O send
+ * rows, 4 O scatter rows (stream-split).  Writes up to cap int64 entries to
+ * out; returns the number of entries, or -status. */
+int64_t dit_sp_layout(int32_t which, int32_t world, int32_t rank, int32_t B, int32_t H, int32_t Nt, int32_t Ni,
+                      int64_t* out, int64_t cap);
+
 /* Integer plan artefacts of `batch` (host outputs; bit-exact tests):
  * row_adapter: int32 [rows] LoRA pool slot of each local row of the
  *   txt-stream GEMM followed by the img-stream GEMM (-1 = none), rows =

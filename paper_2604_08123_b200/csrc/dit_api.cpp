@@ -1514,6 +1514,58 @@ extern "C" int dit_debug_row_adapter(dit_ctx* c, const dit_batch* b, int32_t* ou
   return rows;
 }
 
+extern "C" int dit_nccl_unique_id(void* out128) {
+  if (!out128) return DIT_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DIT_ENCCL;
+  memcpy(out128, &id, sizeof(id));
+  return DIT_OK;
+}
+
+// Host export of the SP index maps the kernels use (kernels.h), for CPU tests.
+//  which 0: shard map, out[b*nloc + i] = global joint row b*N + n of local row i
+//  which 1: QKV send: out[sp_attn-style (sec,b,head,i) index over [3][B][H][nloc]] = send d-vector index
+//  which 2: gather: out[recv d-vector index] = attention-layout d-vector index
+//  which 3: O send: out[(b, n, hl) over [B][N][Hl]] = send2 row index (attn_out_row, SP mode)
+//  which 4: scatter (split = 1): out[recv2 row (rs, b, i)] = local output row
+extern "C" int64_t dit_sp_layout(int32_t which, int32_t world, int32_t rank, int32_t B, int32_t H, int32_t Nt,
+                                 int32_t Ni, int64_t* out, int64_t cap) {
+  const int P = world;
+  if (P < 1 || rank < 0 || rank >= P || B < 1 || H % P || Nt % P || Ni % P || !out) return -DIT_EINVAL;
+  const int nt = Nt / P, ni = Ni / P, nloc = nt + ni, N = Nt + Ni, Hl = H / P;
+  int64_t k = 0;
+  auto put = [&](int64_t v) { if (k < cap) out[k] = v; ++k; };
+  if (which == 0) {
+    for (int b = 0; b < B; ++b)
+      for (int i = 0; i < nloc; ++i) put((int64_t)b * N + sp_global_row(P, nt, ni, rank, i));
+  } else if (which == 1) {
+    for (int sec = 0; sec < 3; ++sec)
+      for (int b = 0; b < B; ++b)
+        for (int h = 0; h < H; ++h)
+          for (int i = 0; i < nloc; ++i) put(sp_qkv_send_vec(B, Hl, nloc, h / Hl, sec, b, h % Hl, i));
+  } else if (which == 2) {
+    for (int rs = 0; rs < P; ++rs)
+      for (int sec = 0; sec < 3; ++sec)
+        for (int b = 0; b < B; ++b)
+          for (int hl = 0; hl < Hl; ++hl)
+            for (int i = 0; i < nloc; ++i) put(sp_attn_vec(B, Hl, N, sec, b, hl, sp_global_row(P, nt, ni, rs, i)));
+  } else if (which == 3) {
+    AttnParams p;
+    memset(&p, 0, sizeof(p));
+    p.B = B; p.H = Hl; p.N = N; p.split = 2; p.nt = nt; p.ni = ni; p.Nt = Nt;
+    for (int b = 0; b < B; ++b)
+      for (int n = 0; n < N; ++n)
+        for (int hl = 0; hl < Hl; ++hl) put(attn_out_row(p, b, n));
+  } else if (which == 4) {
+    for (int rs = 0; rs < P; ++rs)
+      for (int b = 0; b < B; ++b)
+        for (int i = 0; i < nloc; ++i) put(sp_local_row(1, B, nt, ni, b, i));
+  } else {
+    return -DIT_EINVAL;
+  }
+  return k;
+}
+
 extern "C" int dit_debug_shard_map(dit_ctx* c, const dit_batch* b, int32_t* out, int cap) {
   if (!c || !out) return -DIT_EINVAL;
   std::vector<int> rs;

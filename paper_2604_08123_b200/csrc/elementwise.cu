@@ -239,8 +239,8 @@ __global__ void sp_gather_qkv_kernel(const uint4* __restrict__ recv, uint4* __re
   const int b = (int)(t % B); t /= B;
   const int sec = (int)(t % 3); t /= 3;
   const int rs = (int)t;
-  const int n = (i < nt) ? rs * nt + i : P * nt + rs * ni + (i - nt);
-  out[((((long long)sec * B + b) * Hl + hl) * N + n) * g_per_row + g] = recv[gidx];
+  const int n = sp_global_row(P, nt, ni, rs, i);
+  out[sp_attn_vec(B, Hl, N, sec, b, hl, n) * g_per_row + g] = recv[gidx];
 }
 cudaError_t sp_gather_qkv_launch(const void* recv, void* out, int P, int B, int Hl, int nt_loc, int ni_loc, int d,
                                  cudaStream_t s) {
@@ -263,9 +263,7 @@ __global__ void sp_scatter_o_kernel(const uint4* __restrict__ recv, bf16* __rest
   const int i = (int)(t % nloc); t /= nloc;
   const int b = (int)(t % B); t /= B;
   const int rs = (int)t;
-  long long row;
-  if (split) row = (i < nt) ? (long long)b * nt + i : (long long)B * nt + (long long)b * ni + (i - nt);
-  else row = (long long)b * nloc + i;
+  const long long row = sp_local_row(split, B, nt, ni, b, i);
   *reinterpret_cast<uint4*>(out + row * ld_out + (long long)rs * Hl * d + g * 8) = recv[gidx];
 }
 cudaError_t sp_scatter_o_launch(const void* recv, void* out, int ld_out, int split, int P, int B, int Hl, int nt_loc,

@@ -162,7 +162,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         const int hl_n = E.heads / E.sp_world;
         const int dest = head / hl_n, hl = head - dest * hl_n;
         bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
-                    ((((size_t)(dest * 3 + sec) * E.batch + b) * hl_n + hl) * E.seq_len + (E.joint_off + nloc)) * d;
+                    (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j < nch) {

@@ -131,6 +131,27 @@ __host__ __device__ inline long long attn_out_row(const AttnParams& p, int b, in
 }
 cudaError_t attention_launch(const AttnParams& p, cudaStream_t s);
 
+// ------------------------------------------------------------------ Ulysses SP index maps
+// (host + device: the kernels use these, and dit_sp_layout exports them for tests)
+// Global joint row (within one request) of rank rs's local row i (local rows: nt txt then ni img).
+__host__ __device__ inline int sp_global_row(int P, int nt, int ni, int rs, int i) {
+  return i < nt ? rs * nt + i : P * nt + rs * ni + (i - nt);
+}
+// d-vector index of (dest, sec, b, hl, i) in the QKV send layout [P][3][B][Hl][nloc].
+__host__ __device__ inline long long sp_qkv_send_vec(int B, int Hl, int nloc, int dest, int sec, int b, int hl,
+                                                     int i) {
+  return (((long long)(dest * 3 + sec) * B + b) * Hl + hl) * nloc + i;
+}
+// d-vector index of (sec, b, hl, n) in the attention layout [3][B][Hl][N].
+__host__ __device__ inline long long sp_attn_vec(int B, int Hl, int N, int sec, int b, int hl, int n) {
+  return (((long long)sec * B + b) * Hl + hl) * N + n;
+}
+// Local output row of (b, i): split = 1 stream-split (txt rows of all requests first), 0 joint.
+__host__ __device__ inline long long sp_local_row(int split, int B, int nt, int ni, int b, int i) {
+  if (split) return (i < nt) ? (long long)b * nt + i : (long long)B * nt + (long long)b * ni + (i - nt);
+  return (long long)b * (nt + ni) + i;
+}
+
 // ------------------------------------------------------------------ Ulysses SP layout kernels
 // recv [P][3][B][Hl][nloc][d] (chunk r_s = rank r_s's tokens, my heads) ->
 // attention layout [3][B][Hl][N][d], global joint order (txt of all ranks, then img).

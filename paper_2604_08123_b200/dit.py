@@ -66,6 +66,9 @@ EXPORTS = {
     "dit_local_group_create": (C.c_void_p, [C.c_int32]),
     "dit_local_group_destroy": (None, [C.c_void_p]),
     "sp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "dit_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "dit_sp_layout": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                  C.POINTER(C.c_int64), C.c_int64]),
     "dit_debug_row_adapter": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
     "dit_debug_shard_map": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
 }
@@ -244,6 +247,24 @@ class DiT:
         import torch
         s = stream if stream is not None else torch.cuda.current_stream()
         return C.c_void_p(s.cuda_stream)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load_library().dit_nccl_unique_id(buf))
+    return buf.raw
+
+
+def sp_layout(which, world, rank, B, H, Nt, Ni):
+    """Host copy of the SP index maps used by the kernels (see include/dit.h)."""
+    import numpy as np
+    lib = load_library()
+    cap = 3 * B * H * (Nt + Ni) * max(world, 1) + 16
+    out = (C.c_int64 * cap)()
+    n = lib.dit_sp_layout(which, world, rank, B, H, Nt, Ni, out, cap)
+    if n < 0:
+        raise DitError(-n, "sp_layout")
+    return np.frombuffer(out, dtype=np.int64, count=n).copy()
 
 
 def fill_synthetic(t, seed: int, tensor_id: int, scale: float, offset: float, stream=None):
