@@ -277,7 +277,7 @@ def run_gpu(args):
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     model.profile(False)
-    prof = {k: model.profile_read(k) for k in range(7)}
+    prof = {k: model.profile_read(k) for k in list(range(7)) + list(range(10, 19))}
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], device=dev)
@@ -354,6 +354,10 @@ def run_gpu(args):
             "other": {"ms_per_step": prof[4][0] / args.steps},
             "sp_all_to_all": {"ms_per_step": prof[5][0] / args.steps, "launches_per_step": prof[5][2] / args.steps},
             "sp_layout": {"ms_per_step": prof[6][0] / args.steps},
+            "gemm_by_type": {name: {"ms_per_step": prof[k][0] / args.steps,
+                                    "tflops": prof[k][1] / (prof[k][0] / 1e3) / 1e12 if prof[k][0] > 0 else None}
+                             for k, name in zip(range(10, 19), ["embed", "dbl_qkv", "dbl_proj", "dbl_fc1", "dbl_fc2",
+                                                                "sgl_linear1", "sgl_linear2", "final", "lora_shrink"])},
         },
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,

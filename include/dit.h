@@ -186,7 +186,9 @@ int dit_last_launch_count(const dit_ctx* ctx);
  * the launch stream around every kernel while enabled).  kind: 0 tcgen05
  * GEMM (all projections, LoRA shrink/expand), 1 attention, 2 LN-modulate,
  * 3 modulation skinny GEMM, 4 other small kernels, 5 SP all-to-all (NCCL),
- * 6 SP layout gather/scatter kernels.  dit_profile_read
+ * 6 SP layout gather/scatter kernels; GEMM sub-kinds (included in 0):
+ * 10 embeddings, 11 double QKV, 12 double proj, 13 double fc1, 14 double fc2,
+ * 15 single linear1, 16 single linear2, 17 final, 18 LoRA shrink.  dit_profile_read
  * synchronises on the recorded events and returns the summed device time,
  * the summed ALGORITHMIC flops and the number of launches of that kind since
  * the last dit_profile_reset. */

@@ -189,6 +189,7 @@ struct dit_ctx {
   size_t ev_next = 0;
   cudaEvent_t prof_a = nullptr;
   std::vector<int> slot_rank_h;
+  int gemm_label = 0;   // profiling sub-kind of the next GEMM launch (10..18)
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -870,7 +871,7 @@ int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s, double flop
   if (t == 0) return DIT_OK;
   prof_begin(c, s);
   cudaError_t e = gemm_launch(a, c->num_sms, s);
-  prof_end(c, s, 0, flops);
+  prof_end(c, s, c->gemm_label, flops);
   c->launches++;
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   return DIT_OK;
@@ -892,6 +893,7 @@ int run_shrink(dit_ctx* c, int np, const void* const* A, const int* M, const int
     if (R[i]->n_shrink > 0 && c->pools[module[i]].A)
       p[k++] = shrink_problem(c, A[i], M[i], K[i], lda[i], *R[i], module[i], sext_of(c, row_base[i]));
   if (k == 0) return DIT_OK;
+  c->gemm_label = 18;
   return run_gemm(c, p, k, s);
 }
 
@@ -1106,6 +1108,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     et.joint_off = 0;
     GemmProblem p[2] = {base_problem(c, c->xb, Mi, C, C, c->img_in, ei),
                         base_problem(c, b->txt, Mt, Ct, Ct, c->txt_in, et)};
+    c->gemm_label = 10;
     CK(run_gemm(c, p, 2, s));
   }
 
@@ -1241,6 +1244,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         add_lora_ext(c, p[0], c->rs[0], T.lora[0], sext_of(c, 0));
         add_lora_ext(c, p[1], c->rs[1], I.lora[0], sext_of(c, Mt));
       }
+      c->gemm_label = 11;
       CK(run_gemm(c, p, 2, s));
     }
     CK(attention_stage(c->o, D, 1));
@@ -1274,6 +1278,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         add_lora_ext(c, p[0], c->rs[0], modT_l, sext_of(c, 0));
         add_lora_ext(c, p[1], c->rs[1], modI_l, sext_of(c, Mt));
       }
+      c->gemm_label = goff == 2 * D ? 12 : 14;
       return run_gemm(c, p, 2, s);
     };
     CK(shrink2(oT, oI, D, D, T.lora[1], I.lora[1]));
@@ -1301,6 +1306,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         add_lora_ext(c, p[0], c->rs[0], T.lora[2], sext_of(c, 0));
         add_lora_ext(c, p[1], c->rs[1], I.lora[2], sext_of(c, Mt));
       }
+      c->gemm_label = 13;
       CK(run_gemm(c, p, 2, s));
     }
     // deferred ControlNet input of block i: wait right before its consumer
@@ -1368,6 +1374,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.out_col0 = D;
       GemmProblem p = base_problem(c, c->u, Mj, D, D, S.l1, e);
       if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0], sext_of(c, 0));
+      c->gemm_label = 15;
       CK(run_gemm(c, &p, 1, s));
     }
     CK(attention_stage(c->cat, D + F, 0));
@@ -1394,6 +1401,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.gate_off = mj + 2 * D;
       GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
       if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1], sext_of(c, 0));
+      c->gemm_label = 16;
       CK(run_gemm(c, &p, 1, s));
     }
   }
@@ -1426,6 +1434,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     e.v_out = b->v_out;
     e.dsig = c->p_dsig;
     GemmProblem p = base_problem(c, c->u, Mi, D, D, c->fin_lin, e);
+    c->gemm_label = 17;
     CK(run_gemm(c, &p, 1, s));
   }
 
@@ -1446,11 +1455,12 @@ extern "C" int dit_profile(dit_ctx* c, int enable) {
 }
 
 extern "C" int dit_profile_read(dit_ctx* c, int kind, double* total_ms, double* flops, int* launches) {
-  if (!c || kind < 0 || kind > 6) return DIT_EINVAL;
+  if (!c || kind < 0 || kind > 18) return DIT_EINVAL;
   double ms = 0, fl = 0;
   int n = 0;
   for (auto& r : c->prof) {
-    if (r.kind != kind) continue;
+    const bool match = (r.kind == kind) || (kind == 0 && r.kind >= 10);
+    if (!match) continue;
     cudaEventSynchronize(r.b);
     float e = 0.f;
     cudaEventElapsedTime(&e, r.a, r.b);
