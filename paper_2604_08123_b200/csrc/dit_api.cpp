@@ -380,9 +380,8 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
         P.B = w + off;
         off = align_up(off + (size_t)cfg->max_adapters * out * c->r_alloc * 2, 256);
         // A pool viewed [slots*r_alloc][in]; B pool viewed [slots*out][r_alloc]
-        make_tmap_2d(&P.tmA, P.A, in, (uint64_t)cfg->max_adapters * c->r_alloc, (uint64_t)in * 2, 64, GEMM_BN);
-        make_tmap_2d(&P.tmB, P.B, c->r_alloc, (uint64_t)cfg->max_adapters * out, (uint64_t)c->r_alloc * 2, 64,
-                     GEMM_BN);
+        make_tmap_2d(&P.tmA, P.A, in, (uint64_t)cfg->max_adapters * c->r_alloc, (uint64_t)in * 2, 64, 128);
+        make_tmap_2d(&P.tmB, P.B, c->r_alloc, (uint64_t)cfg->max_adapters * out, (uint64_t)c->r_alloc * 2, 64, 128);
       }
     };
     for (int i = 0; i < c->Ld; ++i)
@@ -479,7 +478,7 @@ bool bind_lin(dit_ctx* c, Lin& L, const std::string& name) {
   L.b = b->second.ptr;
   L.out = (int)w->second.shape[0];
   L.in = (int)w->second.shape[1];
-  return make_tmap_2d(&L.tm, L.w, L.in, L.out, (uint64_t)L.in * 2, 64, GEMM_BN);
+  return make_tmap_2d(&L.tm, L.w, L.in, L.out, (uint64_t)L.in * 2, 64, 128);
 }
 
 int bind_all(dit_ctx* c) {
@@ -732,7 +731,7 @@ int build_rowspace(dit_ctx* c, RowSpace& R, int M, int rows_per_req, const std::
                    std::vector<int>& h_tiles, std::vector<int>& h_cnt, std::vector<int2>& h_shrink) {
   R.M = M;
   R.rows_per_req = rows_per_req;
-  R.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  R.tiles_m = (M + GEMM_TM - 1) / GEMM_TM;
   R.h_row_slot.assign(M, -1);
   for (int r = 0; r < M; ++r) R.h_row_slot[r] = req_slot[r / rows_per_req];
   h_tiles.assign((size_t)R.tiles_m * c->slot_cap, 0);
@@ -740,7 +739,7 @@ int build_rowspace(dit_ctx* c, RowSpace& R, int M, int rows_per_req, const std::
   h_shrink.clear();
   for (int m = 0; m < R.tiles_m; ++m) {
     std::vector<int> sl;
-    for (int r = m * GEMM_BM; r < std::min(M, (m + 1) * GEMM_BM); ++r) {
+    for (int r = m * GEMM_TM; r < std::min(M, (m + 1) * GEMM_TM); ++r) {
       int s = R.h_row_slot[r];
       if (s >= 0 && std::find(sl.begin(), sl.end(), s) == sl.end()) sl.push_back(s);
     }
@@ -802,7 +801,7 @@ GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const
   P.M = M;
   P.N = W.out;
   P.K = K;
-  P.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  P.tiles_m = (M + GEMM_TM - 1) / GEMM_TM;
   P.tiles_n = (P.N + GEMM_BN - 1) / GEMM_BN;
   P.num_tiles = P.tiles_m * P.tiles_n;
   P.epi = epi;
@@ -833,7 +832,7 @@ GemmProblem shrink_problem(dit_ctx* c, const void* A, int M, int K, int lda, con
   P.M = M;
   P.N = c->r_alloc;
   P.K = K;
-  P.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  P.tiles_m = (M + GEMM_TM - 1) / GEMM_TM;
   P.tiles_n = 1;
   P.num_tiles = R.n_shrink;
   P.shrink = 1;

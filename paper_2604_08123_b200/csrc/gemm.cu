@@ -1,19 +1,25 @@
-// gemm.cu -- persistent warp-specialised tcgen05 GEMM with fused epilogues.
+// gemm.cu -- persistent warp-specialised tcgen05 GEMM with fused epilogues,
+// 2-SM (CTA pair) version.
 //
 // C[M][N] = A[M][K] * B[N][K]^T (+ LoRA K-extension), bf16 in, fp32 in TMEM.
-// Roles (192 threads, 1 CTA per SM):
-//   warp 0      TMA producer: 4-stage smem ring of A 128x64 + B 256x64 tiles
-//               (SWIZZLE_128B), mbarrier full/empty handshake.
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1
-//               kind::f16 M=128 N=256 K=16, commits stage release and
-//               accumulator-ready to mbarriers.
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 from a double-buffered TMEM
-//               accumulator (2 x 256 columns) and the fused epilogue of the
-//               step row: bias, QK-RMSNorm + RoPE + head-major
+// A cluster of 2 CTAs (one SM pair) owns a 256 x 256 output tile: CTA r loads
+// A rows [m0 + 128 r, +128) and B rows [n0 + 128 r, +128) (half of N) and
+// keeps accumulator rows [128 r, +128) in its TMEM; the leader issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16), which reads both CTAs'
+// shared memory -- each SM streams half the B operand.
+// Roles (384 threads per CTA, 1 CTA per SM):
+//   warp 0      TMA producer (both CTAs): 6-stage ring of A 128x64 + B 128x64
+//               (SWIZZLE_128B); complete_tx lands on the LEADER's full barrier.
+//   warp 1      MMA issuer (leader only, one thread); tcgen05.commit multicast
+//               releases the stage / publishes the accumulator in both CTAs.
+//   warp 2      TMEM allocator (cta_group::2, 512 columns = 2 accumulators).
+//   warps 4-11  epilogue: warp w reads TMEM lanes 32 (w % 4).. and column half
+//               (w - 4) / 4 of a double-buffered accumulator, then the fused
+//               epilogue of the step row: bias, QK-RMSNorm + RoPE + head-major
 //               scatter, GELU, gated residual (+ControlNet), Euler, LoRA shrink.
-// Tiles are scheduled statically (tile += gridDim.x) over up to two problems
-// (the img and txt streams of a double block share one launch), rasterised
-// in groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
+// Tiles are scheduled statically per cluster over up to two problems (the
+// img and txt streams of a double block share one launch), rasterised in
+// groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
 #include <cstdio>
 
 #include "common.cuh"
@@ -21,13 +27,58 @@
 
 namespace dit {
 
-constexpr int STAGES = 4;
-constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-constexpr int B_BYTES = GEMM_BN * GEMM_BK * 2;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;           // 128 rows x 64 per CTA
+constexpr int B_BYTES = (GEMM_BN / 2) * GEMM_BK * 2;     // 128 rows x 64 per CTA (half of N)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 384;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // shared::cluster address of the leader's copy
+
+DEVI uint32_t cluster_rank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+DEVI void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+DEVI void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+DEVI void tma_load_2d_2sm(const void* desc, uint64_t* bar, void* smem, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1)
+      : "memory");
+}
+DEVI void mma_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+DEVI void commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+DEVI void tmem_alloc_2sm(uint32_t* smem_dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "n"(TMEM_COLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+DEVI void tmem_dealloc_2sm(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(TMEM_COLS) : "memory");
+}
 
 size_t gemm_smem_bytes() { return SMEM_BYTES; }
 
@@ -47,7 +98,7 @@ DEVI TileInfo decode_tile(const GemmArgs& A, int t) {
     ti.slot = e.y;
     ti.n = 0;
   } else {
-    int per_group = GEMM_GROUP_M * P.tiles_n;
+    int per_group = GEMM_GROUP_M * P.tiles_n;   // tiles_m counts 256-row pair tiles
     int g = local / per_group;
     int first_m = g * GEMM_GROUP_M;
     int gm = min(GEMM_GROUP_M, P.tiles_m - first_m);
@@ -104,76 +155,79 @@ DEVI void store_bf16_32(bf16* dst, const float (&x)[32], int valid) {
   }
 }
 
-// Epilogue for one accumulator tile; executed by the 128 epilogue threads.
-DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase, int row_in_tile) {
+// Epilogue for one accumulator tile.  Thread = one accumulator row; this warp
+// covers columns [c_lo, c_lo + 128) of the 256-wide tile.
+DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase, int row_in_tile, int c_lo) {
   const EpiParams& E = P.epi;
-  const int r = ti.m * GEMM_BM + row_in_tile;
+  const int r = ti.m * GEMM_TM + row_in_tile;
   const bool row_ok = r < P.M;
   const int n0 = ti.n * GEMM_BN;
   const int b = row_ok ? r / E.rows_per_req : 0;
   const int nloc = row_ok ? r - b * E.rows_per_req : 0;
   const int jrow = b * E.joint_n + E.joint_off + nloc;
   const bf16* bias = reinterpret_cast<const bf16*>(E.bias);
+  const int c_hi = c_lo + GEMM_BN / 2;
 
   if (E.kind == EPI_QKV) {
     const int d = E.head_dim;
     const int D = E.D;
 #pragma unroll 1
-    for (int c0 = 0; c0 < GEMM_BN; c0 += d) {
+    for (int c0 = c_lo; c0 < c_hi; c0 += d) {
       const int col0 = n0 + c0;
       if (col0 >= P.N) break;
       if (col0 < E.qkv_cols) {
-        float x[128];
-        const int nch = d / 32;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j < nch) {
-            uint32_t rr[32];
-            tmem_ld32(tbase + c0 + 32 * j, rr);
-            tmem_ld_wait();
-            float bv[32];
-            load_bias32(bias, col0 + 32 * j, P.N, bv);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) x[32 * j + e] = __uint_as_float(rr[e]) + bv[e];
-          }
-        }
-        if (!row_ok) continue;
         const int sec = col0 / D;
         const int head = (col0 - sec * D) / d;
+        // pass 1: sum of squares over the head (q, k only)
+        float rs = 1.f;
         if (sec < 2) {
-          const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
           float ss = 0.f;
+#pragma unroll 1
+          for (int j = 0; j < d; j += 32) {
+            uint32_t rr[32];
+            tmem_ld32(tbase + c0 + j, rr);
+            tmem_ld_wait();
+            float bv[32];
+            load_bias32(bias, col0 + j, P.N, bv);
 #pragma unroll
-          for (int j = 0; j < 128; ++j)
-            if (j < d) ss += x[j] * x[j];
-          const float rs = rsqrtf(ss / (float)d + 1e-6f);
-          const float2* cs = E.rope + (size_t)(E.joint_off + nloc) * (d / 2);
-#pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            if (2 * j < d) {
-              float x0 = x[2 * j] * rs * __bfloat162float(g[2 * j]);
-              float x1 = x[2 * j + 1] * rs * __bfloat162float(g[2 * j + 1]);
-              float2 c = __ldg(cs + j);
-              x[2 * j] = c.x * x0 - c.y * x1;
-              x[2 * j + 1] = c.y * x0 + c.x * x1;
+            for (int e = 0; e < 32; ++e) {
+              const float x = __uint_as_float(rr[e]) + bv[e];
+              ss += x * x;
             }
           }
+          rs = rsqrtf(ss / (float)d + 1e-6f);
         }
         const int hl_n = E.heads / E.sp_world;
         const int dest = head / hl_n, hl = head - dest * hl_n;
         bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
                     (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
+        const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
+        const float2* cs = E.rope + (size_t)(E.joint_off + nloc) * (d / 2);
+        // pass 2: normalise, rotate interleaved pairs, store
+#pragma unroll 1
+        for (int j = 0; j < d; j += 32) {
+          uint32_t rr[32];
+          tmem_ld32(tbase + c0 + j, rr);
+          tmem_ld_wait();
+          float bv[32], y[32];
+          load_bias32(bias, col0 + j, P.N, bv);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j < nch) {
-            float y[32];
+          for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr[e]) + bv[e];
+          if (sec < 2 && row_ok) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) y[e] = x[32 * j + e];
-            store_bf16_32(dst + 32 * j, y, 32);
+            for (int e = 0; e < 16; ++e) {
+              const float x0 = y[2 * e] * rs * __bfloat162float(g[j + 2 * e]);
+              const float x1 = y[2 * e + 1] * rs * __bfloat162float(g[j + 2 * e + 1]);
+              const float2 c = __ldg(cs + j / 2 + e);
+              y[2 * e] = c.x * x0 - c.y * x1;
+              y[2 * e + 1] = c.y * x0 + c.x * x1;
+            }
           }
+          if (row_ok) store_bf16_32(dst + j, y, 32);
         }
       } else {
         // GELU branch of the single-block linear1 (cols >= 3D)
+#pragma unroll 1
         for (int j = 0; j < d; j += 32) {
           const int col = col0 + j;
           uint32_t rr[32];
@@ -195,7 +249,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
   if (E.kind == EPI_SHRINK) {
     const int rs = row_ok ? E.row_slot[r] : -2;
     const float sc = E.slot_scale[ti.slot];
-    for (int c0 = 0; c0 < E.r_alloc; c0 += 32) {
+#pragma unroll 1
+    for (int c0 = c_lo; c0 < min(c_hi, E.r_alloc); c0 += 32) {
       uint32_t rr[32];
       tmem_ld32(tbase + c0, rr);
       tmem_ld_wait();
@@ -210,7 +265,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
   }
 
 #pragma unroll 1
-  for (int c0 = 0; c0 < GEMM_BN; c0 += 32) {
+  for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
     const int col = n0 + c0;
     if (col >= P.N) break;
     uint32_t rr[32];
@@ -248,22 +303,24 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         }
       }
       if (valid == 32) {
+        float4 h4[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) h4[q] = reinterpret_cast<float4*>(hp)[q];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          float4 h4 = reinterpret_cast<float4*>(hp)[q];
-          float4 g4 = __ldg(reinterpret_cast<const float4*>(gp) + q);
-          h4.x += g4.x * y[4 * q];
-          h4.y += g4.y * y[4 * q + 1];
-          h4.z += g4.z * y[4 * q + 2];
-          h4.w += g4.w * y[4 * q + 3];
+          const float4 g4 = __ldg(reinterpret_cast<const float4*>(gp) + q);
+          h4[q].x += g4.x * y[4 * q];
+          h4[q].y += g4.y * y[4 * q + 1];
+          h4[q].z += g4.z * y[4 * q + 2];
+          h4[q].w += g4.w * y[4 * q + 3];
           if (cn != nullptr) {
-            uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
-            h4.x += kap * bf16_lo(c2.x);
-            h4.y += kap * bf16_hi(c2.x);
-            h4.z += kap * bf16_lo(c2.y);
-            h4.w += kap * bf16_hi(c2.y);
+            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
+            h4[q].x += kap * bf16_lo(c2.x);
+            h4[q].y += kap * bf16_hi(c2.x);
+            h4[q].z += kap * bf16_lo(c2.y);
+            h4[q].w += kap * bf16_hi(c2.y);
           }
-          reinterpret_cast<float4*>(hp)[q] = h4;
+          reinterpret_cast<float4*>(hp)[q] = h4[q];
         }
       } else {
         for (int e = 0; e < valid; ++e) {
@@ -283,7 +340,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
   }
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmArgs args) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -297,6 +355,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t cta = cluster_rank();
+  const bool leader = cta == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     for (int p = 0; p < args.num_problems; ++p) {
@@ -310,18 +371,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 2);      // leader: own expect_tx arrival + the peer producer's remote arrival
+      mbar_init(&empty[i], 1);     // one multicast commit per phase
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 16);   // 8 epilogue warps x 2 CTAs (leader's copy)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) tmem_alloc_2sm(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -329,27 +390,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+      for (int t = cid; t < args.total_tiles; t += ncl) {
         const TileInfo ti = decode_tile(args, t);
         const GemmProblem& P = args.p[ti.p];
+        const int a_row = ti.m * GEMM_TM + (int)cta * GEMM_BM;
         for (int kb = 0; kb < ti.nk_total; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          if (leader)
+            mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          else
+            mbar_arrive_cta(&full[stage], 0);
           uint8_t* a_dst = sA + stage * A_BYTES;
           uint8_t* b_dst = sB + stage * B_BYTES;
           if (kb < ti.nk_base) {
-            tma_load_2d(&P.tmA, &full[stage], a_dst, kb * GEMM_BK, ti.m * GEMM_BM);
+            tma_load_2d_2sm(&P.tmA, &full[stage], a_dst, kb * GEMM_BK, a_row);
             if (P.shrink)
-              tma_load_2d(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.slot * P.epi.r_alloc);
+              tma_load_2d_2sm(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.slot * P.epi.r_alloc + (int)cta * 128);
             else
-              tma_load_2d(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.n * GEMM_BN);
+              tma_load_2d_2sm(&P.tmB, &full[stage], b_dst, kb * GEMM_BK, ti.n * GEMM_BN + (int)cta * 128);
           } else {
             const int e = kb - ti.nk_base;
             const int si = e / P.ext_kblocks;
             const int ek = e - si * P.ext_kblocks;
             const int slot = P.tile_slots[ti.m * P.slot_cap + si];
-            tma_load_2d(&P.tmAx, &full[stage], a_dst, slot * P.epi.r_alloc + ek * GEMM_BK, ti.m * GEMM_BM);
-            tma_load_2d(&P.tmBx, &full[stage], b_dst, ek * GEMM_BK, slot * P.N + ti.n * GEMM_BN);
+            tma_load_2d_2sm(&P.tmAx, &full[stage], a_dst, slot * P.epi.r_alloc + ek * GEMM_BK, a_row);
+            tma_load_2d_2sm(&P.tmBx, &full[stage], b_dst, ek * GEMM_BK, slot * P.N + ti.n * GEMM_BN + (int)cta * 128);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -359,12 +424,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN);
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * GEMM_BM, GEMM_BN);
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++iter) {
+      for (int t = cid; t < args.total_tiles; t += ncl, ++iter) {
         const TileInfo ti = decode_tile(args, t);
         const int acc = iter & 1;
         const uint32_t acc_phase = (iter >> 1) & 1;
@@ -377,40 +442,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            tc_mma_f16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32), idesc,
-                       (kb | k) != 0);
-          }
-          tc_commit(&empty[stage]);
+          for (int k = 0; k < GEMM_BK / 16; ++k)
+            mma_2sm(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32), idesc,
+                    (kb | k) != 0);
+          commit_2sm_mc(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        commit_2sm_mc(&tfull[acc]);
       }
     }
-  } else {
+  } else if (warp >= 4) {
     const int wq = warp & 3;              // TMEM lane quarter this warp may access
-    const int row_in_tile = wq * 32 + lane;
+    const int half = (warp - 4) >> 2;     // column half of the tile
+    const int row_in_tile = (int)cta * GEMM_BM + wq * 32 + lane;
     int iter = 0;
-    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++iter) {
+    for (int t = cid; t < args.total_tiles; t += ncl, ++iter) {
       const TileInfo ti = decode_tile(args, t);
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * GEMM_BN;
-      epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile);
+      epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile, half * (GEMM_BN / 2));
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[acc]);
+        else
+          mbar_arrive_cta(&tempty[acc], 0);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    tmem_dealloc_2sm(tmem_base);
   }
 }
 
@@ -472,8 +543,9 @@ cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s) {
     attr = true;
   }
   if (args.total_tiles <= 0) return cudaSuccess;
-  int grid = args.total_tiles < num_sms ? args.total_tiles : num_sms;
-  gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(args);
+  const int pairs = num_sms / 2;
+  const int clusters = args.total_tiles < pairs ? args.total_tiles : pairs;
+  gemm_kernel<<<2 * clusters, NUM_THREADS, SMEM_BYTES, s>>>(args);
   return cudaGetLastError();
 }
 

@@ -8,7 +8,8 @@ namespace dit {
 
 // ------------------------------------------------------------------ GEMM (tcgen05)
 // Tile 128 x 256 x 64, bf16 in, fp32 accumulate in TMEM, fused epilogues.
-constexpr int GEMM_BM = 128;
+constexpr int GEMM_BM = 128;      // accumulator rows per CTA (= TMEM lanes)
+constexpr int GEMM_TM = 256;      // rows per 2-SM (CTA pair) tile
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_MAX_PROBLEMS = 2;
@@ -67,11 +68,11 @@ struct EpiParams {
 
 struct GemmProblem {
   CUtensorMap tmA;       // A [M][K] bf16, box {64, 128}
-  CUtensorMap tmB;       // B [N][K] bf16, box {64, 256}; or 3D [slot][N][K] for shrink
+  CUtensorMap tmB;       // B [N][K] bf16, box {64, 128} (each CTA of the pair loads half of N)
   CUtensorMap tmAx;      // LoRA K-extension A: S [M][slots*r_alloc], box {64, 128}
-  CUtensorMap tmBx;      // LoRA K-extension B: pool [slot][N][r_alloc] 3D, box {64, 256, 1}
+  CUtensorMap tmBx;      // LoRA K-extension B: pool viewed [slot*N][r_alloc], box {64, 128}
   int M, N, K;
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n;  // tiles_m: 256-row pair tiles
   int tile_begin;        // first global tile index of this problem
   int num_tiles;
   // LoRA: per m-tile list of pool slots (device [tiles_m][slot_cap]) + counts
