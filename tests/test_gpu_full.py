@@ -1,0 +1,194 @@
+"""GPU parity at real sizes + ABI error paths.
+
+* Flux width (D=3072, 24x128 heads) at 1024^2 tokens (Ni=4096, Nt=512), shallow
+  depth (1 double + 1 single block), B=2 with two rank-64 adapters and a
+  ControlNet residual -- element-wise vs the fp64 oracle.
+* Full depth (19 + 38 blocks) at reduced width, ControlNet on every double
+  block for one request and a LoRA for the other -- error accumulation.
+* The bench configuration itself (Flux-Dev 19+38, B=8, 4 rank-64 LoRAs,
+  N=4608) where the oracle cannot follow: properties that hold at any size
+  (bitwise determinism, batch invariance, adapter -1 == base model, adapters
+  and ControlNet actually change the output).
+* Ulysses SP at P=8 (in-process group) at Flux width: bitwise == P=1.
+* Every documented error code of the C ABI, before any device work.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import flux_step as O
+from tests.helpers import cosine, max_rel, oracle_adapter, residuals
+from tests.test_gpu_parity import _model, _shard_step, check
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+def test_flux_width_1024sq_lora_controlnet(torch_cuda):
+    cfg = synth.flux_reduced(1, 1)
+    B, hh, ww, nt = 2, 64, 64, 512
+    m = _model(cfg, B, hh * ww, nt, rank=64, adapters=2)
+    m.register_synthetic_lora(0, rank=64, index=0)
+    m.register_synthetic_lora(1, rank=64, index=1)
+    batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=2)
+    batch.adapter_id = np.array([1, 0], dtype=np.int32)
+    res_bits = {0: {0: synth.controlnet_residual_bf16(0, 0, hh * ww, cfg.hidden)}}
+    lat, v = m.step(batch, controlnet=res_bits)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    ads = {a: oracle_adapter(cfg, 64, a)[0] for a in range(2)}
+    res = {0: {0: O.bf16_to_f64(res_bits[0][0])}}
+    x_o, v_o = O.dit_step(cfg, W, batch, ads, res, n_res=1)
+    check(v, v_o, "v")
+    check(lat, x_o, "latents")
+
+
+def test_full_depth_reduced_width(torch_cuda):
+    cfg = dataclasses.replace(synth.FLUX, hidden=512, heads=4, txt_dim=256, pooled_dim=128)
+    B, hh, ww, nt = 2, 32, 32, 128
+    m = _model(cfg, B, hh * ww, nt, rank=16, adapters=1)
+    m.register_synthetic_lora(7, rank=16, index=0, scale=0.75)
+    batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([-1, 7], dtype=np.int32)
+    batch.cn_scale = np.array([0.8, 1.0], dtype=np.float32)
+    res_bits = {0: {i: synth.controlnet_residual_bf16(0, i, hh * ww, cfg.hidden) for i in range(cfg.depth_double)}}
+    lat, v = m.step(batch, controlnet=res_bits)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    res = {0: {i: O.bf16_to_f64(r) for i, r in res_bits[0].items()}}
+    x_o, v_o = O.dit_step(cfg, W, batch, {7: oracle_adapter(cfg, 16, 0, scale=0.75)[0]}, res,
+                          n_res=cfg.depth_double)
+    check(v, v_o, "v")
+    check(lat, x_o, "latents")
+
+
+def test_bench_config_properties_full_size(torch_cuda):
+    """cfg3 at full size (the launch configuration bench.py times)."""
+    torch = torch_cuda
+    cfg = synth.FLUX
+    m = _model(cfg, 8, 4096, 512, rank=64, adapters=4)
+    for a in range(4):
+        m.register_synthetic_lora(a, rank=64, index=a)
+    batch = synth.make_batch(cfg, 8, 64, 64, 512, n_adapters=4)
+    _, v1 = m.step(batch)
+    _, v2 = m.step(batch)
+    np.testing.assert_array_equal(v1, v2)                              # run-to-run bitwise determinism
+    assert np.isfinite(v1).all()
+    one = dataclasses.replace(batch, latents=batch.latents[3:4], txt=batch.txt[3:4], pooled=batch.pooled[3:4],
+                              sigma=batch.sigma[3:4], sigma_next=batch.sigma_next[3:4],
+                              guidance=batch.guidance[3:4], adapter_id=batch.adapter_id[3:4],
+                              cn_scale=batch.cn_scale[3:4])
+    _, v_one = m.step(one)
+    np.testing.assert_array_equal(v_one[0], v1[3])                     # batch invariance (P9 on GPU)
+    base = dataclasses.replace(one, adapter_id=np.array([-1], dtype=np.int32))
+    _, v_base = m.step(base)
+    assert max_rel(v_base[0], v1[3]) > 0.05                            # the adapter matters ...
+    swapped = dataclasses.replace(one, adapter_id=np.array([(int(one.adapter_id[0]) + 1) % 4], dtype=np.int32))
+    _, v_sw = m.step(swapped)
+    assert max_rel(v_sw[0], v1[3]) > 0.05                              # ... and which one (P12)
+    mixed = dataclasses.replace(batch, adapter_id=np.array([-1] + list(batch.adapter_id[1:]), dtype=np.int32))
+    _, v_mixed = m.step(mixed)
+    base0 = dataclasses.replace(base, latents=batch.latents[0:1], txt=batch.txt[0:1], pooled=batch.pooled[0:1],
+                                sigma=batch.sigma[0:1], sigma_next=batch.sigma_next[0:1])
+    _, v_b0 = m.step(base0)
+    np.testing.assert_array_equal(v_mixed[0], v_b0[0])                 # adapter -1 inside a LoRA batch == base (P3)
+    res = {2: {i: synth.controlnet_residual_bf16(2, i, 4096, cfg.hidden) for i in range(cfg.depth_double)}}
+    _, v_cn = m.step(batch, controlnet=res)
+    assert max_rel(v_cn[2], v1[2]) > 0.02                              # ControlNet consumed ...
+    np.testing.assert_array_equal(v_cn[5], v1[5])                      # ... only by its own request
+
+
+def test_sequence_parallel_p8_flux_width(torch_cuda):
+    from paper_2604_08123_b200 import dit as D
+    cfg = synth.flux_reduced(1, 1)
+    B, hh, ww, nt = 2, 32, 32, 64
+    P = 8
+    ref = _model(cfg, B, hh * ww, nt, rank=64, adapters=1)
+    ref.register_synthetic_lora(0, rank=64, index=0)
+    batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([0, -1], dtype=np.int32)
+    lat1, v1 = ref.step(batch)
+    ref.close()
+    group = D.load_library().dit_local_group_create(P)
+    models = []
+    for r in range(P):
+        mm = _model(cfg, B, hh * ww, nt, rank=64, adapters=1)
+        mm.register_synthetic_lora(0, rank=64, index=0)
+        mm.sp_init_local(group, r)
+        models.append(mm)
+    latP, vP = _shard_step(models, batch, P)
+    np.testing.assert_array_equal(vP, v1)
+    np.testing.assert_array_equal(latP, lat1)
+    for mm in models:
+        mm.close()
+    D.load_library().dit_local_group_destroy(group)
+
+
+def test_abi_error_paths(torch_cuda):
+    torch = torch_cuda
+    import ctypes as C
+    from paper_2604_08123_b200 import DiT, dit as D
+    cfg = synth.TINY
+    E = D.CODES
+    m = DiT(cfg, 2, 16, 8, max_rank=4, max_adapters=1)
+    lib, ctx = m.lib, m.ctx
+    lat = torch.zeros(2, 16, 16, device="cuda")
+    out = torch.zeros_like(lat)
+    txt = torch.zeros(2, 8, 32, dtype=torch.bfloat16, device="cuda")
+    pooled = torch.zeros(2, 16, dtype=torch.bfloat16, device="cuda")
+    mk = lambda B=2, ids=(-1, -1), o=out, h=4, w=4, nt=8: m.make_batch(
+        B, h, w, nt, list(ids)[:B], [1.0] * B, [0.5] * B, [3.5] * B, lat, o, txt, pooled)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.dit_step(ctx, C.byref(mk()), s) == E["DIT_ENOWEIGHTS"]
+    # load the real weights, then every argument error
+    ws = {}
+    for spec in synth.weight_manifest(cfg):
+        t = torch.empty(spec.shape, dtype=torch.bfloat16, device="cuda")
+        D.fill_synthetic(t, 0, spec.tensor_id, spec.scale, spec.offset)
+        ws[spec.name] = t
+    bad = dict(ws)
+    bad["img_in.w"] = torch.empty(3, 3, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(D.DitError) as e:
+        m.dit_load_weights(bad)
+    assert e.value.code == E["DIT_EINVAL"]
+    with pytest.raises(D.DitError):
+        m.dit_load_weights({"not.a.tensor": ws["img_in.w"]})
+    m.dit_load_weights(ws)
+    torch.cuda.synchronize()
+    assert lib.dit_step(ctx, C.byref(mk()), s) == 0
+    assert lib.dit_step(ctx, C.byref(mk(B=3, ids=(-1, -1, -1))), s) == E["DIT_EBATCH"]
+    assert lib.dit_step(ctx, C.byref(mk(o=lat)), s) == E["DIT_EALIAS"]
+    assert lib.dit_step(ctx, C.byref(mk(h=8, w=8)), s) == E["DIT_ESHAPE"]
+    assert lib.dit_step(ctx, C.byref(mk(ids=(3, -1))), s) == E["DIT_EADAPTER"]
+    assert lib.lora_unregister(ctx, 3) == E["DIT_ENOENT"]
+    A = torch.zeros(4, 64, dtype=torch.bfloat16, device="cuda")
+    lt = {"double.0.img.qkv.lora_A": A}
+    m.lora_register(3, 4, 1.0, lt)
+    with pytest.raises(D.DitError) as e:
+        m.lora_register(3, 4, 1.0, lt)
+    assert e.value.code == E["DIT_EEXIST"]
+    with pytest.raises(D.DitError) as e:
+        m.lora_register(4, 4, 1.0, lt)
+    assert e.value.code == E["DIT_ENOSPC"]
+    with pytest.raises(D.DitError) as e:
+        m.lora_register(5, 8, 1.0, lt)
+    assert e.value.code == E["DIT_ERANK"]
+    with pytest.raises(D.DitError) as e:
+        m.lora_register(6, 4, 1.0, {"double.0.img.qkv.lora_A": torch.zeros(4, 65, dtype=torch.bfloat16, device="cuda")})
+    assert e.value.code in (E["DIT_EINVAL"], E["DIT_ENOSPC"])
+    assert lib.dit_step(ctx, C.byref(mk(ids=(3, -1))), s) == 0
+    m.lora_unregister(3)
+    assert lib.controlnet_inject(ctx, 5, 0, txt.data_ptr(), 1.0, None) == E["DIT_EINVAL"]
+    assert lib.controlnet_inject(ctx, 0, 7, txt.data_ptr(), 1.0, None) == E["DIT_EINVAL"]
+    assert lib.controlnet_inject(ctx, 0, 0, None, 1.0, None) == E["DIT_EINVAL"]
+    assert lib.sp_init(ctx, 3, 0, None) == E["DIT_EPARALLEL"]      # 3 does not divide 2 heads
+    assert lib.sp_init(ctx, 2, 2, None) == E["DIT_EINVAL"]
+    torch.cuda.synchronize()
+    m.close()
