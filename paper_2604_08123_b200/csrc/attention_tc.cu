@@ -1,19 +1,29 @@
 // attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (d = 128).
 //
-// One CTA = one 128-row query tile of one (request, head); KV tiles of 128 keys.
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512).
-//   warp 0      TMA producer: Q once, K ring (2 stages) and V ring (2 stages), 3D
-//               tensor maps [B*H][N][128] so rows past N are zero-filled.
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T (SS, both K-major), then
-//               O += P_j V_j with P_j read from TMEM (TS form) and V_j MN-major
-//               in smem.  QK_{j+2} is issued right after PV_j so the tensor
-//               pipe works on the next scores while softmax runs.
-//   warps 4-7   softmax (thread = query row = TMEM lane): tcgen05.ld of S_j,
-//               online softmax in fp32 with exp2, lazy O rescale (only when the
-//               running max grows by > 8 in log2 units, warp-uniform), P_j
-//               packed to bf16 and written with tcgen05.st; final O / l epilogue.
-// Synchronisation is all mbarriers (TMA complete_tx, tcgen05.commit, thread
-// arrivals); see DESIGN.md §5.3 for the phase argument.
+// One CTA = TWO 128-row query tiles (256 queries) of one (request, head); KV
+// tiles of 128 keys shared by both query tiles.  TMEM (512 columns):
+//   S0 [0,128)  S1 [128,256)  O0 [256,384)  O1 [384,512);  P_t (bf16) is written
+//   over the first 64 columns of S_t once the scores have been read.
+// Roles (576 threads = 18 warps):
+//   warp 0      TMA producer: Q0/Q1 once, K ring (2 stages), V ring (2 stages);
+//               3D tensor maps [B*H][N][128] so rows past N are zero-filled.
+//   warp 1      TMEM allocator + MMA issuer (one thread).  Ping-pong schedule:
+//                 QK(0,0) QK(1,0) | PV(0,j) QK(0,j+1) PV(1,j) QK(1,j+1) | ...
+//               so the tensor pipe computes one query tile's PV + next scores
+//               while the other tile's softmax runs.  QK is SS (both K-major),
+//               PV is TS (P from TMEM, V MN-major in smem).
+//   warps 2-9   softmax of query tile 0, warps 10-17 of tile 1.  Two warps per
+//               TMEM lane quarter: each thread owns one query row and 64 of the
+//               128 score columns; the row max is combined through shared
+//               memory (64-thread named barrier per lane quarter), the row sum
+//               stays per half until the epilogue.  Lazy O rescale (only when
+//               the running max grows by > 8 in log2 units), packed f32x2
+//               FFMA/FADD, exp2 with 1/4 of the elements on a degree-3
+//               polynomial (FMA pipe) and 3/4 on MUFU, P packed to bf16 and
+//               stored with tcgen05.st; final O / l epilogue (each half writes
+//               64 output columns).
+// Synchronisation: mbarriers only (TMA complete_tx, tcgen05.commit, thread
+// arrivals); every waiter can be at most one phase behind.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -21,15 +31,24 @@ namespace dit {
 
 namespace attn_tc {
 
-constexpr int BQ = 128, BKV = 128, HD = 128;
+constexpr int BQ = 128, NQ = 2, BKV = 128, HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;         // 32 KB: 128 rows x 128 bf16 (two 64-col swizzle panels)
 constexpr int PANEL = 128 * 64 * 2;              // 16 KB
 constexpr int KST = 2, VST = 2;
-constexpr int SMEM = TILE_BYTES * (1 + KST + VST) + 1024 + 256;
-constexpr int THREADS = 256;
-constexpr uint32_t COL_S0 = 0, COL_O = 256, COL_P0 = 384;
+constexpr int SMEM = TILE_BYTES * (NQ + KST + VST) + 1024 + 128 + 8192;   // + barriers + row max/sum exchange (6 KB)
+constexpr int THREADS = 576;
+constexpr int SM_WARPS_PER_TILE = 8;
+constexpr uint32_t COL_S = 0, COL_O = 256;
 constexpr float RESCALE_THRESH = 8.0f;
 
+DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 DEVI void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -65,11 +84,40 @@ DEVI uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes) {
   return d;
 }
 
-DEVI float fast_exp2(float x) {
+DEVI float mufu_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes: x = n + f, n = rint(x), f in [-0.5, 0.5];
+// 2^f by a degree-3 minimax polynomial (max rel. error 2.1e-4 < bf16 half-ulp),
+// 2^n by adding n to the exponent field.  x is clamped at -125 so the exponent
+// of 2^f (126 or 127) minus n never underflows into the sign bit (2^-125 ~ 0).
+DEVI float poly_exp2(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;             // 1.5 * 2^23: low mantissa bits = rint(x)
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(0.05485438f, f, 0.24182249f);
+  p = fmaf(p, f, 0.69324851f);
+  p = fmaf(p, f, 0.99998755f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Packed version for two arguments (f32x2 FADD/FFMA).
+DEVI float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
+  float2 p = __ffma2_rn(make_float2(0.05485438f, 0.05485438f), f, make_float2(0.24182249f, 0.24182249f));
+  p = __ffma2_rn(p, f, make_float2(0.69324851f, 0.69324851f));
+  p = __ffma2_rn(p, f, make_float2(0.99998755f, 0.99998755f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+DEVI void named_bar_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 struct Maps {
   CUtensorMap q, k, v;   // 3D {128 (d), N, B*H}, box {64, 128, 1}
@@ -78,8 +126,8 @@ struct Maps {
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + TILE_BYTES;
+  uint8_t* sQ = smem;                              // [NQ] tiles
+  uint8_t* sK = smem + NQ * TILE_BYTES;
   uint8_t* sV = sK + KST * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
   uint64_t* q_full = bars;
@@ -87,24 +135,23 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   uint64_t* k_empty = bars + 3;       // [KST]
   uint64_t* v_full = bars + 5;        // [VST]
   uint64_t* v_empty = bars + 7;       // [VST]
-  uint64_t* s_full = bars + 9;        // [2]
-  uint64_t* p_full = bars + 11;       // [2]
-  uint64_t* o_done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_full = bars + 9;        // [NQ]
+  uint64_t* p_full = bars + 11;       // [NQ]
+  uint64_t* o_done = bars + 13;       // [NQ]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  float* xmax = reinterpret_cast<float*>(bars + 16);   // [2 parity][2 tiles][4 quarters][2 halves][32]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int h = blockIdx.y, b = blockIdx.z;
   const int N = p.N;
   const int bh = b * p.H + h;
-  const int q0 = qt * BQ;
+  const int q0 = blockIdx.x * (NQ * BQ);
   const int nkv = (N + BKV - 1) / BKV;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
     tma_prefetch_desc(&maps.v);
-  }
-  if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
@@ -112,12 +159,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], SM_WARPS_PER_TILE);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(o_done, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -125,9 +172,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, TILE_BYTES);
-      tma_load_3d(&maps.q, q_full, sQ, 0, q0, bh);
-      tma_load_3d(&maps.q, q_full, sQ + PANEL, 64, q0, bh);
+      mbar_expect_tx(q_full, NQ * TILE_BYTES);
+      for (int t = 0; t < NQ; ++t) {
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
+      }
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
@@ -145,118 +194,157 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_qk = [&](int j) {
+      auto issue_qk = [&](int t, int j) {
         const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        if (t == 0) mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + t * TILE_BYTES);
         const uint32_t k_addr = smem_u32(sK + st * TILE_BYTES);
-        const uint32_t d = tmem + COL_S0 + st * 128;
+        const uint32_t d = tmem + COL_S + t * 128;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
           tc_mma_f16(d, smem_desc_k_sw128(q_addr + off), smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
         }
-        tc_commit(&k_empty[st]);
-        tc_commit(&s_full[st]);
+        tc_commit(&s_full[t]);
+        if (t == NQ - 1) tc_commit(&k_empty[st]);
       };
-      mbar_wait(q_full, 0);
-      issue_qk(0);
-      if (nkv > 1) issue_qk(1);
-      for (int j = 0; j < nkv; ++j) {
+      auto issue_pv = [&](int t, int j) {
         const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&p_full[st], ph);
-        mbar_wait(&v_full[st], ph);
+        mbar_wait(&p_full[t], j & 1);
+        if (t == 0) mbar_wait(&v_full[st], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + st * TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          mma_ts(tmem + COL_O, tmem + COL_P0 + st * 64 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL), idesc_pv,
-                 (j | kk) != 0);
-        }
-        tc_commit(&v_empty[st]);
-        tc_commit(o_done);
-        if (j + 2 < nkv) issue_qk(j + 2);
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tmem + COL_O + t * 128, tmem + COL_S + t * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
+                 idesc_pv, (j | kk) != 0);
+        tc_commit(&o_done[t]);
+        if (t == NQ - 1) tc_commit(&v_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        issue_pv(0, j);
+        if (j + 1 < nkv) issue_qk(0, j + 1);
+        issue_pv(1, j);
+        if (j + 1 < nkv) issue_qk(1, j + 1);
       }
     }
-  } else if (warp >= 4) {
-    const int wq = warp & 3;
+  } else {
+    const int sw = warp - 2;
+    const int t = sw / SM_WARPS_PER_TILE;          // query tile of this softmax warp
+    const int hh = (sw % SM_WARPS_PER_TILE) / 4;   // column half (64 score columns)
+    const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t colS = tmem + lane_base + COL_S + t * 128 + hh * 64;
+    const uint32_t colP = tmem + lane_base + COL_S + t * 128 + hh * 32;
+    const uint32_t colO = tmem + lane_base + COL_O + t * 128 + hh * 64;
+    const int bar_id = 1 + t * 4 + wq;
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + COL_S0 + st * 128 + c * 32, r);
+      // pass 1: row max over my 64 columns (scores stay in TMEM)
+      const int kv_valid = N - j * BKV - hh * 64;
+      float mx;
+      {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(colS, r0);
+        tmem_ld32(colS + 32, r1);
         tmem_ld_wait();
+        mx = -INFINITY;
+        if (kv_valid >= 64) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]) * sl2;
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[e]), __uint_as_float(r1[e])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (e < kv_valid) mx = fmaxf(mx, __uint_as_float(r0[e]));
+            if (32 + e < kv_valid) mx = fmaxf(mx, __uint_as_float(r1[e]));
+          }
+        }
       }
-      const int kv_valid = N - j * BKV;
-      if (kv_valid < BKV) {
-#pragma unroll
-        for (int e = 0; e < 128; ++e)
-          if (e >= kv_valid) s[e] = -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int e = 1; e < 128; ++e) mx = fmaxf(mx, s[e]);
+      float* xb = xmax + ((((j & 1) * NQ + t) * 4 + wq) * 2) * 32;
+      xb[hh * 32 + lane] = mx;
+      named_bar_sync(bar_id, 64);
+      mx = fmaxf(mx, xb[(hh ^ 1) * 32 + lane]) * sl2;
       const bool need = mx > m_used + RESCALE_THRESH;
       const float m_new = need ? mx : m_used;
       if (j > 0 && __any_sync(0xffffffff, need)) {
-        const float alpha = need ? fast_exp2(m_used - m_new) : 1.0f;
-        mbar_wait(o_done, (j - 1) & 1);
+        const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
+        mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
-          tmem_ld32(tmem + lane_base + COL_O + c * 32, r);
+          tmem_ld32(colO + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(tmem + lane_base + COL_O + c * 32, r);
+          tmem_st32(colO + c * 32, r);
         }
         tmem_st_wait();
         l *= alpha;
       }
       m_used = m_new;
-      float sum = 0.f;
+      const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
+      float2 acc = make_float2(0.f, 0.f);
+      // pass 2: exponentials, P (bf16) over the first half of this tile's S columns
+      uint32_t pr[2][16];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t r[32];
+        uint32_t sr[32];
+        tmem_ld32(colS + c * 32, sr);
+        tmem_ld_wait();
+        if (kv_valid < 64) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p0 = fast_exp2(s[c * 64 + 2 * e] - m_used);
-          const float p1 = fast_exp2(s[c * 64 + 2 * e + 1] - m_used);
-          sum += p0 + p1;
-          r[e] = pack_bf16(p0, p1);
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
         }
-        tmem_st32(tmem + lane_base + COL_P0 + st * 64 + c * 32, r);
+        uint32_t (&r)[16] = pr[c];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2v, nm);
+          float2 pp;
+          if ((e & 1) == 1) {
+            pp = poly_exp2x2(x);                   // 1/4 of the elements on the FMA pipe
+          } else {
+            pp.x = mufu_exp2(x.x);
+            pp.y = mufu_exp2(x.y);
+          }
+          acc = __fadd2_rn(acc, pp);
+          r[e] = pack_bf16(pp.x, pp.y);
+        }
       }
-      l += sum;
+      named_bar_sync(bar_id, 64);   // both halves finished reading S before P overwrites it
+      tmem_st16(colP, pr[0]);
+      tmem_st16(colP + 16, pr[1]);
+      l += acc.x + acc.y;
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[st]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    // epilogue: O / l -> bf16 rows
-    mbar_wait(o_done, (nkv - 1) & 1);
+    // epilogue: combine the two halves' row sums, O / l -> bf16 (64 columns per half)
+    float* lb = xmax + 2 * NQ * 4 * 2 * 32 + ((t * 4 + wq) * 2) * 32;   // after the max buffers
+    lb[hh * 32 + lane] = l;
+    named_bar_sync(bar_id, 64);
+    l += lb[(hh ^ 1) * 32 + lane];
+    mbar_wait(&o_done[t], (nkv - 1) & 1);
     tc_fence_after();
-    const int n = q0 + row;
+    const int n = q0 + t * BQ + row;
     const float inv = 1.0f / l;
     bf16* out = reinterpret_cast<bf16*>(p.out);
     const size_t orow = n < N ? (size_t)attn_out_row(p, b, n) : 0;
-    uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD + hh * 64);
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
-      tmem_ld32(tmem + lane_base + COL_O + c * 32, r);
+      tmem_ld32(colO + c * 32, r);
       tmem_ld_wait();
       if (n < N) {
 #pragma unroll
@@ -273,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -296,7 +384,7 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
       !make_tmap_3d(&m.k, p.k, HD, rows, heads, s1, s2, 64, 128) ||
       !make_tmap_3d(&m.v, p.v, HD, rows, heads, s1, s2, 64, 128))
     return cudaErrorInvalidValue;
-  dim3 grid((p.N + BQ - 1) / BQ, p.H, p.B);
+  dim3 grid((p.N + NQ * BQ - 1) / (NQ * BQ), p.H, p.B);
   attn_tc_kernel<<<grid, THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
