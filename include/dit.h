@@ -210,6 +210,16 @@ void* dit_local_group_create(int32_t world);
 void dit_local_group_destroy(void* group);
 int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 
+/* Bench/test-only: one attention launch, q/k/v device bf16 [B][H][N][d]
+ * head-major, O bf16 [B*N][H*d] (joint rows).  Asynchronous on stream. */
+int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N, int32_t d,
+                        void* out, void* stream);
+
+/* Debug-only: record a clock64 timeline of CTA (0,0,0) of the tcgen05
+ * attention kernel into buf (device int64 [10 events][64 iterations]);
+ * NULL disables (the default). */
+int dit_debug_attention_trace(void* buf);
+
 /* ncclGetUniqueId for sp_init (rank 0 calls it, the caller broadcasts the 128 bytes). */
 int dit_nccl_unique_id(void* out128);
 

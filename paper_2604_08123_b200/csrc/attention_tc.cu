@@ -119,6 +119,13 @@ DEVI float2 poly_exp2x2(float2 x) {
 
 DEVI void named_bar_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
+// Debug timeline (clock64 stamps of one CTA), enabled by dit_debug_attention_trace.
+__device__ long long* g_attn_trace = nullptr;
+#define TRACE(ev, j)                                                                       \
+  do {                                                                                     \
+    if (trace) trace[(ev) * 64 + ((j) & 63)] = clock64();                                  \
+  } while (0)
+
 struct Maps {
   CUtensorMap q, k, v;   // 3D {128 (d), N, B*H}, box {64, 128, 1}
 };
@@ -147,6 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   const int bh = b * p.H + h;
   const int q0 = blockIdx.x * (NQ * BQ);
   const int nkv = (N + BKV - 1) / BKV;
+  long long* trace = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_attn_trace : nullptr;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
@@ -181,10 +189,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(&k_empty[st], ph ^ 1);
+        TRACE(0, j);
         mbar_expect_tx(&k_full[st], TILE_BYTES);
         tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
         tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
         mbar_wait(&v_empty[st], ph ^ 1);
+        TRACE(1, j);
         mbar_expect_tx(&v_full[st], TILE_BYTES);
         tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
         tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
@@ -197,6 +207,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       auto issue_qk = [&](int t, int j) {
         const int st = j & 1;
         if (t == 0) mbar_wait(&k_full[st], (j >> 1) & 1);
+        if (t == 0) TRACE(2, j);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sQ + t * TILE_BYTES);
         const uint32_t k_addr = smem_u32(sK + st * TILE_BYTES);
@@ -212,7 +223,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       auto issue_pv = [&](int t, int j) {
         const int st = j & 1;
         mbar_wait(&p_full[t], j & 1);
+        TRACE(3 + t, j);
         if (t == 0) mbar_wait(&v_full[st], (j >> 1) & 1);
+        if (t == 0) TRACE(5, j);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + st * TILE_BYTES);
 #pragma unroll
@@ -247,6 +260,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[t], j & 1);
+      if (lane == 0 && (sw % SM_WARPS_PER_TILE) == 0) TRACE(6 + t, j);
       tc_fence_after();
       // pass 1: row max over my 64 columns (scores stay in TMEM)
       const int kv_valid = N - j * BKV - hh * 64;
@@ -327,6 +341,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if (lane == 0 && (sw % SM_WARPS_PER_TILE) == 0) TRACE(8 + t, j);
       if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // epilogue: combine the two halves' row sums, O / l -> bf16 (64 columns per half)
@@ -368,6 +383,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 }
 
 }  // namespace attn_tc
+
+cudaError_t attention_set_trace(long long* buf) {
+  return cudaMemcpyToSymbol(attn_tc::g_attn_trace, &buf, sizeof(buf));
+}
 
 cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
   using namespace attn_tc;

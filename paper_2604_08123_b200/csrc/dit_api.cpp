@@ -1523,6 +1523,34 @@ extern "C" int dit_debug_row_adapter(dit_ctx* c, const dit_batch* b, int32_t* ou
   return rows;
 }
 
+// Test/bench-only: one attention launch on head-major q/k/v [B][H][N][d] (bf16),
+// O written joint-row-major [B*N][H*d] (d = 128 -> tcgen05 kernel).
+extern "C" int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N,
+                                   int32_t d, void* out, void* stream) {
+  if (!q || !k || !v || !out || B < 1 || H < 1 || N < 1) return DIT_EINVAL;
+  AttnParams ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.q = q;
+  ap.k = k;
+  ap.v = v;
+  ap.B = B;
+  ap.H = H;
+  ap.N = N;
+  ap.d = d;
+  ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)d);
+  ap.out = out;
+  ap.ld_out = H * d;
+  ap.split = 0;
+  return attention_launch(ap, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
+namespace dit { cudaError_t attention_set_trace(long long* buf); }
+// Debug: record a clock64 timeline of CTA (0,0,0) of the tcgen05 attention kernel
+// into buf (device, 10 events x 64 iterations of int64); NULL disables.
+extern "C" int dit_debug_attention_trace(void* buf) {
+  return dit::attention_set_trace(static_cast<long long*>(buf)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
 extern "C" int dit_nccl_unique_id(void* out128) {
   if (!out128) return DIT_EINVAL;
   ncclUniqueId id;

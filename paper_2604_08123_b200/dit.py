@@ -67,6 +67,9 @@ EXPORTS = {
     "dit_local_group_destroy": (None, [C.c_void_p]),
     "sp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "dit_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "dit_debug_attention_trace": (C.c_int, [C.c_void_p]),
+    "dit_debug_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_void_p, C.c_void_p]),
     "dit_sp_layout": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_int64), C.c_int64]),
     "dit_debug_row_adapter": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),

@@ -1,0 +1,47 @@
+"""Attention kernel alone: TFLOP/s at the bench shape (B=8, H=24, N=4608, d=128) + a parity spot check vs torch SDPA."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2604_08123_b200 import dit  # noqa: E402
+
+lib = dit.load_library()
+B, H, N, d = [int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (8, 24, 4608, 128))]
+g = torch.Generator(device="cuda").manual_seed(0)
+q, k, v = (torch.randn(B, H, N, d, device="cuda", generator=g, dtype=torch.float32).to(torch.bfloat16) for _ in range(3))
+out = torch.empty(B * N, H * d, device="cuda", dtype=torch.bfloat16)
+s = torch.cuda.current_stream()
+call = lambda: lib.dit_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, H, N, d, out.data_ptr(), C.c_void_p(s.cuda_stream))
+assert call() == 0
+torch.cuda.synchronize()
+ref = torch.nn.functional.scaled_dot_product_attention(q[:1, :2].float(), k[:1, :2].float(), v[:1, :2].float())
+got = out.view(B, N, H, d)[:1, :, :2].permute(0, 2, 1, 3).float()
+err = ((got - ref).abs().max() / ref.abs().max()).item()
+for _ in range(3):
+    call()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n = 10
+e0.record(s)
+for _ in range(n):
+    call()
+e1.record(s)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / n
+fl = 4.0 * B * H * N * N * d
+print(f"attention B={B} H={H} N={N} d={d}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  max-norm err vs SDPA {err:.2e}")
+
+if os.environ.get("TRACE"):
+    tr = torch.zeros(10, 64, dtype=torch.int64, device="cuda")
+    lib.dit_debug_attention_trace(tr.data_ptr())
+    call()
+    torch.cuda.synchronize()
+    lib.dit_debug_attention_trace(None)
+    t = tr.cpu().numpy()
+    base = t[t > 0].min()
+    names = ["k_load", "v_load", "mma_kfull", "mma_p0", "mma_p1", "mma_vfull", "sm_s0", "sm_s1", "sm_p0", "sm_p1"]
+    for j in range(min(12, N // 128)):
+        print(j, " ".join(f"{nm}={(t[e, j] - base) if t[e, j] else -1:6d}" for e, nm in enumerate(names)))
