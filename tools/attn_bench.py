@@ -35,13 +35,16 @@ fl = 4.0 * B * H * N * N * d
 print(f"attention B={B} H={H} N={N} d={d}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  max-norm err vs SDPA {err:.2e}")
 
 if os.environ.get("TRACE"):
-    tr = torch.zeros(10, 64, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(20, 64, dtype=torch.int64, device="cuda")
     lib.dit_debug_attention_trace(tr.data_ptr())
     call()
     torch.cuda.synchronize()
     lib.dit_debug_attention_trace(None)
     t = tr.cpu().numpy()
     base = t[t > 0].min()
-    names = ["k_load", "v_load", "mma_kfull", "mma_p0", "mma_p1", "mma_vfull", "sm_s0", "sm_s1", "sm_p0", "sm_p1"]
+    names = ["k_load", "v_load", "mma_kfull", "mma_p0", "mma_p1", "mma_vfull", "sm_s0", "sm_s1", "sm_p0", "sm_p1",
+             "sm_ld", "sm_bar", "sm_exp", "pv_issued", "qk_issued"]
     for j in range(min(12, N // 128)):
         print(j, " ".join(f"{nm}={(t[e, j] - base) if t[e, j] else -1:6d}" for e, nm in enumerate(names)))
+    print("j=5 per-warp s_full wake:", [int(x - base) for x in t[18, :16]])
+    print("j=5 per-warp p arrive   :", [int(x - base) for x in t[16, :16]])
