@@ -1,23 +1,24 @@
 // attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (d = 128).
 //
 // One CTA = one 128-row query tile of one (request, head); KV tiles of 128 keys.
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512).
+// TMEM (448 of 512 columns): S0 [0,128) S1 [128,256) O [256,384) Q [384,448).
+// Q lives in TMEM (bf16 pairs), so BOTH MMAs are TS-form and shared memory only
+// feeds the B operands (K for S = Q K^T, V for O += P V): the tensor pipe reads
+// 64 B/clk of smem instead of 128, leaving bandwidth for the TMA refills.
+// P_j (bf16) overwrites the first 64 columns of S_j after the scores are read;
+// S_{j+2} = Q K^T is issued after O += P_j V_j (in-order tensor pipe).
 // Roles (576 threads = 18 warps):
-//   warp 0      TMA producer: Q once, K ring (3 stages), V ring (2 stages); 3D
-//               tensor maps [B*H][N][128] so rows past N are zero-filled.
-//   warp 1      TMEM allocator + MMA issuer (one thread): S_{j+2} = Q K^T is
-//               issued right after O += P_j V_j, so while the softmax works on
-//               S_j the tensor pipe already computes the next scores (S is
-//               double-buffered).  QK is SS (both K-major), PV is TS (P from
-//               TMEM, V MN-major in smem).
+//   warp 0      TMA producer: K ring (3 stages), V ring (3 stages); 3D tensor
+//               maps [B*H][N][128] so rows past N are zero-filled.
+//   warp 1      TMEM allocator + MMA issuer (one thread).
 //   warps 2-17  softmax: 4 warps per TMEM lane quarter, each thread owns one
-//               query row and 32 of the 128 score columns (one tcgen05.ld);
-//               the row max is combined through shared memory (128-thread
-//               named barrier per lane quarter), row sums stay per column
-//               quarter until the epilogue.  Lazy O rescale (only when the
-//               running max grows by > 8 in log2 units), packed f32x2
-//               FFMA/FADD, exp2 with 1/4 of the elements on a degree-3
-//               polynomial (FMA pipe) and 3/4 on MUFU, P packed to bf16 and
+//               query row and 32 of the 128 score columns (one tcgen05.ld).
+//               They first stage the Q tile into TMEM (global -> registers ->
+//               tcgen05.st).  Per KV tile: row max combined through shared
+//               memory (128-thread named barrier per lane quarter), lazy O
+//               rescale (only when the running max grows by > 8 in log2
+//               units), packed f32x2 FFMA/FADD, exp2 split between MUFU and a
+//               degree-3 polynomial on the FMA pipe, P packed to bf16 and
 //               stored with tcgen05.st; final O / l epilogue (32 columns each).
 // Synchronisation: mbarriers only (TMA complete_tx, tcgen05.commit, thread
 // arrivals); every waiter can be at most one phase behind.
@@ -31,11 +32,12 @@ namespace attn_tc {
 constexpr int BQ = 128, BKV = 128, HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;         // 32 KB: 128 rows x 128 bf16 (two 64-col swizzle panels)
 constexpr int PANEL = 128 * 64 * 2;              // 16 KB
-constexpr int KST = 3, VST = 2;
-constexpr int SMEM = TILE_BYTES * (1 + KST + VST) + 1024 + 256 + 6144;   // + barriers + row max/sum exchange
+constexpr int KST = 3, VST = 3;
+constexpr int SMEM = TILE_BYTES * (KST + VST) + 1024 + 256 + 6144;   // + barriers + row max/sum exchange
+constexpr int POLY_EVERY = 2;   // 1 of every POLY_EVERY packed pairs of exponentials on the FMA pipe
 constexpr int THREADS = 576;
 constexpr int SM_WARPS = 16;
-constexpr uint32_t COL_S = 0, COL_O = 256, COL_P = 384;
+constexpr uint32_t COL_S = 0, COL_O = 256, COL_Q = 384;
 constexpr float RESCALE_THRESH = 8.0f;
 
 DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -130,19 +132,19 @@ struct Maps {
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + TILE_BYTES;
+  uint8_t* sK = smem;
   uint8_t* sV = sK + KST * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;        // [KST]
-  uint64_t* k_empty = bars + 4;       // [KST]
-  uint64_t* v_full = bars + 7;        // [VST]
-  uint64_t* v_empty = bars + 9;       // [VST]
-  uint64_t* s_full = bars + 11;       // [2]
-  uint64_t* p_full = bars + 13;       // [2]
-  uint64_t* o_done = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* k_full = q_full + 1;      // [KST]
+  uint64_t* k_empty = k_full + KST;   // [KST]
+  uint64_t* v_full = k_empty + KST;   // [VST]
+  uint64_t* v_empty = v_full + VST;   // [VST]
+  uint64_t* s_full = v_empty + VST;   // [2]
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  static_assert(1 + 2 * KST + 2 * VST + 5 + 1 <= 32, "barrier block overflows its 256 bytes");
   float* xmax = reinterpret_cast<float*>(bars + 32);   // [2 parity][4 lane q][4 col q][32]  then l: [4][4][32]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -154,10 +156,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   long long* trace = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_attn_trace : nullptr;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
     tma_prefetch_desc(&maps.v);
-    mbar_init(q_full, 1);
+    mbar_init(q_full, SM_WARPS);
     for (int i = 0; i < KST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -181,9 +182,6 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, TILE_BYTES);
-      tma_load_3d(&maps.q, q_full, sQ, 0, q0, bh);
-      tma_load_3d(&maps.q, q_full, sQ + PANEL, 64, q0, bh);
       // K runs ahead of V by one stage (K is consumed a full iteration earlier)
       int jk = 0, jv = 0;
       while (jv < nkv) {
@@ -210,7 +208,6 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
-      const uint32_t q_addr = smem_u32(sQ);
       auto issue_qk = [&](int j) {
         const int st = j % KST;
         mbar_wait(&k_full[st], (j / KST) & 1);
@@ -221,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          tc_mma_f16(d, smem_desc_k_sw128(q_addr + off), smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
+          mma_ts(d, tmem + COL_Q + kk * 8, smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
         }
         TRACE(14, j);
         tc_commit(&k_empty[st]);
@@ -240,7 +237,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         const uint32_t v_addr = smem_u32(sV + vs * TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tmem + COL_O, tmem + COL_P + (j & 1) * 64 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
+          mma_ts(tmem + COL_O, tmem + COL_S + (j & 1) * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
                  idesc_pv, (j | kk) != 0);
         TRACE(13, j);
         tc_commit(&v_empty[vs]);
@@ -257,6 +254,30 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const int bar_id = 1 + wq;
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY, l = 0.f;
+    {   // stage this thread's 32 Q columns of its query row into TMEM (bf16 pairs)
+      const int n = q0 + row;
+      uint32_t qr[16];
+      if (n < N) {
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(p.q) +
+                                                          ((size_t)bh * N + n) * HD + cq * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 u = __ldg(src + i);
+          qr[4 * i] = u.x;
+          qr[4 * i + 1] = u.y;
+          qr[4 * i + 2] = u.z;
+          qr[4 * i + 3] = u.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) qr[i] = 0u;
+      }
+      tmem_st16(tmem + lane_base + COL_Q + cq * 16, qr);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
     for (int j = 0; j < nkv; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
@@ -304,8 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       for (int e = 0; e < 16; ++e) {
         const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2v, nm);
         float2 pp;
-        if ((e & 3) == 3) {
-          pp = poly_exp2x2(x);                     // 1/4 of the elements on the FMA pipe
+        if ((e % POLY_EVERY) == POLY_EVERY - 1) {
+          pp = poly_exp2x2(x);                     // share of the exponentials on the FMA pipe
         } else {
           pp.x = mufu_exp2(x.x);
           pp.y = mufu_exp2(x.y);
@@ -314,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         pr[e] = pack_bf16(pp.x, pp.y);
       }
       if (lane == 0 && sw == 0) TRACE(12, j);
-      tmem_st16(tmem + lane_base + COL_P + st * 64 + cq * 16, pr);
+      tmem_st16(tmem + lane_base + COL_S + st * 128 + cq * 16, pr);   // P over the first 64 columns of S
       l += acc.x + acc.y;
       tmem_st_wait();
       tc_fence_before();
