@@ -1,25 +1,27 @@
 // attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (d = 128).
 //
-// One CTA = one 128-row query tile of one (request, head); KV tiles of 128 keys.
-// TMEM (448 of 512 columns): S0 [0,128) S1 [128,256) O [256,384) Q [384,448).
-// Q lives in TMEM (bf16 pairs), so BOTH MMAs are TS-form and shared memory only
-// feeds the B operands (K for S = Q K^T, V for O += P V): the tensor pipe reads
-// 64 B/clk of smem instead of 128, leaving bandwidth for the TMA refills.
-// P_j (bf16) overwrites the first 64 columns of S_j after the scores are read;
-// S_{j+2} = Q K^T is issued after O += P_j V_j (in-order tensor pipe).
+// One CTA = TWO 128-row query tiles (256 queries) of one (request, head); KV
+// tiles of 128 keys shared by both query tiles.  TMEM (512 columns):
+//   S0 [0,128)  S1 [128,256)  O0 [256,384)  O1 [384,512);  P_t (bf16) is written
+//   over the first 64 columns of S_t once the scores have been read.
 // Roles (576 threads = 18 warps):
-//   warp 0      TMA producer: K ring (3 stages), V ring (3 stages); 3D tensor
-//               maps [B*H][N][128] so rows past N are zero-filled.
-//   warp 1      TMEM allocator + MMA issuer (one thread).
-//   warps 2-17  softmax: 4 warps per TMEM lane quarter, each thread owns one
-//               query row and 32 of the 128 score columns (one tcgen05.ld).
-//               They first stage the Q tile into TMEM (global -> registers ->
-//               tcgen05.st).  Per KV tile: row max combined through shared
-//               memory (128-thread named barrier per lane quarter), lazy O
-//               rescale (only when the running max grows by > 8 in log2
-//               units), packed f32x2 FFMA/FADD, exp2 split between MUFU and a
-//               degree-3 polynomial on the FMA pipe, P packed to bf16 and
-//               stored with tcgen05.st; final O / l epilogue (32 columns each).
+//   warp 0      TMA producer: Q0/Q1 once, K ring (2 stages), V ring (2 stages);
+//               3D tensor maps [B*H][N][128] so rows past N are zero-filled.
+//   warp 1      TMEM allocator + MMA issuer (one thread).  Ping-pong schedule:
+//                 QK(0,0) QK(1,0) | PV(0,j) QK(0,j+1) PV(1,j) QK(1,j+1) | ...
+//               so the tensor pipe computes one query tile's PV + next scores
+//               while the other tile's softmax runs.  QK is SS (both K-major),
+//               PV is TS (P from TMEM, V MN-major in smem).
+//   warps 2-9   softmax of query tile 0, warps 10-17 of tile 1.  Two warps per
+//               TMEM lane quarter: each thread owns one query row and 64 of the
+//               128 score columns; the row max is combined through shared
+//               memory (64-thread named barrier per lane quarter), the row sum
+//               stays per half until the epilogue.  Lazy O rescale (only when
+//               the running max grows by > 8 in log2 units), packed f32x2
+//               FFMA/FADD, exp2 with 1/4 of the elements on a degree-3
+//               polynomial (FMA pipe) and 3/4 on MUFU, P packed to bf16 and
+//               stored with tcgen05.st; final O / l epilogue (each half writes
+//               64 output columns).
 // Synchronisation: mbarriers only (TMA complete_tx, tcgen05.commit, thread
 // arrivals); every waiter can be at most one phase behind.
 #include "common.cuh"
@@ -29,15 +31,14 @@ namespace dit {
 
 namespace attn_tc {
 
-constexpr int BQ = 128, BKV = 128, HD = 128;
+constexpr int BQ = 128, NQ = 2, BKV = 128, HD = 128;
 constexpr int TILE_BYTES = 128 * HD * 2;         // 32 KB: 128 rows x 128 bf16 (two 64-col swizzle panels)
 constexpr int PANEL = 128 * 64 * 2;              // 16 KB
-constexpr int KST = 3, VST = 3;
-constexpr int SMEM = TILE_BYTES * (KST + VST) + 1024 + 256 + 6144;   // + barriers + row max/sum exchange
-constexpr int POLY_EVERY = 2;   // 1 of every POLY_EVERY packed pairs of exponentials on the FMA pipe
+constexpr int KST = 2, VST = 2;
+constexpr int SMEM = TILE_BYTES * (NQ + KST + VST) + 1024 + 128 + 8192;   // + barriers + row max/sum exchange (6 KB)
 constexpr int THREADS = 576;
-constexpr int SM_WARPS = 16;
-constexpr uint32_t COL_S = 0, COL_O = 256, COL_Q = 384;
+constexpr int SM_WARPS_PER_TILE = 8;
+constexpr uint32_t COL_S = 0, COL_O = 256;
 constexpr float RESCALE_THRESH = 8.0f;
 
 DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -132,46 +133,43 @@ struct Maps {
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = smem;
+  uint8_t* sQ = smem;                              // [NQ] tiles
+  uint8_t* sK = smem + NQ * TILE_BYTES;
   uint8_t* sV = sK + KST * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 1;      // [KST]
-  uint64_t* k_empty = k_full + KST;   // [KST]
-  uint64_t* v_full = k_empty + KST;   // [VST]
-  uint64_t* v_empty = v_full + VST;   // [VST]
-  uint64_t* s_full = v_empty + VST;   // [2]
-  uint64_t* p_full = s_full + 2;      // [2]
-  uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-  static_assert(1 + 2 * KST + 2 * VST + 5 + 1 <= 32, "barrier block overflows its 256 bytes");
-  float* xmax = reinterpret_cast<float*>(bars + 32);   // [2 parity][4 lane q][4 col q][32]  then l: [4][4][32]
+  uint64_t* k_full = bars + 1;        // [KST]
+  uint64_t* k_empty = bars + 3;       // [KST]
+  uint64_t* v_full = bars + 5;        // [VST]
+  uint64_t* v_empty = bars + 7;       // [VST]
+  uint64_t* s_full = bars + 9;        // [NQ]
+  uint64_t* p_full = bars + 11;       // [NQ]
+  uint64_t* o_done = bars + 13;       // [NQ]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  float* xmax = reinterpret_cast<float*>(bars + 16);   // [2 parity][2 tiles][4 quarters][2 halves][32]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int h = blockIdx.y, b = blockIdx.z;
   const int N = p.N;
   const int bh = b * p.H + h;
-  const int q0 = blockIdx.x * BQ;
+  const int q0 = blockIdx.x * (NQ * BQ);
   const int nkv = (N + BKV - 1) / BKV;
   long long* trace = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_attn_trace : nullptr;
 
   if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
     tma_prefetch_desc(&maps.v);
-    mbar_init(q_full, SM_WARPS);
-    for (int i = 0; i < KST; ++i) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < VST; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], SM_WARPS);
+      mbar_init(&p_full[i], SM_WARPS_PER_TILE);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(o_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -182,193 +180,197 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      // K runs ahead of V by one stage (K is consumed a full iteration earlier)
-      int jk = 0, jv = 0;
-      while (jv < nkv) {
-        if (jk < nkv && jk <= jv + 1) {
-          const int st = jk % KST;
-          mbar_wait(&k_empty[st], ((jk / KST) & 1) ^ 1);
-          TRACE(0, jk);
-          mbar_expect_tx(&k_full[st], TILE_BYTES);
-          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, jk * BKV, bh);
-          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, jk * BKV, bh);
-          ++jk;
-        } else {
-          const int st = jv % VST;
-          mbar_wait(&v_empty[st], ((jv / VST) & 1) ^ 1);
-          TRACE(1, jv);
-          mbar_expect_tx(&v_full[st], TILE_BYTES);
-          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, jv * BKV, bh);
-          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, jv * BKV, bh);
-          ++jv;
-        }
+      mbar_expect_tx(q_full, NQ * TILE_BYTES);
+      for (int t = 0; t < NQ; ++t) {
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        TRACE(0, j);
+        mbar_expect_tx(&k_full[st], TILE_BYTES);
+        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
+        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        TRACE(1, j);
+        mbar_expect_tx(&v_full[st], TILE_BYTES);
+        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
+        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
-      auto issue_qk = [&](int j) {
-        const int st = j % KST;
-        mbar_wait(&k_full[st], (j / KST) & 1);
-        TRACE(2, j);
+      auto issue_qk = [&](int t, int j) {
+        const int st = j & 1;
+        if (t == 0) mbar_wait(&k_full[st], (j >> 1) & 1);
+        if (t == 0) TRACE(2, j);
         tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + t * TILE_BYTES);
         const uint32_t k_addr = smem_u32(sK + st * TILE_BYTES);
-        const uint32_t d = tmem + COL_S + (j & 1) * 128;
+        const uint32_t d = tmem + COL_S + t * 128;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          mma_ts(d, tmem + COL_Q + kk * 8, smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
+          tc_mma_f16(d, smem_desc_k_sw128(q_addr + off), smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
         }
-        TRACE(14, j);
-        tc_commit(&k_empty[st]);
-        tc_commit(&s_full[j & 1]);
+        tc_commit(&s_full[t]);
+        if (t == NQ - 1) tc_commit(&k_empty[st]);
       };
-      mbar_wait(q_full, 0);
-      issue_qk(0);
-      if (nkv > 1) issue_qk(1);
-      for (int j = 0; j < nkv; ++j) {
-        const int vs = j % VST;
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        TRACE(3, j);
-        mbar_wait(&v_full[vs], (j / VST) & 1);
-        TRACE(5, j);
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&p_full[t], j & 1);
+        TRACE(3 + t, j);
+        if (t == 0) mbar_wait(&v_full[st], (j >> 1) & 1);
+        if (t == 0) TRACE(5, j);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + vs * TILE_BYTES);
+        const uint32_t v_addr = smem_u32(sV + st * TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tmem + COL_O, tmem + COL_S + (j & 1) * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
+          mma_ts(tmem + COL_O + t * 128, tmem + COL_S + t * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
                  idesc_pv, (j | kk) != 0);
-        TRACE(13, j);
-        tc_commit(&v_empty[vs]);
-        tc_commit(o_done);
-        if (j + 2 < nkv) issue_qk(j + 2);
+        tc_commit(&o_done[t]);
+        if (t == NQ - 1) tc_commit(&v_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        issue_pv(0, j);
+        if (j + 1 < nkv) issue_qk(0, j + 1);
+        issue_pv(1, j);
+        if (j + 1 < nkv) issue_qk(1, j + 1);
       }
     }
-  } else if (warp >= 2) {
+  } else {
     const int sw = warp - 2;
-    const int cq = sw >> 2;                        // column quarter (32 score columns)
+    const int t = sw / SM_WARPS_PER_TILE;          // query tile of this softmax warp
+    const int hh = (sw % SM_WARPS_PER_TILE) / 4;   // column half (64 score columns)
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const int bar_id = 1 + wq;
+    const uint32_t colS = tmem + lane_base + COL_S + t * 128 + hh * 64;
+    const uint32_t colP = tmem + lane_base + COL_S + t * 128 + hh * 32;
+    const uint32_t colO = tmem + lane_base + COL_O + t * 128 + hh * 64;
+    const int bar_id = 1 + t * 4 + wq;
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY, l = 0.f;
-    {   // stage this thread's 32 Q columns of its query row into TMEM (bf16 pairs)
-      const int n = q0 + row;
-      uint32_t qr[16];
-      if (n < N) {
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(p.q) +
-                                                          ((size_t)bh * N + n) * HD + cq * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 u = __ldg(src + i);
-          qr[4 * i] = u.x;
-          qr[4 * i + 1] = u.y;
-          qr[4 * i + 2] = u.z;
-          qr[4 * i + 3] = u.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) qr[i] = 0u;
-      }
-      tmem_st16(tmem + lane_base + COL_Q + cq * 16, qr);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
-    }
     for (int j = 0; j < nkv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      if (lane == 0 && sw == 0) TRACE(6, j);
-      if (lane == 0 && j == 5 && trace) trace[18 * 64 + sw] = clock64();
+      mbar_wait(&s_full[t], j & 1);
+      if (lane == 0 && (sw % SM_WARPS_PER_TILE) == 0) TRACE(6 + t, j);
       tc_fence_after();
-      uint32_t sr[32];
-      tmem_ld32(tmem + lane_base + COL_S + st * 128 + cq * 32, sr);
-      tmem_ld_wait();
-      if (lane == 0 && sw == 0) TRACE(10, j);
-      const int kv_valid = N - j * BKV - cq * 32;
-      if (kv_valid < 32) {
+      // pass 1: row max over my 64 columns (scores stay in TMEM)
+      const int kv_valid = N - j * BKV - hh * 64;
+      float mx;
+      {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(colS, r0);
+        tmem_ld32(colS + 32, r1);
+        tmem_ld_wait();
+        mx = -INFINITY;
+        if (kv_valid >= 64) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[e]), __uint_as_float(r1[e])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (e < kv_valid) mx = fmaxf(mx, __uint_as_float(r0[e]));
+            if (32 + e < kv_valid) mx = fmaxf(mx, __uint_as_float(r1[e]));
+          }
+        }
       }
-      float mx = __uint_as_float(sr[0]);
-#pragma unroll
-      for (int e = 1; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
-      float* xb = xmax + (((j & 1) * 4 + wq) * 4) * 32;
-      xb[cq * 32 + lane] = mx;
-      named_bar_sync(bar_id, 128);
-      if (lane == 0 && sw == 0) TRACE(11, j);
-      mx = fmaxf(fmaxf(xb[lane], xb[32 + lane]), fmaxf(xb[64 + lane], xb[96 + lane])) * sl2;
+      float* xb = xmax + ((((j & 1) * NQ + t) * 4 + wq) * 2) * 32;
+      xb[hh * 32 + lane] = mx;
+      named_bar_sync(bar_id, 64);
+      mx = fmaxf(mx, xb[(hh ^ 1) * 32 + lane]) * sl2;
       const bool need = mx > m_used + RESCALE_THRESH;
       const float m_new = need ? mx : m_used;
       if (j > 0 && __any_sync(0xffffffff, need)) {
         const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
-        mbar_wait(o_done, (j - 1) & 1);
+        mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + COL_O + cq * 32, r);
-        tmem_ld_wait();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          tmem_ld32(colO + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-        tmem_st32(tmem + lane_base + COL_O + cq * 32, r);
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tmem_st32(colO + c * 32, r);
+        }
         tmem_st_wait();
         l *= alpha;
       }
       m_used = m_new;
       const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
       float2 acc = make_float2(0.f, 0.f);
-      uint32_t pr[16];
+      // pass 2: exponentials, P (bf16) over the first half of this tile's S columns
+      uint32_t pr[2][16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2v, nm);
-        float2 pp;
-        if ((e % POLY_EVERY) == POLY_EVERY - 1) {
-          pp = poly_exp2x2(x);                     // share of the exponentials on the FMA pipe
-        } else {
-          pp.x = mufu_exp2(x.x);
-          pp.y = mufu_exp2(x.y);
+      for (int c = 0; c < 2; ++c) {
+        uint32_t sr[32];
+        tmem_ld32(colS + c * 32, sr);
+        tmem_ld_wait();
+        if (kv_valid < 64) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
         }
-        acc = __fadd2_rn(acc, pp);
-        pr[e] = pack_bf16(pp.x, pp.y);
+        uint32_t (&r)[16] = pr[c];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2v, nm);
+          float2 pp;
+          if ((e & 1) == 1) {
+            pp = poly_exp2x2(x);                   // 1/4 of the elements on the FMA pipe
+          } else {
+            pp.x = mufu_exp2(x.x);
+            pp.y = mufu_exp2(x.y);
+          }
+          acc = __fadd2_rn(acc, pp);
+          r[e] = pack_bf16(pp.x, pp.y);
+        }
       }
-      if (lane == 0 && sw == 0) TRACE(12, j);
-      tmem_st16(tmem + lane_base + COL_S + st * 128 + cq * 16, pr);   // P over the first 64 columns of S
+      named_bar_sync(bar_id, 64);   // both halves finished reading S before P overwrites it
+      tmem_st16(colP, pr[0]);
+      tmem_st16(colP + 16, pr[1]);
       l += acc.x + acc.y;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && sw == 0) TRACE(8, j);
-      if (lane == 0 && j == 5 && trace) trace[16 * 64 + sw] = clock64();
-      if (lane == 0 && j == 5 && trace) trace[17 * 64 + sw] = 0;
-      if (lane == 0) mbar_arrive(&p_full[st]);
+      if (lane == 0 && (sw % SM_WARPS_PER_TILE) == 0) TRACE(8 + t, j);
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    // epilogue: combine the 4 column quarters' row sums, O / l -> bf16 (32 columns each)
-    float* lb = xmax + 2 * 4 * 4 * 32 + (wq * 4) * 32;
-    lb[cq * 32 + lane] = l;
-    named_bar_sync(bar_id, 128);
-    l = (lb[lane] + lb[32 + lane]) + (lb[64 + lane] + lb[96 + lane]);
-    mbar_wait(o_done, (nkv - 1) & 1);
+    // epilogue: combine the two halves' row sums, O / l -> bf16 (64 columns per half)
+    float* lb = xmax + 2 * NQ * 4 * 2 * 32 + ((t * 4 + wq) * 2) * 32;   // after the max buffers
+    lb[hh * 32 + lane] = l;
+    named_bar_sync(bar_id, 64);
+    l += lb[(hh ^ 1) * 32 + lane];
+    mbar_wait(&o_done[t], (nkv - 1) & 1);
     tc_fence_after();
-    const int n = q0 + row;
+    const int n = q0 + t * BQ + row;
     const float inv = 1.0f / l;
     bf16* out = reinterpret_cast<bf16*>(p.out);
     const size_t orow = n < N ? (size_t)attn_out_row(p, b, n) : 0;
-    uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD + cq * 32);
-    uint32_t r[32];
-    tmem_ld32(tmem + lane_base + COL_O + cq * 32, r);
-    tmem_ld_wait();
-    if (n < N) {
+    uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD + hh * 64);
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t r[32];
+      tmem_ld32(colO + c * 32, r);
+      tmem_ld_wait();
+      if (n < N) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u;
-        u.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-        u.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-        u.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-        u.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-        dst[q] = u;
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+          dst[c * 4 + q] = u;
+        }
       }
     }
   }
@@ -401,7 +403,7 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
       !make_tmap_3d(&m.k, p.k, HD, rows, heads, s1, s2, 64, 128) ||
       !make_tmap_3d(&m.v, p.v, HD, rows, heads, s1, s2, 64, 128))
     return cudaErrorInvalidValue;
-  dim3 grid((p.N + BQ - 1) / BQ, p.H, p.B);
+  dim3 grid((p.N + NQ * BQ - 1) / (NQ * BQ), p.H, p.B);
   attn_tc_kernel<<<grid, THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
