@@ -11,7 +11,7 @@ import os
 from typing import Dict, Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdit.so")
+LIB_PATH = os.environ.get("DIT_LIB_OVERRIDE") or os.path.join(_HERE, "libdit.so")   # override: perf experiments only
 _lib = None
 
 DIT_OK = 0

@@ -43,7 +43,7 @@ if os.environ.get("TRACE"):
     t = tr.cpu().numpy()
     base = t[t > 0].min()
     names = ["k_load", "v_load", "mma_kfull", "mma_p0", "mma_p1", "mma_vfull", "sm_s0", "sm_s1", "sm_p0", "sm_p1",
-             "sm_ld", "sm_bar", "sm_exp", "pv_issued", "qk_issued"]
+             "pv0_1", "pv0_4", "pv0_8", "qk0_1", "qk0_8"]
     for j in range(min(12, N // 128)):
         print(j, " ".join(f"{nm}={(t[e, j] - base) if t[e, j] else -1:6d}" for e, nm in enumerate(names)))
     print("j=5 per-warp s_full wake:", [int(x - base) for x in t[18, :16]])

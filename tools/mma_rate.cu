@@ -1,0 +1,269 @@
+// mma_rate.cu -- standalone microbenchmark: cycles per tcgen05.mma (kind::f16, bf16 -> fp32)
+// for the shapes the attention / GEMM kernels use.  Operand data is garbage (smem / TMEM
+// contents are irrelevant to throughput).  One CTA (or CTA pair) per SM, all SMs busy.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2604_08123_b200/csrc mma_rate.cu
+#include <cstdio>
+
+#include "common.cuh"
+
+#ifndef ITERS_DEF
+#define ITERS_DEF 4096
+#endif
+constexpr int ITERS = ITERS_DEF;
+
+DEVI uint64_t desc_mn(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// attention-like mix: groups of 8 SS (K-major B) into S, then 8 TS (MN-major B) into O
+template <int MODE, bool RANDOM>
+__global__ void __launch_bounds__(128, 1) mma_mix(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  {  // fill the operand smem with random bf16 values (|x| ~ 1): data-dependent power
+    uint32_t* sp = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < 100 * 1024 / 4; i += blockDim.x) {
+      uint32_t hsh = (uint32_t)(i * 2654435761u) ^ (blockIdx.x * 97u);
+      hsh ^= hsh >> 13; hsh *= 0x5bd1e995u; hsh ^= hsh >> 15;
+      sp[i] = (RANDOM ? ((hsh & 0x807F807Fu) | 0x3F003F00u) : 0u);
+    }
+    __syncthreads();
+  }
+
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (MODE == 2 ? 0u : (1u << 16));
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS / 16; ++i) {
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+        tc_mma_f16(tmem + (i & 1) * 128, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+      }
+      if (MODE >= 1) tc_commit(&bar);
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t bdesc = MODE == 2 ? smem_desc_k_sw128(vb + (kk >> 2) * 16384 + (kk & 3) * 32)
+                                         : desc_mn(vb + kk * 2048, 16384);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
+            "r"(tmem + 384 + (i & 1) * 64 + kk * 8), "l"(bdesc), "r"(id_pv), "r"(1));
+      }
+      if (MODE >= 1) tc_commit(&bar);
+    }
+    tc_commit(&bar);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+// exact attention order: for t in {0,1}: PV(t) [A = P_t from TMEM, D = O_t], QK(t) [D = S_t]
+// ALIAS: P_t lives in the first 64 columns of S_t (WAR hazard PV -> QK); else a separate region.
+__device__ uint8_t* g_src = nullptr;
+template <bool ALIAS, int TMA_STREAM = 0>
+__global__ void __launch_bounds__(128, 1) mma_attn_order(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  __shared__ uint64_t cbar;
+  __shared__ volatile int stop;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); mbar_init(&cbar, 1); stop = 0; fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (TMA_STREAM && threadIdx.x == 64) {
+    // bulk copies of 16 KB from global into smem [98 KB ... ) (a region the MMAs do not read)
+    uint32_t ph = 0;
+    const uint8_t* src = g_src + (size_t)blockIdx.x * (1 << 20);
+    int n = 0;
+    while (!stop && n < 100000) {
+      mbar_expect_tx(&cbar, TMA_STREAM * 16384);
+      for (int c = 0; c < TMA_STREAM; ++c)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::
+                     "r"(smem_u32(smem + 65536 + 32768 + (c & 1) * 16384)), "l"(src + ((n * TMA_STREAM + c) % 48) * 16384),
+                     "r"(smem_u32(&cbar)) : "memory");
+      mbar_wait(&cbar, ph);
+      ph ^= 1;
+      ++n;
+    }
+  }
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    // ALIAS: S0 0, S1 128, O0 256, O1 384, P_t = S_t.  Separate: S0 0, S1 128, O0 256, P0 384, P1 448 (O1 = O0)
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS / 32; ++i) {
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t pcol = ALIAS ? (uint32_t)(t * 128) : (uint32_t)(384 + t * 64);
+        const uint32_t ocol = ALIAS ? (uint32_t)(256 + t * 128) : 256u;
+        for (int kk = 0; kk < 8; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + ocol),
+              "r"(tmem + pcol + kk * 8), "l"(desc_mn(vb + kk * 2048, 16384)), "r"(id_pv), "r"(1));
+        tc_commit(&bar);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma_f16(tmem + t * 128, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+        }
+        tc_commit(&bar);
+      }
+    }
+    tc_commit(&bar);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+    stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+template <int N, bool TS, bool RANDOM = false>
+__global__ void __launch_bounds__(128, 1) mma_1cta(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  {  // fill the operand smem with random bf16 values (|x| ~ 1): data-dependent power
+    uint32_t* sp = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < 100 * 1024 / 4; i += blockDim.x) {
+      uint32_t hsh = (uint32_t)(i * 2654435761u) ^ (blockIdx.x * 97u);
+      hsh ^= hsh >> 13; hsh *= 0x5bd1e995u; hsh ^= hsh >> 15;
+      sp[i] = (RANDOM ? ((hsh & 0x807F807Fu) | 0x3F003F00u) : 0u);
+    }
+    __syncthreads();
+  }
+
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 32) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N);
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS; ++i) {
+      if (TS) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+            "r"(tmem + 384), "l"(smem_desc_k_sw128(b)), "r"(idesc), "r"(1));
+      } else {
+        tc_mma_f16(tmem, smem_desc_k_sw128(a), smem_desc_k_sw128(b), idesc, 1);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+DEVI uint32_t cl_rank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+DEVI void cl_sync() { asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma_2cta(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  cl_sync();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 32 && cl_rank() == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    constexpr uint32_t idesc = idesc_bf16_f32(256, N);
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS; ++i)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+          "l"(smem_desc_k_sw128(a)), "l"(smem_desc_k_sw128(b)), "r"(idesc), "r"(1));
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(&bar)), "h"((uint16_t)1));
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  }
+  tc_fence_before();
+  cl_sync();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <typename K>
+void run(K kern, const char* name, double macs_per_instr, int grid) {
+  long long* d;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+  kern<<<grid, 128, 140 * 1024>>>(d);
+  kern<<<grid, 128, 140 * 1024>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long cyc = 0;
+  cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) { printf("%-34s error %s\n", name, cudaGetErrorString(e)); return; }
+  const double cpi = (double)cyc / ITERS;
+  printf("%-34s %7.1f clk/instr  %7.0f MAC/clk per SM\n", name, cpi, macs_per_instr / cpi / (grid > 148 ? 1 : 1));
+}
+
+int main() {
+  int sms = 148;
+  uint8_t* src;
+  cudaMalloc(&src, (size_t)160 << 20);
+  cudaMemset(src, 0x3f, (size_t)160 << 20);
+  cudaMemcpyToSymbol(g_src, &src, sizeof(src));
+  run(mma_1cta<64, false>, "1cta SS M128 N64 K16", 128.0 * 64 * 16, sms);
+  run(mma_1cta<128, false>, "1cta SS M128 N128 K16", 128.0 * 128 * 16, sms);
+  run(mma_1cta<256, false>, "1cta SS M128 N256 K16", 128.0 * 256 * 16, sms);
+  run(mma_1cta<128, true>, "1cta TS M128 N128 K16", 128.0 * 128 * 16, sms);
+  run(mma_1cta<256, true>, "1cta TS M128 N256 K16", 128.0 * 256 * 16, sms);
+  // per SM of the pair: half the MACs of one 2-CTA instruction
+  run(mma_attn_order<true>, "attn order, P aliased over S", 128.0 * 128 * 16, sms);
+  run(mma_attn_order<false>, "attn order, P separate", 128.0 * 128 * 16, sms);
+  run(mma_attn_order<true, 1>, "attn order + TMA stream 16KB", 128.0 * 128 * 16, sms);
+  run(mma_attn_order<true, 2>, "attn order + TMA stream 2x16KB", 128.0 * 128 * 16, sms);
+  run(mma_mix<1, false>, "mix SS-QK + TS-PV +commits zeros", 128.0 * 128 * 16, sms);
+  run(mma_mix<1, true>, "mix SS-QK + TS-PV +commits RANDOM", 128.0 * 128 * 16, sms);
+  run(mma_1cta<256, false, true>, "1cta SS M128 N256 RANDOM", 128.0 * 256 * 16, sms);
+  run(mma_1cta<128, false, true>, "1cta SS M128 N128 RANDOM", 128.0 * 128 * 16, sms);
+  run(mma_2cta<128>, "2cta SS M256 N128 K16 (per SM)", 128.0 * 128 * 16, sms);
+  run(mma_2cta<256>, "2cta SS M256 N256 K16 (per SM)", 128.0 * 256 * 16, sms);
+  return 0;
+}
