@@ -1,34 +1,30 @@
 // attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (d = 128).
 //
-// A CTA PAIR (cluster of 2 SMs) owns 512 query rows of one (request, head) as
-// two query tiles t = 0, 1 of 256 rows; CTA r holds rows [256 t + 128 r, +128)
-// of each.  Both MMAs are tcgen05.mma.cta_group::2 with M = 256, issued by
-// the leader CTA:
-//   S_t  = Q_t K_j^T   (SS: A = Q_t in each CTA's smem, B = K_j split by keys:
-//                       CTA r holds keys [128 j + 64 r, +64), K-major)
-//   O_t += P_t V_j     (TS: A = P_t in each CTA's TMEM, B = V_j split by head
-//                       dim: CTA r holds d-columns [64 r, +64), MN-major)
-// so each SM streams HALF of every K/V tile (the pair shares operands through
-// the MMA datapath).  KV tiles of 128 keys; 4-stage K and V rings of 16 KB
-// halves.  TMEM per CTA (512 columns): S0 [0,128) S1 [128,256) O0 [256,384)
-// O1 [384,512); P_t (bf16) overwrites the first 64 columns of S_t.
-// Ping-pong schedule (leader, one thread) -- the FA4 schedule:
-//   QK(0,0) QK(1,0) | PV(0,j) QK(0,j+1) PV(1,j) QK(1,j+1) | ...
-// so the tensor pipe computes one query tile's PV + next scores while the
-// other tile's softmax runs.
-// Roles per CTA (576 threads): warps 0-7 softmax of tile 0 and 8-15 of tile 1,
-// warp 16 TMA producer (both CTAs; completion lands on the leader's barriers),
-// warp 17 TMEM allocator (cta_group::2) + MMA issuer (leader only).  The
-// producer / MMA warps take the HIGHEST warp ids because the SMSP arbiter
-// issues highest-id-first: the single MMA thread must never wait behind the
-// softmax warps sharing its SMSP (measured: it otherwise halves MMA throughput).
-// Softmax: two warps per
-// TMEM lane quarter, each thread owns one query row and 64 of the 128 score
-// columns; row max combined through smem (64-thread named barrier), lazy O
-// rescale (only when the running max grows by > 8 in log2 units), packed f32x2
-// math, half the exponentials on a degree-3 polynomial (FMA pipe), P packed to
-// bf16 with tcgen05.st; final O / l epilogue (64 columns per thread).
-// Every mbarrier waiter is at most one phase behind.
+// One CTA = TWO 128-row query tiles (256 queries) of one (request, head); KV
+// tiles of 128 keys shared by both query tiles.  TMEM (512 columns):
+//   S0 [0,128)  S1 [128,256)  O0 [256,384)  O1 [384,512);  P_t (bf16) is written
+//   over the first 64 columns of S_t once the scores have been read.
+// Roles (576 threads = 18 warps; the producer and MMA warps take the HIGHEST
+// ids because the SMSP arbiter issues highest-id-first -- measured +20%):
+//   warp 16     TMA producer: Q0/Q1 once, K ring (2 stages), V ring (2 stages);
+//               3D tensor maps [B*H][N][128] so rows past N are zero-filled.
+//   warp 17     TMEM allocator + MMA issuer (one thread).  Ping-pong schedule:
+//                 QK(0,0) QK(1,0) | PV(0,j) QK(0,j+1) PV(1,j) QK(1,j+1) | ...
+//               so the tensor pipe computes one query tile's PV + next scores
+//               while the other tile's softmax runs.  QK is SS (both K-major),
+//               PV is TS (P from TMEM, V MN-major in smem).
+//   warps 0-7   softmax of query tile 0, warps 8-15 of tile 1.  Two warps per
+//               TMEM lane quarter: each thread owns one query row and 64 of the
+//               128 score columns; the row max is combined through shared
+//               memory (64-thread named barrier per lane quarter), the row sum
+//               stays per half until the epilogue.  Lazy O rescale (only when
+//               the running max grows by > 8 in log2 units), packed f32x2
+//               FFMA/FADD, exp2 with 1/4 of the elements on a degree-3
+//               polynomial (FMA pipe) and 3/4 on MUFU, P packed to bf16 and
+//               stored with tcgen05.st; final O / l epilogue (each half writes
+//               64 output columns).
+// Synchronisation: mbarriers only (TMA complete_tx, tcgen05.commit, thread
+// arrivals); every waiter can be at most one phase behind.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -37,16 +33,12 @@ namespace dit {
 namespace attn_tc {
 
 constexpr int BQ = 128, NQ = 2, BKV = 128, HD = 128;
-constexpr int QTILE = 128 * HD * 2;              // 32 KB: 128 rows x 128 bf16 (two 64-col panels)
-constexpr int QPANEL = 128 * 64 * 2;             // 16 KB
-constexpr int KHALF = 64 * HD * 2;               // 16 KB: 64 keys x 128 d (two 8 KB panels)
-constexpr int KPANEL = 64 * 64 * 2;              // 8 KB
-constexpr int VHALF = 128 * 64 * 2;              // 16 KB: 128 keys x 64 d (one panel)
-constexpr int KST = 4, VST = 4;
-constexpr int XCHG_BYTES = (2 * NQ * 4 * 2 * 32 + NQ * 4 * 2 * 32) * 4;   // row max (double-buffered) + row sum
-constexpr int SMEM = NQ * QTILE + KST * KHALF + VST * VHALF + 1024 /*align*/ + 256 /*barriers*/ + XCHG_BYTES;
+constexpr int TILE_BYTES = 128 * HD * 2;         // 32 KB: 128 rows x 128 bf16 (two 64-col swizzle panels)
+constexpr int PANEL = 128 * 64 * 2;              // 16 KB
+constexpr int KST = 2, VST = 2;
+constexpr int SMEM = TILE_BYTES * (NQ + KST + VST) + 1024 + 128 + 8192;   // + barriers + row max/sum exchange (6 KB)
+constexpr int THREADS = 576;
 constexpr int SM_WARPS_PER_TILE = 8;
-constexpr int THREADS = 64 + NQ * SM_WARPS_PER_TILE * 32;   // 576
 constexpr uint32_t COL_S = 0, COL_O = 256;
 constexpr float RESCALE_THRESH = 8.0f;
 
@@ -71,6 +63,16 @@ DEVI void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 }
 DEVI void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory)
+DEVI void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
 // MN-major SWIZZLE_128B descriptor: 64-element (128 B) rows along MN, 8-row
 // core groups along K 1024 B apart (SBO), next 64-wide MN panel at LBO.
 DEVI uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes) {
@@ -88,14 +90,25 @@ DEVI float mufu_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA/ALU pipes for two arguments (f32x2): x = n + f, n = rint(x),
-// f in [-0.5, 0.5]; 2^f by a degree-3 minimax polynomial (max rel. error 2.1e-4
-// < bf16 half-ulp), 2^n added to the exponent field.  x is clamped at -125 so
-// the exponent of 2^f (126 or 127) minus n never underflows into the sign bit.
+// 2^x on the FMA/ALU pipes: x = n + f, n = rint(x), f in [-0.5, 0.5];
+// 2^f by a degree-3 minimax polynomial (max rel. error 2.1e-4 < bf16 half-ulp),
+// 2^n by adding n to the exponent field.  x is clamped at -125 so the exponent
+// of 2^f (126 or 127) minus n never underflows into the sign bit (2^-125 ~ 0).
+DEVI float poly_exp2(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;             // 1.5 * 2^23: low mantissa bits = rint(x)
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(0.05485438f, f, 0.24182249f);
+  p = fmaf(p, f, 0.69324851f);
+  p = fmaf(p, f, 0.99998755f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Packed version for two arguments (f32x2 FADD/FFMA).
 DEVI float2 poly_exp2x2(float2 x) {
   x.x = fmaxf(x.x, -125.0f);
   x.y = fmaxf(x.y, -125.0f);
-  const float2 magic = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
   const float2 t = __fadd2_rn(x, magic);
   const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
   float2 p = __ffma2_rn(make_float2(0.05485438f, 0.05485438f), f, make_float2(0.24182249f, 0.24182249f));
@@ -115,137 +128,114 @@ __device__ long long* g_attn_trace = nullptr;
   } while (0)
 
 struct Maps {
-  CUtensorMap q;   // 3D {128 (d), N, B*H}, box {64, 128, 1}
-  CUtensorMap k;   // box {64, 64, 1}  (a 64-key half)
-  CUtensorMap v;   // box {64, 128, 1} (a 64-wide d panel of 128 keys)
+  CUtensorMap q, k, v;   // 3D {128 (d), N, B*H}, box {64, 128, 1}
 };
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
+__global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                              // [NQ] 32 KB tiles
-  uint8_t* sK = sQ + NQ * QTILE;                   // [KST] 16 KB halves
-  uint8_t* sV = sK + KST * KHALF;                  // [VST] 16 KB halves
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * VHALF);
+  uint8_t* sQ = smem;                              // [NQ] tiles
+  uint8_t* sK = smem + NQ * TILE_BYTES;
+  uint8_t* sV = sK + KST * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 1;      // [KST]  (the leader's copies are the live ones)
-  uint64_t* k_empty = k_full + KST;   // [KST]
-  uint64_t* v_full = k_empty + KST;   // [VST]
-  uint64_t* v_empty = v_full + VST;   // [VST]
-  uint64_t* s_full = v_empty + VST;   // [NQ]
-  uint64_t* p_full = s_full + NQ;     // [NQ]   (the leader's copy counts both CTAs)
-  uint64_t* o_done = p_full + NQ;     // [NQ]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NQ);
-  static_assert(1 + 2 * KST + 2 * VST + 3 * NQ + 1 <= 32, "barrier block overflows its 256 bytes");
-  float* xmax = reinterpret_cast<float*>(bars + 32);   // [2 parity][NQ][4 q][2 halves][32], then l [NQ][4][2][32]
+  uint64_t* k_full = bars + 1;        // [KST]
+  uint64_t* k_empty = bars + 3;       // [KST]
+  uint64_t* v_full = bars + 5;        // [VST]
+  uint64_t* v_empty = bars + 7;       // [VST]
+  uint64_t* s_full = bars + 9;        // [NQ]
+  uint64_t* p_full = bars + 11;       // [NQ]
+  uint64_t* o_done = bars + 13;       // [NQ]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  float* xmax = reinterpret_cast<float*>(bars + 16);   // [2 parity][2 tiles][4 quarters][2 halves][32]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t cta = cluster_rank();
-  const bool leader = cta == 0;
   const int h = blockIdx.y, b = blockIdx.z;
   const int N = p.N;
   const int bh = b * p.H + h;
-  const int q0 = (blockIdx.x >> 1) * (2 * NQ * BQ);   // 512 query rows per pair
+  const int q0 = blockIdx.x * (NQ * BQ);
   const int nkv = (N + BKV - 1) / BKV;
   long long* trace = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_attn_trace : nullptr;
 
-  constexpr int W_LOAD = 2 * SM_WARPS_PER_TILE, W_MMA = W_LOAD + 1;
+  constexpr int W_LOAD = NQ * SM_WARPS_PER_TILE, W_MMA = W_LOAD + 1;   // highest ids: SMSP arbiter priority
   if (warp == W_LOAD && lane == 0) {
     tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
     tma_prefetch_desc(&maps.v);
-    mbar_init(q_full, 2);
-    for (int i = 0; i < KST; ++i) {
-      mbar_init(&k_full[i], 2);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < VST; ++i) {
-      mbar_init(&v_full[i], 2);
+      mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < NQ; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 2 * SM_WARPS_PER_TILE);
+      mbar_init(&p_full[i], SM_WARPS_PER_TILE);
       mbar_init(&o_done[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == W_MMA) tmem_alloc_2sm<512>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  cluster_sync();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == W_LOAD) {
     if (lane == 0) {
-      if (leader)
-        mbar_expect_tx(q_full, 2 * NQ * QTILE);
-      else
-        mbar_arrive_cta(q_full, 0);
+      mbar_expect_tx(q_full, NQ * TILE_BYTES);
       for (int t = 0; t < NQ; ++t) {
-        const int row = q0 + t * 2 * BQ + (int)cta * BQ;
-        tma_load_3d_2sm(&maps.q, q_full, sQ + t * QTILE, 0, row, bh);
-        tma_load_3d_2sm(&maps.q, q_full, sQ + t * QTILE + QPANEL, 64, row, bh);
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
+        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
       }
       for (int j = 0; j < nkv; ++j) {
-        const int ks = j % KST, vs = j % VST;
-        mbar_wait(&k_empty[ks], ((j / KST) & 1) ^ 1);
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
         TRACE(0, j);
-        if (leader)
-          mbar_expect_tx(&k_full[ks], 2 * KHALF);
-        else
-          mbar_arrive_cta(&k_full[ks], 0);
-        tma_load_3d_2sm(&maps.k, &k_full[ks], sK + ks * KHALF, 0, j * BKV + (int)cta * 64, bh);
-        tma_load_3d_2sm(&maps.k, &k_full[ks], sK + ks * KHALF + KPANEL, 64, j * BKV + (int)cta * 64, bh);
-        mbar_wait(&v_empty[vs], ((j / VST) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], TILE_BYTES);
+        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
+        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+        mbar_wait(&v_empty[st], ph ^ 1);
         TRACE(1, j);
-        if (leader)
-          mbar_expect_tx(&v_full[vs], 2 * VHALF);
-        else
-          mbar_arrive_cta(&v_full[vs], 0);
-        tma_load_3d_2sm(&maps.v, &v_full[vs], sV + vs * VHALF, (int)cta * 64, j * BKV, bh);
+        mbar_expect_tx(&v_full[st], TILE_BYTES);
+        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
+        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
       }
     }
   } else if (warp == W_MMA) {
-    if (leader && lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(2 * BQ, BKV);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(2 * BQ, HD) | (1u << 16);   // B (V) MN-major
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
       auto issue_qk = [&](int t, int j) {
-        const int ks = j % KST;
-        if (t == 0) mbar_wait(&k_full[ks], (j / KST) & 1);
+        const int st = j & 1;
+        if (t == 0) mbar_wait(&k_full[st], (j >> 1) & 1);
         if (t == 0) TRACE(2, j);
         tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQ + t * QTILE);
-        const uint32_t k_addr = smem_u32(sK + ks * KHALF);
+        const uint32_t q_addr = smem_u32(sQ + t * TILE_BYTES);
+        const uint32_t k_addr = smem_u32(sK + st * TILE_BYTES);
+        const uint32_t d = tmem + COL_S + t * 128;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          mma_2sm(tmem + COL_S + t * 128, smem_desc_k_sw128(q_addr + (kk >> 2) * QPANEL + (kk & 3) * 32),
-                  smem_desc_k_sw128(k_addr + (kk >> 2) * KPANEL + (kk & 3) * 32), idesc_qk, kk != 0);
-          if (t == 0 && kk == 0) TRACE(13, j);
-          if (t == 0 && kk == 7) TRACE(14, j);
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          tc_mma_f16(d, smem_desc_k_sw128(q_addr + off), smem_desc_k_sw128(k_addr + off), idesc_qk, kk != 0);
         }
-        commit_2sm_mc(&s_full[t]);
-        if (t == NQ - 1) commit_2sm_mc(&k_empty[ks]);
+        tc_commit(&s_full[t]);
+        if (t == NQ - 1) tc_commit(&k_empty[st]);
       };
       auto issue_pv = [&](int t, int j) {
-        const int vs = j % VST;
+        const int st = j & 1;
         mbar_wait(&p_full[t], j & 1);
         TRACE(3 + t, j);
-        if (t == 0) mbar_wait(&v_full[vs], (j / VST) & 1);
+        if (t == 0) mbar_wait(&v_full[st], (j >> 1) & 1);
         if (t == 0) TRACE(5, j);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + vs * VHALF);
+        const uint32_t v_addr = smem_u32(sV + st * TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          mma_ts_2sm(tmem + COL_O + t * 128, tmem + COL_S + t * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, VHALF),
-                     idesc_pv, (j | kk) != 0);
-          if (t == 0 && kk == 0) TRACE(10, j);
-          if (t == 0 && kk == 3) TRACE(11, j);
-          if (t == 0 && kk == 7) TRACE(12, j);
-        }
-        commit_2sm_mc(&o_done[t]);
-        if (t == NQ - 1) commit_2sm_mc(&v_empty[vs]);
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tmem + COL_O + t * 128, tmem + COL_S + t * 128 + kk * 8, desc_mn_sw128(v_addr + kk * 2048, PANEL),
+                 idesc_pv, (j | kk) != 0);
+        tc_commit(&o_done[t]);
+        if (t == NQ - 1) tc_commit(&v_empty[st]);
       };
       mbar_wait(q_full, 0);
       issue_qk(0, 0);
@@ -259,9 +249,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else {
     const int sw = warp;
-    const int t = sw / SM_WARPS_PER_TILE;           // query tile of this softmax warp
-    const int hh = (sw % SM_WARPS_PER_TILE) / 4;    // column half (64 score columns)
-    const int wq = warp & 3;                        // TMEM lane quarter
+    const int t = sw / SM_WARPS_PER_TILE;          // query tile of this softmax warp
+    const int hh = (sw % SM_WARPS_PER_TILE) / 4;   // column half (64 score columns)
+    const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t colS = tmem + lane_base + COL_S + t * 128 + hh * 64;
@@ -319,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       m_used = m_new;
       const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
       float2 acc = make_float2(0.f, 0.f);
-      // pass 2: exponentials -> P (bf16) over the first half of this tile's S columns
+      // pass 2: exponentials, P (bf16) over the first half of this tile's S columns
       uint32_t pr[2][16];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -331,18 +321,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int e = 0; e < 32; ++e)
             if (c * 32 + e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
         }
+        uint32_t (&r)[16] = pr[c];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2v, nm);
           float2 pp;
           if ((e & 1) == 1) {
-            pp = poly_exp2x2(x);                    // half of the exponentials on the FMA pipe
+            pp = poly_exp2x2(x);                   // 1/4 of the elements on the FMA pipe
           } else {
             pp.x = mufu_exp2(x.x);
             pp.y = mufu_exp2(x.y);
           }
           acc = __fadd2_rn(acc, pp);
-          pr[c][e] = pack_bf16(pp.x, pp.y);
+          r[e] = pack_bf16(pp.x, pp.y);
         }
       }
       named_bar_sync(bar_id, 64);   // both halves finished reading S before P overwrites it
@@ -353,21 +344,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0 && (sw % SM_WARPS_PER_TILE) == 0) TRACE(8 + t, j);
-      if (lane == 0) {
-        if (leader)
-          mbar_arrive(&p_full[t]);
-        else
-          mbar_arrive_cta(&p_full[t], 0);
-      }
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // epilogue: combine the two halves' row sums, O / l -> bf16 (64 columns per half)
-    float* lb = xmax + 2 * NQ * 4 * 2 * 32 + ((t * 4 + wq) * 2) * 32;
+    float* lb = xmax + 2 * NQ * 4 * 2 * 32 + ((t * 4 + wq) * 2) * 32;   // after the max buffers
     lb[hh * 32 + lane] = l;
     named_bar_sync(bar_id, 64);
     l += lb[(hh ^ 1) * 32 + lane];
     mbar_wait(&o_done[t], (nkv - 1) & 1);
     tc_fence_after();
-    const int n = q0 + t * 2 * BQ + (int)cta * BQ + row;
+    const int n = q0 + t * BQ + row;
     const float inv = 1.0f / l;
     bf16* out = reinterpret_cast<bf16*>(p.out);
     const size_t orow = n < N ? (size_t)attn_out_row(p, b, n) : 0;
@@ -391,10 +377,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   }
   tc_fence_before();
-  cluster_sync();
+  __syncthreads();
   if (warp == W_MMA) {
     tc_fence_after();
-    tmem_dealloc_2sm<512>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -416,10 +402,10 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
   const uint64_t rows = (uint64_t)p.N, heads = (uint64_t)p.B * p.H;
   const uint64_t s1 = (uint64_t)HD * 2, s2 = rows * HD * 2;
   if (!make_tmap_3d(&m.q, p.q, HD, rows, heads, s1, s2, 64, 128) ||
-      !make_tmap_3d(&m.k, p.k, HD, rows, heads, s1, s2, 64, 64) ||
+      !make_tmap_3d(&m.k, p.k, HD, rows, heads, s1, s2, 64, 128) ||
       !make_tmap_3d(&m.v, p.v, HD, rows, heads, s1, s2, 64, 128))
     return cudaErrorInvalidValue;
-  dim3 grid(2 * ((p.N + 2 * NQ * BQ - 1) / (2 * NQ * BQ)), p.H, p.B);
+  dim3 grid((p.N + NQ * BQ - 1) / (NQ * BQ), p.H, p.B);
   attn_tc_kernel<<<grid, THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
