@@ -8,15 +8,17 @@
 // tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16), which reads both CTAs'
 // shared memory -- each SM streams half the B operand.
 // Roles (384 threads per CTA, 1 CTA per SM):
-//   warp 0      TMA producer (both CTAs): 6-stage ring of A 128x64 + B 128x64
-//               (SWIZZLE_128B); complete_tx lands on the LEADER's full barrier.
-//   warp 1      MMA issuer (leader only, one thread); tcgen05.commit multicast
-//               releases the stage / publishes the accumulator in both CTAs.
-//   warp 2      TMEM allocator (cta_group::2, 512 columns = 2 accumulators).
-//   warps 4-11  epilogue: warp w reads TMEM lanes 32 (w % 4).. and column half
-//               (w - 4) / 4 of a double-buffered accumulator, then the fused
+//   warps 0-7   epilogue: warp w reads TMEM lanes 32 (w % 4).. and column half
+//               w / 4 of a double-buffered accumulator, then the fused
 //               epilogue of the step row: bias, QK-RMSNorm + RoPE + head-major
 //               scatter, GELU, gated residual (+ControlNet), Euler, LoRA shrink.
+//   warp 8      TMA producer (both CTAs): 6-stage ring of A 128x64 + B 128x64
+//               (SWIZZLE_128B); complete_tx lands on the LEADER's full barrier.
+//   warp 9      MMA issuer (leader only, one thread) + TMEM allocator; tcgen05.commit multicast
+//               releases the stage / publishes the accumulator in both CTAs.
+//   (The producer / MMA warps take the HIGHEST warp ids: the SMSP arbiter
+//   issues highest-id-first, so the single MMA thread never waits behind the
+//   epilogue warps that share its SMSP.)
 // Tiles are scheduled statically per cluster over up to two problems (the
 // img and txt streams of a double block share one launch), rasterised in
 // groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
@@ -32,7 +34,8 @@ constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;           // 128 rows x 64 per CT
 constexpr int B_BYTES = (GEMM_BN / 2) * GEMM_BK * 2;     // 128 rows x 64 per CTA (half of N)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_THREADS = 384;
+constexpr int NUM_THREADS = 320;
+constexpr int W_LOAD = 8, W_MMA = 9;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 size_t gemm_smem_bytes() { return SMEM_BYTES; }
 
@@ -318,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const bool leader = cta == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_LOAD && lane == 0) {
     for (int p = 0; p < args.num_problems; ++p) {
       tma_prefetch_desc(&args.p[p].tmA);
       tma_prefetch_desc(&args.p[p].tmB);
@@ -328,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (warp == 1 && lane == 0) {
+  if (warp == W_MMA && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 2);      // leader: own expect_tx arrival + the peer producer's remote arrival
       mbar_init(&empty[i], 1);     // one multicast commit per phase
@@ -339,13 +342,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == W_LOAD) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -383,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     if (leader && lane == 0) {
       constexpr uint32_t idesc_full = idesc_bf16_f32(2 * GEMM_BM, GEMM_BN);
 
@@ -418,9 +421,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         commit_2sm_mc(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {
+  } else {
     const int wq = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = (warp - 4) >> 2;     // column half of the tile
+    const int half = warp >> 2;           // column half of the tile
     const int row_in_tile = (int)cta * GEMM_BM + wq * 32 + lane;
     int iter = 0;
     for (int t = cid; t < args.total_tiles; t += ncl, ++iter) {
@@ -443,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
   tc_fence_before();
   cluster_sync();
-  if (warp == 2) {
+  if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
   }
