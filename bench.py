@@ -28,8 +28,21 @@ sys.path.insert(0, ROOT)
 
 METRIC = "denoise steps/s (Flux-Dev 1024², mixed LoRA) at 1/2/4/8 B200; % bf16 peak"
 UNIT = "steps/s"
-WORKLOAD = "Flux-Dev-shaped 19+38 blocks, D=3072, 24x128 heads, 1024^2 (4096 img + 512 txt tokens), " \
-           "B=8 cross-workflow batch, 4 distinct rank-64 LoRAs (ids permuted [0,0,1,1,2,2,3,3]), mixed sigmas"
+_FLUX = "Flux-Dev-shaped 19+38 blocks, D=3072, 24x128 heads, "
+# BASELINE.json configs; cfg3 is the metric configuration (the default).
+WORKLOADS = {
+    "cfg2": dict(B=1, h=64, w=64, nt=512, adapters=0, cn=False,
+                 desc=_FLUX + "1024^2 (4096 img + 512 txt tokens), B=1, no adapters"),
+    "cfg3": dict(B=8, h=64, w=64, nt=512, adapters=4, cn=False,
+                 desc=_FLUX + "1024^2 (4096 img + 512 txt tokens), B=8 cross-workflow batch, 4 distinct rank-64 "
+                              "LoRAs (ids permuted [0,0,1,1,2,2,3,3]), mixed sigmas"),
+    "cfg4": dict(B=4, h=64, w=64, nt=512, adapters=0, cn=True,
+                 desc=_FLUX + "1024^2, B=4, ControlNet residual injected into all 19 double blocks (deferred, "
+                              "re-registered every step)"),
+    "cfg5": dict(B=1, h=128, w=128, nt=512, adapters=0, cn=False,
+                 desc=_FLUX + "2048^2 (16384 img + 512 txt tokens), B=1"),
+}
+WORKLOAD = WORKLOADS["cfg3"]["desc"]
 
 
 def load_peaks():
@@ -227,14 +240,15 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = f"cuda:{local}"
     cfg = synth.FLUX
-    B, H_, W_, NT = 8, 64, 64, 512
-    n_ad, rank_lora = 4, 64
-    model = SyntheticDiT(cfg, max_batch=B, max_img_tokens=H_ * W_, max_txt_tokens=NT, max_rank=rank_lora,
-                         max_adapters=n_ad, device=local)
+    wl = WORKLOADS[args.workload]
+    B, H_, W_, NT = wl["B"], wl["h"], wl["w"], wl["nt"]
+    n_ad, rank_lora = wl["adapters"], 64
+    model = SyntheticDiT(cfg, max_batch=B, max_img_tokens=H_ * W_, max_txt_tokens=NT,
+                         max_rank=rank_lora if n_ad else 0, max_adapters=n_ad, device=local)
     for a in range(n_ad):
         model.register_synthetic_lora(a, rank=rank_lora, index=a, scale=1.0)
     if world > 1:
-        # Ulysses SP (strong scaling): the SAME B=8 batch, tokens sharded over the ranks
+        # Ulysses SP (strong scaling): the SAME batch, tokens sharded over the ranks
         import torch.distributed as dist
         from paper_2604_08123_b200.dit import nccl_unique_id
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -247,6 +261,19 @@ def run_gpu(args):
     lat, txt, pooled, out, v = model.device_inputs(batch)
     cb = model.make_batch(B, H_, W_, NT, batch.adapter_id, batch.sigma, batch.sigma_next, batch.guidance,
                           lat, out, txt, pooled, v_out=None, cn_scale=batch.cn_scale)
+    residuals = None
+    if wl["cn"]:
+        from paper_2604_08123_b200.dit import fill_synthetic
+        residuals = torch.empty(B, cfg.depth_double, nil, cfg.hidden, dtype=torch.bfloat16, device=dev)
+        fill_synthetic(residuals, 4000, 0, 0.1 * 3 ** 0.5, 0.0)     # U(-a, a), std 0.1
+
+    def one_step():
+        if residuals is not None:
+            for bb in range(B):
+                for i in range(cfg.depth_double):
+                    model.lib.controlnet_inject(model.ctx, bb, i, residuals[bb, i].data_ptr(), 1.0, None)
+        model.dit_step(cb)
+
     stream = torch.cuda.current_stream()
     flops = model.step_flops(cb)
 
@@ -256,7 +283,7 @@ def run_gpu(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        model.dit_step(cb)
+        one_step()
     torch.cuda.synchronize()
     launches_per_step = model.last_launch_count()
 
@@ -270,7 +297,7 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        model.dit_step(cb)
+        one_step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -301,7 +328,7 @@ def run_gpu(args):
         lat.copy_(h_lat, non_blocking=True)
         txt.copy_(h_txt, non_blocking=True)
         pooled.copy_(h_pool, non_blocking=True)
-        model.dit_step(cb)
+        one_step()
         h_out.copy_(out, non_blocking=True)
     t1.record(stream)
     torch.cuda.synchronize()
@@ -334,7 +361,7 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": B, "seq_len": H_ * W_ + NT,
+        "config": {"workload": wl["desc"], "name": args.workload, "global_batch": B, "seq_len": H_ * W_ + NT,
                    "parallelism": f"ulysses-sp{world}" if world > 1 else "single-gpu",
                    "l2": "inputs larger than L2 (26 GB weights+adapters streamed per step vs 126 MB L2)"},
         "tflops_per_step": flops / 1e12,
@@ -363,7 +390,7 @@ def run_gpu(args):
         "clocks": clk,
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and args.workload == "cfg3":
         line["cpu_baseline"] = cpu_baseline(B)
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -379,6 +406,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS),
+                    help="BASELINE.json config (cfg3 = the metric configuration, default)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
