@@ -27,8 +27,15 @@ def torch_cuda():
 
 
 def check(g, o, what=""):
+    import json
+    import os
+    log = os.environ.get("PARITY_LOG")
     for b in range(o.shape[0]):
         r, c = max_rel(g[b], o[b]), cosine(g[b], o[b])
+        if log:
+            with open(log, "a") as f:
+                f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "what": what,
+                                    "request": b, "max_rel": r, "cos": c}) + "\n")
         assert r <= TOL_REL and c >= TOL_COS, f"{what} request {b}: max_rel={r:.3e} cos={c:.6f}"
 
 
