@@ -22,6 +22,7 @@
 #include <mutex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -147,6 +148,7 @@ struct dit_ctx {
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   LocalGroup* local_group = nullptr;
+  bool force_sp = false;             // test-only: SP data path at world == 1 (DIT_FORCE_SP)
   bf16_t* sp = nullptr;              // [send1 | recv1 | send2 | recv2] at P > 1
   bf16_t* qkv = nullptr;             // attention layout [3][B][H/P][N][d]
   // workspace carve-outs
@@ -256,7 +258,7 @@ Layout layout_of(const dit_config& c) {
   L.h = cv.take(R * D * 4);
   L.u = cv.take(R * D * 2);
   L.qkv = cv.take(3 * R * D * 2);
-  L.sp = cv.take(4 * R * D * 2);
+  L.sp = cv.take(8 * R * D * 2);   // SP send/recv buffers: 8 B*N_loc*D*P elements at any P (incl. the forced P=1 test path)
   L.o = cv.take(R * D * 2);
   L.cat = cv.take(R * (D + F) * 2);
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
@@ -700,7 +702,11 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   if (!c) return DIT_EINVAL;
   if (world < 1 || rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad world/rank %d/%d", world, rank);
   if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
-  if (world == 1) {
+  // DIT_FORCE_SP=1 (test-only): a 1-rank NCCL communicator drives the full
+  // sequence-parallel data path (all-to-alls + gather/scatter) at world == 1.
+  const char* force = getenv("DIT_FORCE_SP");
+  c->force_sp = force && force[0] == '1' && uid != nullptr;
+  if (world == 1 && !c->force_sp) {
     c->world = 1;
     c->rank = 0;
     c->local_group = nullptr;
@@ -1116,6 +1122,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   // [P][3][B][H/P][N_loc][d] -> a2a -> global order -> attention on H/P heads over the
   // full sequence -> O in [P][B][N_loc][H/P*d] -> a2a -> scatter into the local rows.
   const int Hl = H / P, Nglob = P * N;
+  const bool sp = P > 1 || c->force_sp;   // Ulysses exchange active
   auto a2a = [&](const void* snd, void* rcv, size_t count) -> int {
     prof_begin(c, s);
     if (c->comm) {
@@ -1134,7 +1141,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     bf16_t* recv1 = send1 + (size_t)P * pp1;
     bf16_t* send2 = recv1 + (size_t)P * pp1;
     bf16_t* recv2 = send2 + (size_t)P * pp2;
-    if (P > 1) {
+    if (sp) {
       CK(a2a(send1, recv1, pp1));
       CKK(sp_gather_qkv_launch(recv1, c->qkv, P, B, Hl, nt, ni, d, s), 6, 0.0);
     }
@@ -1152,7 +1159,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     ap.nt = nt;
     ap.ni = ni;
     ap.Nt = Nt;
-    if (P == 1) {
+    if (!sp) {
       ap.out = out;
       ap.ld_out = ld_out;
       ap.split = split;
@@ -1162,7 +1169,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       ap.split = 2;
     }
     CKK(attention_launch(ap, s), 1, 4.0 * B * (double)Nglob * Nglob * Hl * d);
-    if (P > 1) {
+    if (sp) {
       CK(a2a(send2, recv2, pp2));
       CKK(sp_scatter_o_launch(recv2, out, ld_out, split, P, B, Hl, nt, ni, d, s), 6, 0.0);
     }
@@ -1219,7 +1226,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.kind = EPI_QKV;
       e.joint_n = N;
       e.D = D;
-      e.qkv = (P == 1) ? c->qkv : c->sp;
+      e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
       e.batch = B;
       e.sp_world = P;
       e.rope = c->rope;
@@ -1358,7 +1365,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.joint_off = 0;
       e.joint_n = N;
       e.D = D;
-      e.qkv = (P == 1) ? c->qkv : c->sp;
+      e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
       e.batch = B;
       e.sp_world = P;
       e.q_gamma = S.qn;

@@ -192,3 +192,28 @@ def test_abi_error_paths(torch_cuda):
     assert lib.sp_init(ctx, 2, 2, None) == E["DIT_EINVAL"]
     torch.cuda.synchronize()
     m.close()
+
+
+def test_nccl_sp_path_world1_bitwise(torch_cuda):
+    """DIT_FORCE_SP: a real 1-rank NCCL communicator drives ncclAlltoAll + gather/scatter at P=1.
+
+    Exercises the exact NCCL calls of the multi-GPU path (ncclCommInitRank, ncclAlltoAll on the
+    compute stream, send/recv layouts) on the one GPU gpurun gives; output must be bitwise equal to
+    the plain P=1 path."""
+    import os
+    from paper_2604_08123_b200.dit import nccl_unique_id
+    cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, rope_axes=(16, 56, 56))
+    batch = synth.make_batch(cfg, 2, 8, 8, 16, n_adapters=1)
+    batch.adapter_id = np.array([0, -1], dtype=np.int32)
+    ref = _model(cfg, 2, 64, 16, rank=8, adapters=1)
+    ref.register_synthetic_lora(0, rank=8, index=0)
+    _, v1 = ref.step(batch)
+    os.environ["DIT_FORCE_SP"] = "1"
+    try:
+        m = _model(cfg, 2, 64, 16, rank=8, adapters=1)
+        m.register_synthetic_lora(0, rank=8, index=0)
+        m.sp_init(1, 0, nccl_unique_id())
+        _, v2 = m.step(batch)
+    finally:
+        del os.environ["DIT_FORCE_SP"]
+    np.testing.assert_array_equal(v2, v1)
