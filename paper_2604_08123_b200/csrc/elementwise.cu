@@ -12,13 +12,29 @@
 namespace dit {
 
 // ------------------------------------------------------------------ LN-modulate
-constexpr int LN_MAXV = 24;   // float4 per lane: D <= 3072
+// One 128-thread block per row: thread t holds float4 columns t + 128 i
+// (i < 6 for D <= 3072) in registers, two block reductions (mean, then the
+// centred variance), modulated bf16 out.  ~40 registers -> full occupancy, so
+// enough 16-byte loads are in flight to run near the HBM roofline.
+constexpr int LN_THREADS = 128;
+constexpr int LN_MAXV = 6;   // float4 per thread: D <= 3072
 
-__global__ void __launch_bounds__(256) lnmod_kernel(const LnModParams p, int total_rows) {
-  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (warp_global >= total_rows) return;
-  int seg = 0, r = warp_global;
+DEVI float block_sum_128(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  v = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(LN_THREADS) lnmod_kernel(const LnModParams p, int total_rows) {
+  __shared__ float red[4];
+  int r = blockIdx.x;
+  if (r >= total_rows) return;
+  int seg = 0;
   if (p.nseg > 1 && r >= p.seg_rows[0]) {
     seg = 1;
     r -= p.seg_rows[0];
@@ -29,32 +45,29 @@ __global__ void __launch_bounds__(256) lnmod_kernel(const LnModParams p, int tot
   const int jrow = b * p.joint_n + p.seg_joint_off[seg] + n;
   const int D = p.D;
   const int nv = D / 4;
+  const int t = threadIdx.x;
   const float4* hrow = reinterpret_cast<const float4*>(p.h + (size_t)jrow * D);
   float4 x[LN_MAXV];
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i) {
-    const int c = lane + 32 * i;
+    const int c = t + LN_THREADS * i;
     if (c < nv) {
-      x[i] = hrow[c];
+      x[i] = __ldcs(hrow + c);
       sum += (x[i].x + x[i].y) + (x[i].z + x[i].w);
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
-  const float mean = sum / (float)D;
+  const float mean = block_sum_128(sum, red) / (float)D;
   float var = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i) {
-    const int c = lane + 32 * i;
+    const int c = t + LN_THREADS * i;
     if (c < nv) {
       const float a = x[i].x - mean, bb = x[i].y - mean, cc = x[i].z - mean, dd = x[i].w - mean;
       var += (a * a + bb * bb) + (cc * cc + dd * dd);
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffff, var, o);
-  const float rstd = rsqrtf(var / (float)D + 1e-6f);
+  const float rstd = rsqrtf(block_sum_128(var, red) / (float)D + 1e-6f);
   const float* modb = p.seg_mod[seg] + (size_t)b * p.mod_stride;
   const float4* sh = reinterpret_cast<const float4*>(modb + p.seg_shift_off[seg]);
   const float4* sc = reinterpret_cast<const float4*>(modb + p.seg_scale_off[seg]);
@@ -62,7 +75,7 @@ __global__ void __launch_bounds__(256) lnmod_kernel(const LnModParams p, int tot
   uint2* urow = reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(p.u) + (size_t)out_row * D);
 #pragma unroll
   for (int i = 0; i < LN_MAXV; ++i) {
-    const int c = lane + 32 * i;
+    const int c = t + LN_THREADS * i;
     if (c < nv) {
       const float4 s4 = __ldg(sh + c), c4 = __ldg(sc + c);
       uint2 o;
@@ -74,11 +87,10 @@ __global__ void __launch_bounds__(256) lnmod_kernel(const LnModParams p, int tot
 }
 
 cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
-  if (p.D % 4 != 0 || p.D / 4 > LN_MAXV * 32) return cudaErrorInvalidValue;
-  int total = p.seg_rows[0] + (p.nseg > 1 ? p.seg_rows[1] : 0);
+  if (p.D % 4 != 0 || p.D / 4 > LN_MAXV * LN_THREADS) return cudaErrorInvalidValue;
+  const int total = p.seg_rows[0] + (p.nseg > 1 ? p.seg_rows[1] : 0);
   if (total <= 0) return cudaSuccess;
-  int blocks = (total * 32 + 255) / 256;
-  lnmod_kernel<<<blocks, 256, 0, s>>>(p, total);
+  lnmod_kernel<<<total, LN_THREADS, 0, s>>>(p, total);
   return cudaGetLastError();
 }
 

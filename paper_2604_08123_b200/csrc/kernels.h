@@ -13,7 +13,10 @@ constexpr int GEMM_TM = 256;      // rows per 2-SM (CTA pair) tile
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_MAX_PROBLEMS = 2;
-constexpr int GEMM_GROUP_M = 16;   // rasterisation: tiles sweep all N within a group of 16 M-tiles
+#ifndef GEMM_GROUP_M_DEF
+#define GEMM_GROUP_M_DEF 16
+#endif
+constexpr int GEMM_GROUP_M = GEMM_GROUP_M_DEF;   // rasterisation: tiles sweep all N within a group of M-tiles
 
 enum EpiKind : int {
   EPI_STORE_H = 0,  // h[jrow][c] = acc + bias                (fp32, embeddings)
