@@ -43,8 +43,12 @@ if os.environ.get("TRACE"):
     t = tr.cpu().numpy()
     base = t[t > 0].min()
     names = ["k_load", "v_load", "mma_kfull", "mma_p0", "mma_p1", "mma_vfull", "sm_s0", "sm_s1", "sm_p0", "sm_p1",
-             "pv0_1", "pv0_4", "pv0_8", "qk0_1", "qk0_8"]
-    for j in range(min(12, N // 128)):
-        print(j, " ".join(f"{nm}={(t[e, j] - base) if t[e, j] else -1:6d}" for e, nm in enumerate(names)))
-    print("j=5 per-warp s_full wake:", [int(x - base) for x in t[18, :16]])
-    print("j=5 per-warp p arrive   :", [int(x - base) for x in t[16, :16]])
+             "ld0", "ld1", "xchg0", "xchg1"]
+    for j in range(min(14, N // 128)):
+        print(j, " ".join(f"{nm}={(t[e, j] - base) if t[e, j] else -1:7d}" for e, nm in enumerate(names)))
+    # per-iteration phase durations of tile 0 (median over j = 4 .. nkv-2)
+    import numpy as np
+    J = range(4, min(60, N // 128) - 1)
+    d = lambda a, b_, dj=0: int(np.median([t[b_, j + dj] - t[a, j] for j in J]))
+    print("tile0: S wake->ld done", d(6, 10), " ld->xchg", d(10, 12), " xchg->P arrive", d(12, 8),
+          " P arrive->MMA sees it", d(8, 3), " MMA issues PV0 -> next S0 wake", d(3, 6, 1), " period", d(6, 6, 1))

@@ -140,6 +140,197 @@ __global__ void __launch_bounds__(128, 1) mma_attn_order(long long* out) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
 }
 
+
+// attention MMA order with LDW extra warps streaming tcgen05.ld (32x32b.x32) from the S
+// columns (and, if ST, tcgen05.st of 16 bf16x2 columns into the P region) concurrently:
+// does softmax-side TMEM traffic slow the tensor pipe?
+template <int LDW, bool ST, bool MMA_ON = true, int NLD = 1>
+__global__ void __launch_bounds__(640, 1) mma_with_ld(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  __shared__ volatile int stop;
+  __shared__ unsigned long long nld;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); stop = 0; nld = 0; fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp >= 4 && warp < 4 + LDW) {
+    const uint32_t lq = (uint32_t)(warp & 3) * 32;
+    uint32_t r[32], r2[32], r3[32], r4[32];
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    while (!stop && n < 2000000) {
+      const uint32_t col = (uint32_t)((n & 3) * 32);
+      tmem_ld32(tmem + (lq << 16) + col, r);
+      if (NLD >= 2) tmem_ld32(tmem + (lq << 16) + ((col + 32) & 127), r2);
+      if (NLD >= 4) { tmem_ld32(tmem + (lq << 16) + ((col + 64) & 127), r3); tmem_ld32(tmem + (lq << 16) + ((col + 96) & 127), r4); }
+      tmem_ld_wait();
+      #pragma unroll
+      for (int i = 0; i < 32; ++i) acc += r[i] + (NLD >= 2 ? r2[i] : 0u) + (NLD >= 4 ? r3[i] ^ r4[i] : 0u);
+      if (ST) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                     ::"r"(tmem + (lq << 16) + 128 + (uint32_t)((n & 3) * 16)), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+                     "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+                     "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      ++n;
+    }
+    if (acc == 0x12345) out[1] = acc;
+    if ((threadIdx.x & 31) == 0) atomicAdd(&nld, n);
+  }
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    long long t0 = clock64();
+    if (!MMA_ON) { while (clock64() - t0 < 64 * ITERS) {} }
+    for (int i = 0; i < (MMA_ON ? ITERS / 32 : 0); ++i) {
+      for (int t = 0; t < 2; ++t) {
+        for (int kk = 0; kk < 8; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256 + t * 128),
+              "r"(tmem + 192 + kk * 8), "l"(desc_mn(vb + kk * 2048, 16384)), "r"(id_pv), "r"(1));
+        tc_commit(&bar);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma_f16(tmem + t * 64, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+        }
+        tc_commit(&bar);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; }
+    stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[2] = (long long)nld;
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+// attention MMA order with ALUW extra warps hammering the FMA pipe (FFMA2) and MUFU (ex2):
+// does heavy CUDA-core work on the same SM slow the tensor pipe?
+template <int ALUW, int KIND>
+__global__ void __launch_bounds__(640, 1) mma_with_alu(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); stop = 0; fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp >= 4 && warp < 4 + ALUW) {
+    float2 a[8];
+    for (int i = 0; i < 8; ++i) a[i] = make_float2(threadIdx.x * 1e-3f + i, i * 0.5f);
+    float e[8];
+    for (int i = 0; i < 8; ++i) e[i] = -(float)i * 0.01f * threadIdx.x;
+    int n = 0;
+    while (!stop && n < 1000000) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (KIND & 1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], make_float2(0.999f, 0.999f), make_float2(1e-3f, 2e-3f));
+        }
+        if (KIND & 2) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(e[i])); e[i] = y * -0.5f; }
+        }
+      }
+      ++n;
+    }
+    float sacc = 0;
+    for (int i = 0; i < 8; ++i) sacc += a[i].x + a[i].y + e[i];
+    if (sacc == 1234.5f) out[1] = 1;
+  }
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    for (int w = 0; w < 20000; ++w) __nanosleep(100);   // let the ALU warps ramp up
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS / 32; ++i) {
+      for (int t = 0; t < 2; ++t) {
+        for (int kk = 0; kk < 8; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256 + t * 128),
+              "r"(tmem + 192 + kk * 8), "l"(desc_mn(vb + kk * 2048, 16384)), "r"(id_pv), "r"(1));
+        tc_commit(&bar);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma_f16(tmem + t * 64, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+        }
+        tc_commit(&bar);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; }
+    stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+// serialized groups: issue G MMAs (PV-form then QK-form halves) + commit, wait for the
+// commit, repeat -- the per-group latency an empty tensor pipe adds.
+template <int G>
+__global__ void __launch_bounds__(128, 1) mma_group_latency(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    const int groups = ITERS / G;
+    long long t0 = clock64();
+    for (int i = 0; i < groups; ++i) {
+      for (int kk = 0; kk < G; ++kk) {
+        if (kk < G / 2 || G == 8) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
+              "r"(tmem + 192 + (kk & 7) * 8), "l"(desc_mn(vb + (kk & 7) * 2048, 16384)), "r"(id_pv), "r"(1));
+        } else {
+          const int k2 = kk & 7;
+          const uint32_t off = (k2 >> 2) * 16384 + (k2 & 3) * 32;
+          tc_mma_f16(tmem, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, k2 != 0);
+        }
+      }
+      tc_commit(&bar);
+      mbar_wait(&bar, i & 1);
+    }
+    long long t1 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
 template <int N, bool TS, bool RANDOM = false>
 __global__ void __launch_bounds__(128, 1) mma_1cta(long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -243,6 +434,24 @@ void run(K kern, const char* name, double macs_per_instr, int grid) {
   printf("%-34s %7.1f clk/instr  %7.0f MAC/clk per SM\n", name, cpi, macs_per_instr / cpi / (grid > 148 ? 1 : 1));
 }
 
+template <typename K>
+void run_ld(K kern, const char* name, int grid, int ldw) {
+  long long* d;
+  cudaMalloc(&d, 24);
+  cudaMemset(d, 0, 24);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+  kern<<<grid, 640, 140 * 1024>>>(d);
+  kern<<<grid, 640, 140 * 1024>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[3] = {0, 0, 0};
+  cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) { printf("%-34s error %s\n", name, cudaGetErrorString(e)); return; }
+  const double cpi = (double)h[0] / ITERS;
+  printf("%-34s %7.1f clk/instr  %7.0f MAC/clk per SM  ld batches per clk (all warps) %.3f  clk per batch per warp %.0f\n",
+         name, cpi, 128.0 * 128 * 16 / cpi, (double)h[2] / (double)h[0], (double)h[0] * ldw / (double)(h[2] + 1));
+}
+
 int main() {
   int sms = 148;
   uint8_t* src;
@@ -255,6 +464,22 @@ int main() {
   run(mma_1cta<128, true>, "1cta TS M128 N128 K16", 128.0 * 128 * 16, sms);
   run(mma_1cta<256, true>, "1cta TS M128 N256 K16", 128.0 * 256 * 16, sms);
   // per SM of the pair: half the MACs of one 2-CTA instruction
+  run(mma_group_latency<1>, "serial groups of 1 MMA", 128.0 * 128 * 16, sms);
+  run(mma_group_latency<2>, "serial groups of 2 MMA", 128.0 * 128 * 16, sms);
+  run(mma_group_latency<8>, "serial groups of 8 MMA (PV)", 128.0 * 128 * 16, sms);
+  run(mma_group_latency<16>, "serial groups of 16 MMA (PV+QK)", 128.0 * 128 * 16, sms);
+  run(mma_group_latency<64>, "serial groups of 64 MMA", 128.0 * 128 * 16, sms);
+  run_ld(mma_with_ld<4, false>, "attn order + 4 ld warps", sms, 4);
+  run_ld(mma_with_ld<16, false>, "attn order + 16 ld warps", sms, 16);
+  run_ld(mma_with_ld<16, true>, "attn order + 16 ld+st warps", sms, 16);
+  run_ld(mma_with_ld<4, false, false>, "NO MMA, 4 ld warps x1", sms, 4);
+  run_ld(mma_with_ld<4, false, false, 2>, "NO MMA, 4 ld warps x2", sms, 4);
+  run_ld(mma_with_ld<4, false, false, 4>, "NO MMA, 4 ld warps x4", sms, 4);
+  run_ld(mma_with_ld<16, false, false>, "NO MMA, 16 ld warps x1", sms, 16);
+  run_ld(mma_with_ld<16, false, false, 4>, "NO MMA, 16 ld warps x4", sms, 16);
+  run_ld(mma_with_ld<4, false, true, 2>, "MMA, 4 ld warps x2", sms, 4);
+  run_ld(mma_with_ld<4, false, true, 4>, "MMA, 4 ld warps x4", sms, 4);
+  run_ld(mma_with_ld<16, false, true, 4>, "MMA, 16 ld warps x4", sms, 16);
   run(mma_attn_order<true>, "attn order, P aliased over S", 128.0 * 128 * 16, sms);
   run(mma_attn_order<false>, "attn order, P separate", 128.0 * 128 * 16, sms);
   run(mma_attn_order<true, 1>, "attn order + TMA stream 16KB", 128.0 * 128 * 16, sms);
