@@ -49,7 +49,11 @@ DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef MBAR_SUSPEND_HINT
+#define MBAR_SUSPEND_HINT 1
+#endif
 DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if MBAR_SUSPEND_HINT
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -57,6 +61,15 @@ DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA
@@ -103,6 +116,80 @@ DEVI void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// Warp-converged issue (call with all 32 lanes; one lane elected inside the asm): eight
+// K=16 SS MMAs covering K = 128 of two K-major SWIZZLE_128B operands laid out as two
+// 64-column panels `panel` bytes apart.  Descriptor offsets are added in PTX so every
+// operand stays warp-uniform (no per-MMA register->uniform moves or elect loops).
+template <uint32_t PANEL_BYTES>
+DEVI void tc_mma_ss_k128_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  constexpr uint32_t P4 = PANEL_BYTES >> 4;
+  asm volatile(
+      "{\n\t.reg .pred L, p;\n\t.reg .b32 alo, ahi, blo, bhi, x, y;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|L, -1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 {alo, ahi}, %1;\n\tmov.b64 {blo, bhi}, %2;\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s32 x, alo, 2;\n\tadd.s32 y, blo, 2;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 4;\n\tadd.s32 y, blo, 4;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 6;\n\tadd.s32 y, blo, 6;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, %5;\n\tadd.s32 y, blo, %5;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, %6;\n\tadd.s32 y, blo, %6;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, %7;\n\tadd.s32 y, blo, %7;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, %8;\n\tadd.s32 y, blo, %8;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum), "n"(P4), "n"(P4 + 2), "n"(P4 + 4), "n"(P4 + 6)
+      : "memory");
+}
+// Warp-converged: eight K=16 TS MMAs (A = bf16 pairs in TMEM, 8 columns per step; B
+// MN-major SWIZZLE_128B, 8 K-rows = 1024 B per step) covering K = 128.
+DEVI void tc_mma_ts_k128_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred L, p;\n\t.reg .b32 blo, bhi, y, ta;\n\t.reg .b64 b;\n\t"
+      "elect.sync _|L, -1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 {blo, bhi}, %2;\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.s32 ta, %1, 8;\n\tadd.s32 y, blo, 128;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 16;\n\tadd.s32 y, blo, 256;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 24;\n\tadd.s32 y, blo, 384;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 32;\n\tadd.s32 y, blo, 512;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 40;\n\tadd.s32 y, blo, 640;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 48;\n\tadd.s32 y, blo, 768;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t"
+      "add.s32 ta, %1, 56;\n\tadd.s32 y, blo, 896;\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// Warp-converged single TS MMA (one elected lane issues).
+DEVI void tc_mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred L, p;\n\t"
+      "elect.sync _|L, -1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// Warp-converged commit (one elected lane).
+DEVI void tc_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred L;\n\telect.sync _|L, -1;\n\t"
+      "@L tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete.
 DEVI void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

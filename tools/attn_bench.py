@@ -52,3 +52,5 @@ if os.environ.get("TRACE"):
     d = lambda a, b_, dj=0: int(np.median([t[b_, j + dj] - t[a, j] for j in J]))
     print("tile0: S wake->ld done", d(6, 10), " ld->xchg", d(10, 12), " xchg->P arrive", d(12, 8),
           " P arrive->MMA sees it", d(8, 3), " MMA issues PV0 -> next S0 wake", d(3, 6, 1), " period", d(6, 6, 1))
+    print("MMA thread: k_full wait", d(14, 2), " p_full0 wait", d(15, 3), " p_full1 wait", d(16, 4),
+          " PV0 issue start -> QK0 k_full wait start", d(5, 14, 1), " QK0 issued -> PV1 wait start", d(2, 16))

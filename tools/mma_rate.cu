@@ -331,6 +331,130 @@ __global__ void __launch_bounds__(128, 1) mma_group_latency(long long* out) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
 }
 
+// attention MMA order (2 tiles x [8 PV + 8 QK]) with the synchronisation the kernel does
+// around each group: MODE 1 = tcgen05.fence::after_thread_sync before each group,
+// MODE 2 = + mbarrier wait on an already-completed phase, MODE 3 = + the MMA thread waits
+// for the commit of the group two groups back (what the data dependencies allow at best).
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) mma_sync_cost(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar[4];
+  __shared__ uint64_t done;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    mbar_init(&done, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 32) {
+    mbar_arrive(&done);   // phase 0 complete
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    long long t0 = clock64();
+    int g = 0;
+    for (int i = 0; i < ITERS / 32; ++i) {
+      for (int t = 0; t < 2; ++t, ++g) {
+        if (MODE >= 2) mbar_wait(&done, 0);
+        if (MODE == 3 && g >= 2) mbar_wait(&bar[t], ((g - 2) >> 1) & 1);
+        if (MODE >= 1) tc_fence_after();
+        for (int kk = 0; kk < 8; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256 + t * 128),
+              "r"(tmem + t * 128 + kk * 8), "l"(desc_mn(vb + kk * 2048, 16384)), "r"(id_pv), "r"(1));
+        tc_commit(&bar[2 + t]);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma_f16(tmem + t * 128, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+        }
+        tc_commit(&bar[t]);
+      }
+    }
+    mbar_wait(&bar[1], ((g - 1) >> 1) & 1);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+// attention MMA order while one thread keeps DEPTH 16-KB bulk copies global->smem in flight
+// (ring over a 64-KB smem region the MMAs do not read): smem write bandwidth vs. SS operand reads.
+template <int DEPTH>
+__global__ void __launch_bounds__(128, 1) mma_with_tma_ring(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  __shared__ uint64_t cb[8];
+  __shared__ volatile int stop;
+  __shared__ unsigned long long nbytes;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar, 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&cb[i], 1);
+    stop = 0;
+    nbytes = 0;
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (DEPTH > 0 && threadIdx.x == 64) {
+    const uint8_t* src = g_src + (size_t)(blockIdx.x % 8) * (1 << 20);   // L2-resident source
+    long long n = 0;
+    while (!stop && n < 4000000) {
+      const int slot = (int)(n % (DEPTH > 0 ? DEPTH : 1));
+      if (n >= DEPTH) mbar_wait(&cb[slot], (uint32_t)(((n / (DEPTH > 0 ? DEPTH : 1)) - 1) & 1));
+      mbar_expect_tx(&cb[slot], 16384);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::
+                   "r"(smem_u32(smem + 98304 + slot * 16384)), "l"(src + (n % 64) * 16384), "r"(smem_u32(&cb[slot])) : "memory");
+      ++n;
+    }
+    nbytes = (unsigned long long)n * 16384;
+  }
+  if (threadIdx.x == 32) {
+    const uint32_t q = smem_u32(smem), kb = smem_u32(smem + 32768), vb = smem_u32(smem + 65536);
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);
+    for (int w = 0; w < 2000; ++w) __nanosleep(100);
+    long long t0 = clock64();
+    for (int i = 0; i < ITERS / 32; ++i) {
+      for (int t = 0; t < 2; ++t) {
+        for (int kk = 0; kk < 8; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256 + t * 128),
+              "r"(tmem + t * 128 + kk * 8), "l"(desc_mn(vb + kk * 2048, 16384)), "r"(id_pv), "r"(1));
+        tc_commit(&bar);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma_f16(tmem + t * 128, smem_desc_k_sw128(q + off), smem_desc_k_sw128(kb + off), id_qk, kk != 0);
+        }
+        tc_commit(&bar);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; }
+    stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[2] = (long long)(nbytes / 64);
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
 template <int N, bool TS, bool RANDOM = false>
 __global__ void __launch_bounds__(128, 1) mma_1cta(long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -435,13 +559,14 @@ void run(K kern, const char* name, double macs_per_instr, int grid) {
 }
 
 template <typename K>
-void run_ld(K kern, const char* name, int grid, int ldw) {
+void run_ld(K kern, const char* name, int grid, int ldw, int threads = 640, int smem_kb = 140) {
   long long* d;
   cudaMalloc(&d, 24);
   cudaMemset(d, 0, 24);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  kern<<<grid, 640, 140 * 1024>>>(d);
-  kern<<<grid, 640, 140 * 1024>>>(d);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kb * 1024);
+  kern<<<grid, threads, smem_kb * 1024>>>(d);
+  kern<<<grid, threads, smem_kb * 1024>>>(d);
+  if (cudaGetLastError() != cudaSuccess) { printf("%-34s launch error\n", name); return; }
   cudaError_t e = cudaDeviceSynchronize();
   long long h[3] = {0, 0, 0};
   cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
@@ -464,6 +589,14 @@ int main() {
   run(mma_1cta<128, true>, "1cta TS M128 N128 K16", 128.0 * 128 * 16, sms);
   run(mma_1cta<256, true>, "1cta TS M128 N256 K16", 128.0 * 256 * 16, sms);
   // per SM of the pair: half the MACs of one 2-CTA instruction
+  run_ld(mma_with_tma_ring<0>, "attn order, no TMA", sms, 1, 128, 180);
+  run_ld(mma_with_tma_ring<1>, "attn order + TMA ring depth 1", sms, 1, 128, 180);
+  run_ld(mma_with_tma_ring<2>, "attn order + TMA ring depth 2", sms, 1, 128, 180);
+  run_ld(mma_with_tma_ring<4>, "attn order + TMA ring depth 4", sms, 1, 128, 180);
+  run(mma_sync_cost<0>, "attn order, no sync", 128.0 * 128 * 16, sms);
+  run(mma_sync_cost<1>, "attn order + fence::after", 128.0 * 128 * 16, sms);
+  run(mma_sync_cost<2>, "attn order + done-wait + fence", 128.0 * 128 * 16, sms);
+  run(mma_sync_cost<3>, "attn order + wait group g-2", 128.0 * 128 * 16, sms);
   run(mma_group_latency<1>, "serial groups of 1 MMA", 128.0 * 128 * 16, sms);
   run(mma_group_latency<2>, "serial groups of 2 MMA", 128.0 * 128 * 16, sms);
   run(mma_group_latency<8>, "serial groups of 8 MMA (PV)", 128.0 * 128 * 16, sms);
