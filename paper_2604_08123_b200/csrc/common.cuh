@@ -310,6 +310,32 @@ DEVI void mma_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t
       : "memory");
 }
 // arrive on the mbarrier at this smem offset in BOTH CTAs once prior MMAs complete
+// Warp-converged (call with all 32 lanes of the leader CTA's MMA warp): the four K=16 MMAs of
+// one 64-wide K-block of two K-major SWIZZLE_128B operands (+32 B per step), one elected lane.
+DEVI void mma_2sm_k64_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred L, p;\n\t.reg .b32 alo, ahi, blo, bhi, x, y;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|L, -1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 {alo, ahi}, %1;\n\tmov.b64 {blo, bhi}, %2;\n\t"
+      "@L tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s32 x, alo, 2;\n\tadd.s32 y, blo, 2;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 4;\n\tadd.s32 y, blo, 4;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 6;\n\tadd.s32 y, blo, 6;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+DEVI void commit_2sm_mc_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred L;\n\telect.sync _|L, -1;\n\t"
+      "@L tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 DEVI void commit_2sm_mc(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
