@@ -367,9 +367,10 @@ def run_gpu(args):
         "tflops_per_step": flops / 1e12,
         "achieved_tflops": flops / (ms_step / 1e3) / 1e12,
         "pct_bf16_peak": 100.0 * flops / (ms_step / 1e3) / 1e12 / (world * peaks["bf16"]),
-        "roofline": {"bound": "tensor", "kernel": "gemm_kernel (tcgen05 128x256x64, fused epilogues)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_kernel (2-SM tcgen05, 256x256x64 pair tiles, fused epilogues)",
                      "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                      "frac": (achieved / peaks["bf16_sus"]) if achieved else None, "traffic": traffic,
+                     "traffic_source": "ncu dram__bytes_read.sum+dram__bytes_write.sum per gemm_kernel launch, mean over one warm step (profiles/gemm_traffic.json)" if traffic else None,
                      "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside the long step)",
                      "launches": g_n, "share_of_step": g_ms / prof_total if prof_total else None},
         "kernels": {

@@ -63,7 +63,10 @@ static_assert(2 * 128 * ATTN_REG_SOFTMAX + 128 * ATTN_REG_OTHER <= THREADS * 168
 #ifndef ATTN_POLY_MOD
 #define ATTN_POLY_MOD 4
 #endif
-constexpr int POLY_MOD = ATTN_POLY_MOD;   // every POLY_MOD-th exp2 pair on the FMA-pipe polynomial
+#ifndef ATTN_POLY_RES
+#define ATTN_POLY_RES 1
+#endif
+constexpr int POLY_MOD = ATTN_POLY_MOD, POLY_RES = ATTN_POLY_RES;   // every POLY_MOD-th exp2 pair on the FMA-pipe polynomial
 constexpr uint32_t COL_S = 0, COL_O = 256;
 constexpr float RESCALE_THRESH = 8.0f;
 
@@ -181,15 +184,15 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   uint64_t* p_full = bars + 11;       // [NQ]
   uint64_t* o_done = bars + 13;       // [NQ]
   uint64_t* p_tail = bars + 15;       // [NQ] last quarter of P stored (split P arrive)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* o_free = bars + 17;       // [NQ] epilogue has read O (next work item may overwrite it)
+  uint64_t* q_empty = bars + 19;      // last QK of a work item done (Q tiles reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int h = blockIdx.y, b = blockIdx.z;
   const int N = p.N;
-  const int bh = b * p.H + h;
-  const int q0 = blockIdx.x * (NQ * BQ);
   const int nkv = (N + BKV - 1) / BKV;
-  long long* trace = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? g_attn_trace : nullptr;
+  const int nqb = (N + NQ * BQ - 1) / (NQ * BQ);
+  const int total = nqb * p.H * p.B;               // work items: (query block, head, request), block fastest
 
   constexpr int W_LOAD = NQ * SM_WARPS_PER_TILE + 2, W_MMA = W_LOAD + 1;   // highest ids: SMSP arbiter priority
   if (warp == W_LOAD && lane == 0) {
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     tma_prefetch_desc(&maps.k);
     tma_prefetch_desc(&maps.v);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       mbar_init(&p_full[i], SM_WARPS_PER_TILE);
       mbar_init(&o_done[i], 1);
       mbar_init(&p_tail[i], SM_WARPS_PER_TILE);
+      mbar_init(&o_free[i], SM_WARPS_PER_TILE);
     }
     fence_barrier_init();
   }
@@ -216,26 +221,32 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   const uint32_t tmem = *tmem_slot;
   if (warp >= NQ * SM_WARPS_PER_TILE) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REG_OTHER));
+   long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;   // loaded after setmaxnreg (no spill)
    if (warp == W_LOAD) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, NQ * TILE_BYTES);
-      for (int t = 0; t < NQ; ++t) {
-        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
-        tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        TRACE(0, j);
-        mbar_expect_tx(&k_full[st], TILE_BYTES);
-        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
-        tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        TRACE(1, j);
-        mbar_expect_tx(&v_full[st], TILE_BYTES);
-        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
-        tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+      int g = 0, it = 0;                           // kv-tile counter (ring position), item counter
+      for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+        const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
+        mbar_expect_tx(q_full, NQ * TILE_BYTES);
+        for (int t = 0; t < NQ; ++t) {
+          tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
+          tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
+        }
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int st = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          mbar_wait(&k_empty[st], ph ^ 1);
+          if (it == 0) TRACE(0, j);
+          mbar_expect_tx(&k_full[st], TILE_BYTES);
+          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
+          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          if (it == 0) TRACE(1, j);
+          mbar_expect_tx(&v_full[st], TILE_BYTES);
+          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
+          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+        }
       }
     }
   } else if (warp == W_MMA) {
@@ -244,24 +255,27 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
     constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-    auto issue_qk = [&](int t, int j) {
-      const int st = j & 1;
-      if (t == 0 && lane == 0) TRACE(14, j);
-      if (t == 0 && (ATTN_FAKE != 3 || j < 2)) mbar_wait(&k_full[st], (j >> 1) & 1);
-      if (t == 0 && lane == 0) TRACE(2, j);
+    bool tr = false;
+    // g: global kv-tile index (K/V ring stage + phase, and the s/p/o barrier phases)
+    auto issue_qk = [&](int t, int g, int j) {
+      const int st = g & 1;
+      if (t == 0 && lane == 0 && tr) TRACE(14, j);
+      if (t == 0) mbar_wait(&k_full[st], (g >> 1) & 1);
+      if (t == 0 && lane == 0 && tr) TRACE(2, j);
       tc_fence_after();
       tc_mma_ss_k128_warp<PANEL>(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
                                  smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
       tc_commit_warp(&s_full[t]);
       if (t == NQ - 1) tc_commit_warp(&k_empty[st]);
     };
-    auto issue_pv = [&](int t, int j) {
-      const int st = j & 1;
-      if (lane == 0) TRACE(15 + t, j);
-      mbar_wait(&p_full[t], j & 1);
-      if (lane == 0) TRACE(3 + t, j);
-      if (t == 0 && (ATTN_FAKE != 3 || j < 2)) mbar_wait(&v_full[st], (j >> 1) & 1);
-      if (t == 0 && lane == 0) TRACE(5, j);
+    auto issue_pv = [&](int t, int g, int j, int it) {
+      const int st = g & 1;
+      if (lane == 0 && tr) TRACE(15 + t, j);
+      mbar_wait(&p_full[t], g & 1);
+      if (lane == 0 && tr) TRACE(3 + t, j);
+      if (j == 0 && it > 0) mbar_wait(&o_free[t], (it - 1) & 1);   // previous item's O read out
+      if (t == 0) mbar_wait(&v_full[st], (g >> 1) & 1);
+      if (t == 0 && lane == 0 && tr) TRACE(5, j);
       tc_fence_after();
       {
         // P columns of kv [0, 96) are released first (split arrive), the last 32 after
@@ -270,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < 6; ++kk)
           tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, (j | kk) != 0);
-        mbar_wait(&p_tail[t], j & 1);
+        mbar_wait(&p_tail[t], g & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 6; kk < 8; ++kk) tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, 1);
@@ -278,18 +292,27 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       tc_commit_warp(&o_done[t]);
       if (t == NQ - 1) tc_commit_warp(&v_empty[st]);
     };
-    mbar_wait(q_full, 0);
-    issue_qk(0, 0);
-    issue_qk(1, 0);
-    for (int j = 0; j < nkv; ++j) {
-      issue_pv(0, j);
-      if (j + 1 < nkv) issue_qk(0, j + 1);
-      issue_pv(1, j);
-      if (j + 1 < nkv) issue_qk(1, j + 1);
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it, g += nkv) {
+      tr = trace != nullptr && it == 0;
+      mbar_wait(q_full, it & 1);
+      issue_qk(0, g, 0);
+      issue_qk(1, g, 0);
+      if (nkv == 1) tc_commit_warp(q_empty);
+      for (int j = 0; j < nkv; ++j) {
+        issue_pv(0, g + j, j, it);
+        if (j + 1 < nkv) issue_qk(0, g + j + 1, j + 1);
+        issue_pv(1, g + j, j, it);
+        if (j + 1 < nkv) {
+          issue_qk(1, g + j + 1, j + 1);
+          if (j + 2 == nkv) tc_commit_warp(q_empty);   // last QK of this item issued
+        }
+      }
     }
    }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ATTN_REG_SOFTMAX));
+    long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
     // softmax: warps 0-3 own query tile 0, warps 4-7 tile 1; one query row per thread
     // (TMEM lane = row), all 128 score columns of it in registers: no cross-warp exchange.
     const int t = warp >> 2;
@@ -299,135 +322,143 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const uint32_t colS = tmem + lane_base + COL_S + t * 128;
     const uint32_t colO = tmem + lane_base + COL_O + t * 128;
     const float sl2 = p.scale_log2;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      if (lane == 0 && wq == 0) TRACE(6 + t, j);
-      tc_fence_after();
-#if ATTN_FAKE
-      {  // timing experiment: no softmax math (ATTN_FAKE=1: no S read either)
-        uint32_t z[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) z[e] = 0x3f803f80u;
-        if (ATTN_FAKE == 2) {
-          uint32_t sr[32];
-          for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, sr);
-          tmem_ld_wait();
-          if (sr[lane] == 0x12345678u) z[0] = 0;
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_st16(colS + c * 16, z);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0 && wq == 0) TRACE(8 + t, j);
-        if (lane == 0) mbar_arrive(&p_full[t]);
-        l = 1.f;
-        continue;
-      }
-#endif
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-      tmem_ld_wait();
-      if (lane == 0 && wq == 0) TRACE(10 + t, j);
-      const int kv_valid = N - j * BKV;
-      if (kv_valid < BKV) {
-#pragma unroll
-        for (int e = 0; e < 128; ++e)
-          if (e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
-      }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int e = 0; e < 128; e += 8)
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-          m4[a] = fmaxf(m4[a], fmaxf(__uint_as_float(sr[e + 2 * a]), __uint_as_float(sr[e + 2 * a + 1])));
-      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
-      if (lane == 0 && wq == 0) TRACE(12 + t, j);
-      const bool need = mx > m_used + RESCALE_THRESH;
-      const float m_new = need ? mx : m_used;
-      if (j > 0 && __any_sync(0xffffffff, need)) {
-        const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
-        mbar_wait(&o_done[t], (j - 1) & 1);
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const bool tr = trace != nullptr && it == 0 && lane == 0 && wq == 0;
+      const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
+      const int b = bh / p.H, h = bh - b * p.H;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j, ++g) {
+        mbar_wait(&s_full[t], g & 1);
+        if (tr) TRACE(6 + t, j);
         tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          uint32_t r[16];
-          tmem_ld16(colO + c * 16, r);
-          tmem_ld_wait();
+#if ATTN_FAKE
+        {  // timing experiment: no softmax math (ATTN_FAKE=1: no S read either)
+          uint32_t z[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st16(colO + c * 16, r);
-        }
-        tmem_st_wait();
-        l *= alpha;
-      }
-      m_used = m_new;
-      const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
-      // exponentials (kept in sr as fp32 for the row sum); P (bf16 pairs) over the first 64
-      // columns of this row's S, 16 at a time
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[32 * c + 2 * e]), __uint_as_float(sr[32 * c + 2 * e + 1])), sl2v, nm);
-          float2 pp;
-          if ((e % POLY_MOD) == POLY_MOD - 1) {
-            pp = poly_exp2x2(x);                   // 1/POLY_MOD of the elements on the FMA pipe
-          } else {
-            pp.x = mufu_exp2(x.x);
-            pp.y = mufu_exp2(x.y);
+          for (int e = 0; e < 16; ++e) z[e] = 0x3f803f80u;
+          if (ATTN_FAKE == 2) {
+            uint32_t sr[32];
+            for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, sr);
+            tmem_ld_wait();
+            if (sr[lane] == 0x12345678u) z[0] = 0;
           }
-          sr[32 * c + 2 * e] = __float_as_uint(pp.x);
-          sr[32 * c + 2 * e + 1] = __float_as_uint(pp.y);
-          r[e] = pack_bf16(pp.x, pp.y);
-        }
-        tmem_st16(colS + c * 16, r);
-        if (c == 2) {   // kv [0, 96) of P are in TMEM: let the PV MMA start on them
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_st16(colS + c * 16, z);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0 && wq == 0) TRACE(8 + t, j);
+          if (tr) TRACE(8 + t, j);
           if (lane == 0) mbar_arrive(&p_full[t]);
+          if (lane == 0) mbar_arrive(&p_tail[t]);
+          l = 1.f;
+          continue;
         }
+#endif
+        uint32_t sr[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        tmem_ld_wait();
+        if (tr) TRACE(10 + t, j);
+        const int kv_valid = N - j * BKV;
+        if (kv_valid < BKV) {
+#pragma unroll
+          for (int e = 0; e < 128; ++e)
+            if (e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
+        }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int e = 0; e < 128; e += 8)
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            m4[a] = fmaxf(m4[a], fmaxf(__uint_as_float(sr[e + 2 * a]), __uint_as_float(sr[e + 2 * a + 1])));
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
+        if (tr) TRACE(12 + t, j);
+        const bool need = mx > m_used + RESCALE_THRESH;
+        const float m_new = need ? mx : m_used;
+        if (j > 0 && __any_sync(0xffffffff, need)) {
+          const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
+          mbar_wait(&o_done[t], (g - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t r[16];
+            tmem_ld16(colO + c * 16, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            tmem_st16(colO + c * 16, r);
+          }
+          tmem_st_wait();
+          l *= alpha;
+        }
+        m_used = m_new;
+        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
+        // exponentials (kept in sr as fp32 for the row sum); P (bf16 pairs) over the first 64
+        // columns of this row's S, 16 at a time
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[32 * c + 2 * e]), __uint_as_float(sr[32 * c + 2 * e + 1])), sl2v, nm);
+            float2 pp;
+            if ((e % POLY_MOD) >= POLY_MOD - POLY_RES) {
+              pp = poly_exp2x2(x);                   // POLY_RES/POLY_MOD of the pairs on the FMA pipe
+            } else {
+              pp.x = mufu_exp2(x.x);
+              pp.y = mufu_exp2(x.y);
+            }
+            sr[32 * c + 2 * e] = __float_as_uint(pp.x);
+            sr[32 * c + 2 * e + 1] = __float_as_uint(pp.y);
+            r[e] = pack_bf16(pp.x, pp.y);
+          }
+          tmem_st16(colS + c * 16, r);
+          if (c == 2) {   // kv [0, 96) of P are in TMEM: let the PV MMA start on them
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (tr) TRACE(8 + t, j);
+            if (lane == 0) mbar_arrive(&p_full[t]);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_tail[t]);
+        // row sum off the critical path (the PV MMA is already running)
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 128; e += 4) {
+          acc0 = __fadd2_rn(acc0, make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])));
+          acc1 = __fadd2_rn(acc1, make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])));
+        }
+        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
       }
-      tmem_st_wait();
+      // epilogue: read O out of TMEM, release it to the next work item, then O / l -> bf16
+      // (one 256-byte output row per thread)
+      mbar_wait(&o_done[t], (g - 1) & 1);
+      tc_fence_after();
+      uint32_t o[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(colO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32 * c]));
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_tail[t]);
-      // row sum off the critical path (the PV MMA is already running)
-      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < 128; e += 4) {
-        acc0 = __fadd2_rn(acc0, make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])));
-        acc1 = __fadd2_rn(acc1, make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])));
-      }
-      l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-    }
-    // epilogue: O / l -> bf16, one 256-byte output row per thread
-    mbar_wait(&o_done[t], (nkv - 1) & 1);
-    tc_fence_after();
-    const int n = q0 + t * BQ + row;
-    const float inv = 1.0f / l;
-    bf16* out = reinterpret_cast<bf16*>(p.out);
-    const size_t orow = n < N ? (size_t)attn_out_row(p, b, n) : 0;
-    uint4* dst = reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD);
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      tmem_ld32(colO + c * 32, r);
-      tmem_ld_wait();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+      const int n = q0 + t * BQ + row;
       if (n < N) {
+        const float inv = 1.0f / l;
+        bf16* out = reinterpret_cast<bf16*>(p.out);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)attn_out_row(p, b, n) * p.ld_out + (size_t)h * HD);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 16; ++q) {
           uint4 u;
-          u.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-          dst[c * 4 + q] = u;
+          u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+          dst[q] = u;
         }
       }
     }
@@ -461,8 +492,16 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
       !make_tmap_3d(&m.k, p.k, HD, rows, heads, s1, s2, 64, 128) ||
       !make_tmap_3d(&m.v, p.v, HD, rows, heads, s1, s2, 64, 128))
     return cudaErrorInvalidValue;
-  dim3 grid((p.N + NQ * BQ - 1) / (NQ * BQ), p.H, p.B);
-  attn_tc_kernel<<<grid, THREADS, SMEM, s>>>(m, p);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // persistent: one CTA per SM walks work items (query block fastest, so the CTAs running at
+  // the same time share each head's K/V in L2)
+  const int total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
+  attn_tc_kernel<<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
 
