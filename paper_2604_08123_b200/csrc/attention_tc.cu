@@ -366,13 +366,16 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           for (int e = 0; e < 128; ++e)
             if (e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
         }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float m8[8];
 #pragma unroll
-        for (int e = 0; e < 128; e += 8)
+        for (int a = 0; a < 8; ++a) m8[a] = fmaxf(__uint_as_float(sr[2 * a]), __uint_as_float(sr[2 * a + 1]));
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-            m4[a] = fmaxf(m4[a], fmaxf(__uint_as_float(sr[e + 2 * a]), __uint_as_float(sr[e + 2 * a + 1])));
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
+        for (int e = 16; e < 128; e += 16)
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+            m8[a] = fmaxf(m8[a], fmaxf(__uint_as_float(sr[e + 2 * a]), __uint_as_float(sr[e + 2 * a + 1])));
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
         if (tr) TRACE(12 + t, j);
         const bool need = mx > m_used + RESCALE_THRESH;
         const float m_new = need ? mx : m_used;
@@ -425,9 +428,14 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_tail[t]);
-        // row sum off the critical path (the PV MMA is already running)
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        uint64_t tok = 0;
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(smem_u32(&p_tail[t])) : "memory");
+        // row sum off the critical path (the PV MMA is already running): seeded with a zero
+        // derived from the arrive's state token, so ptxas cannot hoist it above the arrive
+        tok = __shfl_sync(0xffffffffu, tok, 0);
+        const float z = tok == ~0ull ? 1.0f : 0.0f;
+        float2 acc0 = make_float2(z, z), acc1 = make_float2(z, z);
 #pragma unroll
         for (int e = 0; e < 128; e += 4) {
           acc0 = __fadd2_rn(acc0, make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])));
