@@ -117,6 +117,40 @@ DEVI void store_bf16_32(bf16* dst, const float (&x)[32], int valid) {
   }
 }
 
+// d = 128 QKV epilogue helpers: 64 accumulator columns + bias -> y (fp32)
+DEVI void load_head_half(uint32_t taddr, const bf16* bias, float (&y)[64]) {
+  tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&y[0]));
+  tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&y[32]));
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 64; j += 8) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(bias + j));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      y[j + 2 * e] += bf16_lo(w[e]);
+      y[j + 2 * e + 1] += bf16_hi(w[e]);
+    }
+  }
+}
+// RMSNorm scale (rs * gamma) then RoPE on interleaved pairs; cs = (cos, sin) pairs of these columns
+DEVI void norm_rope_half(float (&y)[64], float rs, const bf16* g, const float4* cs) {
+#pragma unroll
+  for (int j = 0; j < 64; j += 8) {
+    const uint4 gu = __ldg(reinterpret_cast<const uint4*>(g + j));
+    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+    const float4 c01 = __ldg(cs + j / 4), c23 = __ldg(cs + j / 4 + 1);
+    const float cr[4][2] = {{c01.x, c01.y}, {c01.z, c01.w}, {c23.x, c23.y}, {c23.z, c23.w}};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float x0 = y[j + 2 * e] * rs * bf16_lo(gw[e]);
+      const float x1 = y[j + 2 * e + 1] * rs * bf16_hi(gw[e]);
+      y[j + 2 * e] = cr[e][0] * x0 - cr[e][1] * x1;
+      y[j + 2 * e + 1] = cr[e][1] * x0 + cr[e][0] * x1;
+    }
+  }
+}
+
 // Epilogue for one accumulator tile.  Thread = one accumulator row; this warp
 // covers columns [c_lo, c_lo + 128) of the 256-wide tile.
 #ifndef GEMM_EPI_FAKE
@@ -156,6 +190,44 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
       if (col0 < E.qkv_cols) {
         const int sec = col0 / D;
         const int head = (col0 - sec * D) / d;
+        const int hl_n = E.heads / E.sp_world;
+        const int dest = head / hl_n, hl = head - dest * hl_n;
+        bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
+                    (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
+        if (d == 128) {
+          // head in two 64-column halves: half 0 read for the RMS statistic, half 1 read and
+          // kept, processed, then half 0 re-read and processed (3 TMEM reads instead of 8)
+          float ss = 0.f;
+          if (sec < 2) {
+            float y[64];
+            load_head_half(tbase + c0, bias + col0, y);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) ss = fmaf(y[e], y[e], ss);
+          }
+          float y[64];
+          load_head_half(tbase + c0 + 64, bias + col0 + 64, y);   // (tcgen05.ld: all lanes)
+          float rs = 1.f;
+          if (sec < 2) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) ss = fmaf(y[e], y[e], ss);
+            rs = rsqrtf(ss / (float)d + 1e-6f);
+          }
+          const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
+          const float4* cs = reinterpret_cast<const float4*>(E.rope + (size_t)(E.joint_off + nloc) * (d / 2));
+          if (sec < 2) norm_rope_half(y, rs, g + 64, cs + 16);
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 32) store_bf16_32(dst + 64 + j, *reinterpret_cast<const float(*)[32]>(&y[j]), 32);
+          }
+          load_head_half(tbase + c0, bias + col0, y);
+          if (sec < 2) norm_rope_half(y, rs, g, cs);
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 32) store_bf16_32(dst + j, *reinterpret_cast<const float(*)[32]>(&y[j]), 32);
+          }
+          continue;
+        }
+        // generic head size (d = 32 / 64 test configurations): two passes of 32 columns
         // pass 1: sum of squares over the head (q, k only)
         float rs = 1.f;
         if (sec < 2) {
@@ -175,10 +247,6 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           }
           rs = rsqrtf(ss / (float)d + 1e-6f);
         }
-        const int hl_n = E.heads / E.sp_world;
-        const int dest = head / hl_n, hl = head - dest * hl_n;
-        bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
-                    (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
         const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
         const float2* cs = E.rope + (size_t)(E.joint_off + nloc) * (d / 2);
         // pass 2: normalise, rotate interleaved pairs, store
@@ -243,18 +311,24 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
   }
 
 #pragma unroll 1
-  for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+  for (int c2 = c_lo; c2 < c_hi; c2 += 64) {
+    if (n0 + c2 >= P.N) break;
+    // two 32-column accumulator reads in flight per wait
+    uint32_t rr2[64];
+    tmem_ld32(tbase + c2, *reinterpret_cast<uint32_t(*)[32]>(&rr2[0]));
+    tmem_ld32(tbase + c2 + 32, *reinterpret_cast<uint32_t(*)[32]>(&rr2[32]));
+    tmem_ld_wait();
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int c0 = c2 + hh * 32;
     const int col = n0 + c0;
     if (col >= P.N) break;
-    uint32_t rr[32];
-    tmem_ld32(tbase + c0, rr);
-    tmem_ld_wait();
     if (!row_ok) continue;
     const int valid = min(32, P.N - col);
     float bv[32], y[32];
     load_bias32(bias, col, P.N, bv);
 #pragma unroll
-    for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr[e]) + bv[e];
+    for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr2[hh * 32 + e]) + bv[e];
     if (E.kind == EPI_GELU) {
 #pragma unroll
       for (int e = 0; e < 32; ++e) y[e] = gelu_tanh_f(y[e]);
@@ -323,6 +397,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         }
       }
     }
+  }
   }
 }
 
