@@ -355,7 +355,7 @@ def run_gpu(args):
             traffic = json.load(open(tp)).get("bytes_per_launch")
         except Exception:
             traffic = None
-    prof_total = sum(p[0] for p in prof.values())
+    prof_total = sum(prof[k][0] for k in range(7))   # kinds 0-6 partition the step (10-18 split kind 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -14,6 +14,8 @@ def launch_list(path):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
         k = r["Kernel Name"].split("(")[0].split("<")[0]
+        if k.endswith("fill_synth_kernel"):   # synthetic weight generation (setup, not part of a step)
+            continue
         scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "msecond": 1.0}.get(r["Metric Unit"], 1e-6)
         agg[k][0] += 1
         agg[k][1] += float(r["Metric Value"].replace(",", "")) * scale
