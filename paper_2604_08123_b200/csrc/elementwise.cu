@@ -86,11 +86,113 @@ __global__ void __launch_bounds__(LN_THREADS) lnmod_kernel(const LnModParams p, 
   }
 }
 
+// Persistent variant for large row counts: each 128-thread block walks rows
+// r = blockIdx.x, +gridDim.x, ...; one thread streams the NEXT row of fp32 h into
+// a shared-memory stage with a bulk copy (cp.async.bulk, mbarrier complete_tx)
+// while the block normalises the current one from the other stage, so the HBM
+// reads stay in flight independently of the reductions (the one-block-per-row
+// kernel is limited by register occupancy to ~120 KB in flight per SM).
+constexpr int LNP_STAGES = 2;
+constexpr int LNP_MAXD = 3072;
+
+DEVI int ln_row_of(const LnModParams& p, int r, int& seg, int& b, int& n, int& out_row) {
+  seg = 0;
+  out_row = r;
+  if (p.nseg > 1 && r >= p.seg_rows[0]) {
+    seg = 1;
+    r -= p.seg_rows[0];
+  }
+  const int rpr = p.seg_rows_per_req[seg];
+  b = r / rpr;
+  n = r - b * rpr;
+  return b * p.joint_n + p.seg_joint_off[seg] + n;   // row of h
+}
+
+__global__ void __launch_bounds__(LN_THREADS) lnmod_persistent_kernel(const __grid_constant__ LnModParams p, int total_rows) {
+  __shared__ __align__(128) float4 stage[LNP_STAGES][LNP_MAXD / 4];
+  __shared__ __align__(8) uint64_t full[LNP_STAGES];
+  __shared__ float red[4];
+  const int D = p.D, nv = D / 4, t = threadIdx.x;
+  const uint32_t bytes = (uint32_t)D * 4;
+  if (t == 0) {
+    for (int i = 0; i < LNP_STAGES; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int r, int st) {
+    int seg, b, n, orow;
+    const int jrow = ln_row_of(p, r, seg, b, n, orow);
+    mbar_expect_tx(&full[st], bytes);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                     "r"(smem_u32(&stage[st][0])), "l"(p.h + (size_t)jrow * D), "r"(bytes), "r"(smem_u32(&full[st]))
+                 : "memory");
+  };
+  int it = 0;
+  if (t == 0 && (int)blockIdx.x < total_rows) issue(blockIdx.x, 0);
+  for (int r = blockIdx.x; r < total_rows; r += gridDim.x, ++it) {
+    const int st = it % LNP_STAGES;
+    // the stage being refilled was released by the __syncthreads at the end of the last row
+    if (t == 0 && r + (int)gridDim.x < total_rows) issue(r + gridDim.x, (it + 1) % LNP_STAGES);
+    mbar_wait(&full[st], (it / LNP_STAGES) & 1);
+    int seg, b, n, out_row;
+    ln_row_of(p, r, seg, b, n, out_row);
+    float4 x[LN_MAXV];
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i) {
+      const int c = t + LN_THREADS * i;
+      if (c < nv) {
+        x[i] = stage[st][c];
+        sum += (x[i].x + x[i].y) + (x[i].z + x[i].w);
+      }
+    }
+    const float mean = block_sum_128(sum, red) / (float)D;
+    float var = 0.f;
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i) {
+      const int c = t + LN_THREADS * i;
+      if (c < nv) {
+        const float a = x[i].x - mean, bb = x[i].y - mean, cc = x[i].z - mean, dd = x[i].w - mean;
+        var += (a * a + bb * bb) + (cc * cc + dd * dd);
+      }
+    }
+    const float rstd = rsqrtf(block_sum_128(var, red) / (float)D + 1e-6f);
+    const float* modb = p.seg_mod[seg] + (size_t)b * p.mod_stride;
+    const float4* sh = reinterpret_cast<const float4*>(modb + p.seg_shift_off[seg]);
+    const float4* sc = reinterpret_cast<const float4*>(modb + p.seg_scale_off[seg]);
+    uint2* urow = reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(p.u) + (size_t)out_row * D);
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i) {
+      const int c = t + LN_THREADS * i;
+      if (c < nv) {
+        const float4 s4 = __ldg(sh + c), c4 = __ldg(sc + c);
+        uint2 o;
+        o.x = pack_bf16((1.f + c4.x) * ((x[i].x - mean) * rstd) + s4.x, (1.f + c4.y) * ((x[i].y - mean) * rstd) + s4.y);
+        o.y = pack_bf16((1.f + c4.z) * ((x[i].z - mean) * rstd) + s4.z, (1.f + c4.w) * ((x[i].w - mean) * rstd) + s4.w);
+        urow[c] = o;
+      }
+    }
+    // (block_sum_128's trailing __syncthreads already ordered every read of this stage
+    // before the next iteration's refill of it)
+  }
+}
+
 cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
   if (p.D % 4 != 0 || p.D / 4 > LN_MAXV * LN_THREADS) return cudaErrorInvalidValue;
   const int total = p.seg_rows[0] + (p.nseg > 1 ? p.seg_rows[1] : 0);
   if (total <= 0) return cudaSuccess;
-  lnmod_kernel<<<total, LN_THREADS, 0, s>>>(p, total);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool aligned = (reinterpret_cast<uintptr_t>(p.h) & 15) == 0 && (p.D * 4) % 16 == 0;
+  if (p.D <= LNP_MAXD && aligned && total >= 8 * sms) {
+    lnmod_persistent_kernel<<<8 * sms, LN_THREADS, 0, s>>>(p, total);
+  } else {
+    lnmod_kernel<<<total, LN_THREADS, 0, s>>>(p, total);
+  }
   return cudaGetLastError();
 }
 
