@@ -215,8 +215,8 @@ int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N, int32_t d,
                         void* out, void* stream);
 
-/* Debug-only: record a clock64 timeline of CTA (0,0,0) of the tcgen05
- * attention kernel into buf (device int64 [10 events][64 iterations]);
+/* Debug-only: record a clock64 timeline of CTA 0's first work item of the
+ * tcgen05 attention kernel into buf (device int64 [20 events][64 kv tiles]);
  * NULL disables (the default). */
 int dit_debug_attention_trace(void* buf);
 

@@ -208,3 +208,31 @@ def test_sequence_parallel_local_group(torch_cuda, P, hidden, heads):
     for m in models:
         m.close()
     D.load_library().dit_local_group_destroy(group)
+
+
+@pytest.mark.parametrize("B,H,N", [(3, 70, 333), (1, 3, 129), (2, 150, 1000)])
+def test_attention_kernel_vs_torch_fp32(torch_cuda, B, H, N):
+    """tcgen05 attention alone (d = 128) against a plain PyTorch fp32 reference: more work items
+    than SMs (persistent CTAs walk several), ragged query blocks and ragged KV tails."""
+    import ctypes as C
+    import torch
+    from paper_2604_08123_b200 import dit
+    lib = dit.load_library()
+    d = 128
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + H * 10 + N)
+    q, k, v = (torch.randn(B, H, N, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    out = torch.zeros(B * N, H * d, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream()
+    assert lib.dit_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, H, N, d, out.data_ptr(),
+                                   C.c_void_p(s.cuda_stream)) == 0
+    torch.cuda.synchronize()
+    qf, kf, vf = q.float(), k.float(), v.float()
+    p = torch.softmax((qf @ kf.transpose(-1, -2)) / d ** 0.5, dim=-1)
+    ref = (p @ vf).permute(0, 2, 1, 3).reshape(B * N, H * d)
+    got = out.float()
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    cos = torch.nn.functional.cosine_similarity(got.flatten(), ref.flatten(), dim=0).item()
+    # bf16 P and O (2^-9 relative rounding) bound the error; every row must be written
+    assert torch.isfinite(got).all()
+    assert err < 1e-2, err
+    assert cos > 0.9999, cos
