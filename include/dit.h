@@ -124,6 +124,29 @@ int lora_register(dit_ctx* ctx, int32_t adapter_id, int32_t rank, float scale,
  * Errors: DIT_ENOENT. */
 int lora_unregister(dit_ctx* ctx, int32_t adapter_id);
 
+/* ---------------------------------------------------- merged LoRA (hot patch) */
+/* Weight patching (adapters "patch the base model's weights
+ * before inference, incurring no additional computational overhead"; hot-patch
+ * at a step boundary once an asynchronously loaded adapter arrives,
+ * PAPER.md:391-400).  lora_merge writes W' = bf16(W + scale * B A) of EVERY
+ * adapted linear (same set as lora_register) for the registered adapter
+ * `adapter_id` into `merged` and makes the ctx run those linears from W';
+ * enqueued on `stream` (a cudaStream_t).  `merged`: caller-owned device memory,
+ * >= dit_merge_bytes(cfg), 256-byte aligned, layout = the adapted linears in
+ * pool order, each [out][in] bf16 at a 256-byte aligned offset; it must stay
+ * alive until lora_unmerge.  The base weights are never written, so
+ * lora_unmerge restores them exactly (a pointer switch).  While an adapter is
+ * merged the ctx is a patched replica specialised to it:
+ * every request of a dit_step must name that adapter (else DIT_EADAPTER) and
+ * no per-step LoRA work runs; it cannot be unregistered.
+ * Errors: DIT_ENOENT (not registered), DIT_EEXIST (an adapter is already
+ * merged), DIT_ENOMEM (buffer too small), DIT_EINVAL (NULL / misaligned),
+ * DIT_ENOWEIGHTS, DIT_ECUDA.  Validation precedes any enqueue. */
+size_t dit_merge_bytes(const dit_config* cfg);
+int lora_merge(dit_ctx* ctx, int32_t adapter_id, void* merged, size_t bytes, void* stream);
+/* Restore the base weights.  Errors: DIT_ENOENT (nothing merged). */
+int lora_unmerge(dit_ctx* ctx);
+
 /* -------------------------------------------------------------- ControlNet */
 /* Deferred input "controlnet_inputs": register the
  * residual of request `slot` of the NEXT dit_step for double block `block`:

@@ -42,7 +42,9 @@ struct Lin {
   const void* w = nullptr;
   const void* b = nullptr;
   int out = 0, in = 0;
-  CUtensorMap tm;  // weight [out][in], box {64, 256}
+  CUtensorMap tm;    // weight [out][in], box {64, 128}
+  CUtensorMap tm_m;  // merged (patched) copy W' = W + s B A while a lora_merge is active
+  bool has_m = false;
 };
 
 struct LoraPool {     // one adapted module
@@ -141,6 +143,7 @@ struct dit_ctx {
   std::map<int, int> adapter_slot;      // adapter id -> pool slot
   std::vector<float> slot_scale_h;
   std::vector<cudaEvent_t> slot_last_use;
+  int merged_adapter = -1;           // lora_merge: adapter patched into tm_m copies (-1: none)
   // ControlNet registrations for the next step
   struct CnReg { const void* ptr; float scale; cudaEvent_t ready; };
   std::map<std::pair<int, int>, CnReg> cn;   // (slot, block)
@@ -643,8 +646,105 @@ extern "C" int lora_unregister(dit_ctx* c, int32_t adapter_id) {
   if (!c) return DIT_EINVAL;
   auto it = c->adapter_slot.find(adapter_id);
   if (it == c->adapter_slot.end()) return c->fail(DIT_ENOENT, "adapter %d not registered", adapter_id);
+  if (adapter_id == c->merged_adapter) return c->fail(DIT_EINVAL, "adapter %d is merged; lora_unmerge first", adapter_id);
   cudaEventSynchronize(c->slot_last_use[it->second]);
   c->adapter_slot.erase(it);
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ merged LoRA (hot patch)
+namespace {
+// Adapted linears in LoRA-pool module order: double blocks (img then txt stream; qkv, proj,
+// fc1, fc2), then single blocks (linear1, linear2).  (out, in) from the config alone.
+void adapted_shapes(const dit_config& cfg, std::vector<std::pair<int, int>>& v) {
+  const int D = cfg.hidden, F = cfg.mlp_ratio * cfg.hidden;
+  v.clear();
+  for (int i = 0; i < cfg.depth_double; ++i)
+    for (int s = 0; s < 2; ++s) {
+      v.push_back({3 * D, D});
+      v.push_back({D, D});
+      v.push_back({F, D});
+      v.push_back({D, F});
+    }
+  for (int j = 0; j < cfg.depth_single; ++j) {
+    v.push_back({3 * D + F, D});
+    v.push_back({D, D + F});
+  }
+}
+std::vector<std::pair<Lin*, int>> adapted_lins(dit_ctx* c) {
+  std::vector<std::pair<Lin*, int>> v;
+  for (int i = 0; i < c->Ld; ++i)
+    for (int s = 0; s < 2; ++s) {
+      DoubleStream& X = c->dbl[s][i];
+      Lin* L[4] = {&X.qkv, &X.proj, &X.fc1, &X.fc2};
+      for (int q = 0; q < 4; ++q) v.push_back({L[q], X.lora[q]});
+    }
+  for (int j = 0; j < c->Ls; ++j) {
+    v.push_back({&c->sgl[j].l1, c->sgl[j].lora[0]});
+    v.push_back({&c->sgl[j].l2, c->sgl[j].lora[1]});
+  }
+  return v;
+}
+}  // namespace
+
+extern "C" size_t dit_merge_bytes(const dit_config* cfg) {
+  if (!cfg_valid(cfg, nullptr)) return 0;
+  std::vector<std::pair<int, int>> v;
+  adapted_shapes(*cfg, v);
+  size_t off = 0;
+  for (auto& oi : v) off = align_up(off + (size_t)oi.first * oi.second * 2, 256);
+  return off;
+}
+
+extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t bytes, void* stream) {
+  if (!c) return DIT_EINVAL;
+  auto it = c->adapter_slot.find(adapter_id);
+  if (it == c->adapter_slot.end()) return c->fail(DIT_ENOENT, "adapter %d not registered", adapter_id);
+  if (c->merged_adapter >= 0) return c->fail(DIT_EEXIST, "adapter %d is already merged", c->merged_adapter);
+  if (!c->weights_ready) return c->fail(DIT_ENOWEIGHTS, "base weights not (fully) loaded");
+  if (!merged || (reinterpret_cast<uintptr_t>(merged) & 255)) return c->fail(DIT_EINVAL, "merged buffer must be 256-byte aligned");
+  const size_t need = dit_merge_bytes(&c->cfg);
+  if (bytes < need) return c->fail(DIT_ENOMEM, "merged buffer %zu bytes < %zu", bytes, need);
+  const int slot = it->second;
+  const float scale = c->slot_scale_h[slot];
+  const int ra = c->r_alloc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto lins = adapted_lins(c);
+  // validate everything before enqueuing anything
+  std::vector<CUtensorMap> maps(lins.size());
+  size_t off = 0;
+  std::vector<size_t> offs(lins.size());
+  for (size_t k = 0; k < lins.size(); ++k) {
+    const Lin& L = *lins[k].first;
+    offs[k] = off;
+    if (!make_tmap_2d(&maps[k], static_cast<uint8_t*>(merged) + off, L.in, L.out, (uint64_t)L.in * 2, 64, 128))
+      return c->fail(DIT_EINVAL, "tensor map for the merged copy failed");
+    off = align_up(off + (size_t)L.out * L.in * 2, 256);
+  }
+  for (size_t k = 0; k < lins.size(); ++k) {
+    Lin& L = *lins[k].first;
+    const LoraPool& P = c->pools[lins[k].second];
+    cudaError_t e = lora_merge_launch(L.w, static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
+                                      static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2,
+                                      static_cast<uint8_t*>(merged) + offs[k], L.out, L.in, ra, scale, s);
+    if (e != cudaSuccess) return c->fail(DIT_ECUDA, "lora_merge kernel: %s", cudaGetErrorString(e));
+  }
+  for (size_t k = 0; k < lins.size(); ++k) {
+    lins[k].first->tm_m = maps[k];
+    lins[k].first->has_m = true;
+  }
+  cudaEventRecord(c->slot_last_use[slot], s);
+  c->merged_adapter = adapter_id;
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
+extern "C" int lora_unmerge(dit_ctx* c) {
+  if (!c) return DIT_EINVAL;
+  if (c->merged_adapter < 0) return c->fail(DIT_ENOENT, "no adapter is merged");
+  for (auto& lm : adapted_lins(c)) lm.first->has_m = false;   // base weights were never written: exact restore
+  c->merged_adapter = -1;
   c->plan_B = -1;
   return DIT_OK;
 }
@@ -803,7 +903,7 @@ GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const
   GemmProblem P;
   memset(&P, 0, sizeof(P));
   make_tmap_2d(&P.tmA, A, K, M, (uint64_t)lda * 2, 64, GEMM_BM);
-  P.tmB = W.tm;
+  P.tmB = (c->merged_adapter >= 0 && W.has_m) ? W.tm_m : W.tm;
   P.M = M;
   P.N = W.out;
   P.K = K;
@@ -921,7 +1021,7 @@ extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
   // LoRA: 2 r (in + out) per row per adapted linear, rows of adapted requests only
   for (int i = 0; i < b->batch; ++i) {
     int aid = b->adapter_id ? b->adapter_id[i] : -1;
-    if (aid < 0) continue;
+    if (aid < 0 || c->merged_adapter >= 0) continue;   // merged: the delta is inside the base GEMMs
     double r = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
     f += c->Ld * 2 * r * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
     f += c->Ls * 2 * r * N * ((D + 3 * D + F) + (D + F + D));
@@ -972,6 +1072,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   std::vector<int> req_slot(B, -1);
   for (int i = 0; i < B; ++i) {
     const int aid = b->adapter_id[i];
+    if (c->merged_adapter >= 0) {   // patched replica: specialised to its adapter
+      if (aid != c->merged_adapter)
+        return c->fail(DIT_EADAPTER, "adapter %d is merged; request %d uses %d", c->merged_adapter, i, aid);
+      continue;                     // its LoRA is in the weights: no per-step LoRA work
+    }
     if (aid < 0) continue;
     auto it = c->adapter_slot.find(aid);
     if (it == c->adapter_slot.end()) return c->fail(DIT_EADAPTER, "request %d uses unregistered adapter %d", i, aid);
@@ -1506,7 +1611,7 @@ int debug_prepare(dit_ctx* c, const dit_batch* b, std::vector<int>& req_slot, in
   req_slot.assign(b->batch, -1);
   for (int i = 0; i < b->batch; ++i) {
     const int aid = b->adapter_id ? b->adapter_id[i] : -1;
-    if (aid < 0) continue;
+    if (aid < 0 || c->merged_adapter >= 0) continue;
     auto it = c->adapter_slot.find(aid);
     if (it == c->adapter_slot.end()) return -DIT_EADAPTER;
     req_slot[i] = it->second;

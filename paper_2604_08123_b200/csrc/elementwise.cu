@@ -196,6 +196,117 @@ cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ merged LoRA
+// Weight patching: W' = bf16(W + s * B A) for one adapted linear.
+// A 128 x 128 output tile per CTA, 8 warps x 16 rows; the rank-r product runs on
+// mma.sync m16n8k16 (r <= 128: 8 K-steps at most) with the B rows (A operand) and the
+// A columns (B operand, ldmatrix .trans from its [k][n] storage) staged in shared memory.
+// Bandwidth-bound: 2 bytes read + 2 written per weight (+ the tiny factors).
+constexpr int LM_TILE = 128, LM_PAD = 8, LM_MAXR = 128;
+
+DEVI void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+DEVI void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+
+__global__ void __launch_bounds__(256) lora_merge_kernel(const bf16* __restrict__ W, const bf16* __restrict__ A,
+                                                         const bf16* __restrict__ Bm, bf16* __restrict__ out, int rows,
+                                                         int cols, int ra, float scale) {
+  extern __shared__ __align__(16) uint8_t lm_smem[];
+  bf16* sB = reinterpret_cast<bf16*>(lm_smem);                        // [128][ra + PAD]   (B rows of the tile)
+  bf16* sA = sB + LM_TILE * (ra + LM_PAD);                            // [ra][128 + PAD]   (A columns of the tile)
+  const int row0 = blockIdx.y * LM_TILE, col0 = blockIdx.x * LM_TILE;
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  const int ldb = ra + LM_PAD, lda = LM_TILE + LM_PAD;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int r0 = row0 + warp * 16 + gid;
+  // W pairs at this thread's accumulator positions, loaded first so the HBM latency overlaps
+  // the factor staging and the MMAs
+  uint32_t w2[16][2];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + h * 8, col = col0 + j * 8 + 2 * tig;
+      w2[j][h] = (r < rows && col + 1 < cols) ? __ldcs(reinterpret_cast<const unsigned int*>(W + (size_t)r * cols + col)) : 0u;
+    }
+  for (int i = t; i < LM_TILE * (ra / 8); i += blockDim.x) {   // 16-byte chunks of B rows
+    const int r = i / (ra / 8), k8 = (i - r * (ra / 8)) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row0 + r < rows) v = __ldg(reinterpret_cast<const uint4*>(Bm + (size_t)(row0 + r) * ra + k8));
+    *reinterpret_cast<uint4*>(sB + r * ldb + k8) = v;
+  }
+  for (int i = t; i < ra * (LM_TILE / 8); i += blockDim.x) {   // 16-byte chunks of A rows
+    const int k = i / (LM_TILE / 8), c8 = (i - k * (LM_TILE / 8)) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (col0 + c8 + 8 <= cols) {
+      v = __ldg(reinterpret_cast<const uint4*>(A + (size_t)k * cols + col0 + c8));
+    } else if (col0 + c8 < cols) {
+      bf16 e[8];
+      for (int q = 0; q < 8; ++q) e[q] = col0 + c8 + q < cols ? A[(size_t)k * cols + col0 + c8 + q] : __float2bfloat16_rn(0.f);
+      v = *reinterpret_cast<uint4*>(e);
+    }
+    *reinterpret_cast<uint4*>(sA + k * lda + c8) = v;
+  }
+  __syncthreads();
+  float acc[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  const uint32_t sB_base = smem_u32(sB), sA_base = smem_u32(sA);
+  for (int k0 = 0; k0 < ra; k0 += 16) {
+    uint32_t a[4];
+    ldsm_x4(sB_base + (uint32_t)(((warp * 16 + (lane & 15)) * ldb + k0 + (lane >> 4) * 8) * 2), a[0], a[1], a[2], a[3]);
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      uint32_t b[4];
+      // lanes 0-15: k rows k0..k0+15 of n-block j; lanes 16-31: the same rows of n-block j+1
+      ldsm_x4_t(sA_base + (uint32_t)(((k0 + (lane & 15)) * lda + j * 8 + (lane >> 4) * 8) * 2), b[0], b[1], b[2], b[3]);
+      const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+      mma_bf16_16816(acc[j], a, b0);
+      mma_bf16_16816(acc[j + 1], a, b1);
+    }
+  }
+  // C fragment: (row gid, cols 2 tig, 2 tig + 1) and (row gid + 8, same cols) of each n-block
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = col0 + j * 8 + 2 * tig;
+    if (col >= cols) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + h * 8;
+      if (r >= rows) continue;
+      const size_t off = (size_t)r * cols + col;
+      if (col + 1 < cols) {
+        __stcs(reinterpret_cast<unsigned int*>(out + off),
+               pack_bf16(bf16_lo(w2[j][h]) + scale * acc[j][2 * h], bf16_hi(w2[j][h]) + scale * acc[j][2 * h + 1]));
+      } else {
+        out[off] = __float2bfloat16_rn(__bfloat162float(W[off]) + scale * acc[j][2 * h]);
+      }
+    }
+  }
+}
+
+cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
+                              float scale, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || ra <= 0 || ra % 16 || ra > LM_MAXR || cols % 2) return cudaErrorInvalidValue;
+  const int smem = (LM_TILE * (ra + LM_PAD) + ra * (LM_TILE + LM_PAD)) * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(lora_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (LM_TILE * (LM_MAXR + LM_PAD) + LM_MAXR * (LM_TILE + LM_PAD)) * 2);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((cols + LM_TILE - 1) / LM_TILE, (rows + LM_TILE - 1) / LM_TILE);
+  lora_merge_kernel<<<grid, 256, smem, s>>>(static_cast<const bf16*>(W), static_cast<const bf16*>(A),
+                                            static_cast<const bf16*>(Bm), static_cast<bf16*>(out), rows, cols, ra, scale);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ skinny GEMM
 // One warp computes 16 output rows n (all 8 batch columns) over the full K.
 // Per 32-wide K chunk, thread (gid, tig) loads 16 B of W row gid and row gid+8

@@ -185,6 +185,11 @@ struct LnModParams {
 };
 cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s);
 
+// Merged LoRA (weight patching): out[o][i] = bf16(W[o][i] + scale * sum_k Bm[o][k] A[k][i]),
+// W / out bf16 [rows][cols], Bm bf16 [rows][ra], A bf16 [ra][cols], ra a multiple of 16 (<= 128).
+cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
+                              float scale, cudaStream_t s);
+
 // out[b][n] (+)= sum_k x[b][k] * W[n][k] + bias[n] for b < 8, with x bf16 [8][K]
 // (zero rows beyond B).  Segment table lets one launch cover many weights.
 struct SkinnySeg {

@@ -52,6 +52,9 @@ EXPORTS = {
     "lora_register": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.POINTER(dit_tensor), C.c_int,
                                 C.c_void_p]),
     "lora_unregister": (C.c_int, [C.c_void_p, C.c_int32]),
+    "dit_merge_bytes": (C.c_size_t, [C.POINTER(dit_config)]),
+    "lora_merge": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "lora_unmerge": (C.c_int, [C.c_void_p]),
     "controlnet_inject": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p]),
     "sp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
@@ -181,6 +184,25 @@ class DiT:
 
     def lora_unregister(self, adapter_id: int):
         _check(self.lib.lora_unregister(self.ctx, adapter_id), self.ctx)
+
+    def merge_bytes(self) -> int:
+        return int(self.lib.dit_merge_bytes(C.byref(self.c_cfg)))
+
+    def lora_merge(self, adapter_id: int, merged=None, stream=None):
+        """Patch `adapter_id` into a copy of the adapted weights (caller-owned `merged`, a uint8
+        device tensor of >= merge_bytes(); allocated here if None and kept until lora_unmerge)."""
+        import torch
+        if merged is None:
+            merged = torch.empty(self.merge_bytes() + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        ptr = merged.data_ptr()
+        pad = (-ptr) % 256
+        self._merged = merged
+        _check(self.lib.lora_merge(self.ctx, adapter_id, C.c_void_p(ptr + pad), merged.numel() - pad,
+                                   self._stream(stream)), self.ctx)
+
+    def lora_unmerge(self):
+        _check(self.lib.lora_unmerge(self.ctx), self.ctx)
+        self._merged = None
 
     def controlnet_inject(self, slot: int, block: int, residual, scale: float = 1.0, ready_event=None):
         self._keep.append(residual)

@@ -1,0 +1,109 @@
+"""Merged-LoRA (weight patching) mode: lora_merge / lora_unmerge.
+
+PAPER.md:335-345 (adapters patch the base weights, no per-step overhead), :391-400 (hot-patch
+at a step boundary).  The merged copy W' = bf16(W + s B A) is checked against numpy, a merged
+step against the fp64 oracle (whose unmerged LoRA equals the merged form, pin P2), and
+lora_unmerge against the pre-merge step bit for bit."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import flux_step as O
+from oracle.flux_step import bf16_to_f64
+from tests.helpers import oracle_adapter
+from tests.test_gpu_parity import _model, check, torch_cuda  # noqa: F401 (fixture)
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16_rne(x64: np.ndarray) -> np.ndarray:
+    b = np.asarray(x64, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def _merged_modules(m, cfg):
+    """The merged buffer of the model, split per adapted linear (pool order, 256-byte aligned)."""
+    buf = m._merged
+    pad = (-buf.data_ptr()) % 256
+    raw = buf.cpu().numpy()[pad:]
+    W = synth.make_weights_bf16(cfg)
+    out, off = {}, 0
+    for mod, _, _ in synth.lora_targets(cfg):
+        o, i = W[mod + ".w"].shape
+        out[mod] = raw[off:off + o * i * 2].view(np.uint16).reshape(o, i)
+        off = (off + o * i * 2 + 255) // 256 * 256
+    return out
+
+
+def test_merged_weights_match_numpy(torch_cuda):
+    cfg = synth.TINY_SINGLE
+    rank, scale = 8, 0.75
+    m = _model(cfg, 2, 16, 8, rank=rank, adapters=2)
+    m.register_synthetic_lora(5, rank=rank, index=1, scale=scale)
+    m.lora_merge(5)
+    torch_cuda.cuda.synchronize()
+    got = _merged_modules(m, cfg)
+    W = synth.make_weights_bf16(cfg)
+    L = synth.make_lora_bf16(cfg, rank, 1)
+    for mod, _, _ in synth.lora_targets(cfg):
+        ref = bf16_to_f64(W[mod + ".w"]) + scale * bf16_to_f64(L[mod + ".lora_B"]) @ bf16_to_f64(L[mod + ".lora_A"])
+        want = _bf16_rne(ref)
+        g = got[mod]
+        # same value up to one bf16 ulp (fp32 accumulation order), and almost always exact
+        ulp = np.abs(g.astype(np.int64) - want.astype(np.int64))
+        assert ulp.max() <= 1, (mod, int(ulp.max()))
+        assert (ulp == 0).mean() > 0.99, (mod, float((ulp == 0).mean()))
+
+
+@pytest.mark.parametrize("cfg_name", ["TINY", "TINY_SINGLE"])
+def test_merged_step_parity_and_exact_restore(torch_cuda, cfg_name):
+    cfg = getattr(synth, cfg_name)
+    rank = 8
+    m = _model(cfg, 2, 16, 8, rank=rank, adapters=2)
+    m.register_synthetic_lora(3, rank=rank, index=0)
+    batch = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=1)
+    batch.adapter_id = np.array([3, 3], dtype=np.int32)
+    lat_u, v_u = m.step(batch)                       # unmerged (segmented LoRA)
+    base = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=1)
+    base.adapter_id = np.array([-1, -1], dtype=np.int32)
+    lat_b, v_b = m.step(base)                        # bare base model
+    m.lora_merge(3)
+    lat_m, v_m = m.step(batch)                       # patched replica
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = O.dit_step(cfg, W, batch, {3: oracle_adapter(cfg, rank, 0)[0]})
+    check(v_m, v_o, "v merged")
+    check(lat_m, x_o, "latents merged")
+    # the merged and segmented forms agree to rounding (not bitwise: W' is rounded to bf16)
+    assert np.abs(v_m - v_u).max() / np.abs(v_u).max() < 2e-2
+    with pytest.raises(Exception):
+        m.step(base)                                 # a patched replica only serves its adapter
+    m.lora_unmerge()
+    lat_u2, v_u2 = m.step(batch)
+    lat_b2, v_b2 = m.step(base)
+    np.testing.assert_array_equal(v_u2, v_u)         # restore is exact
+    np.testing.assert_array_equal(lat_b2, lat_b)
+    np.testing.assert_array_equal(v_b2, v_b)
+
+
+def test_merge_error_paths(torch_cuda):
+    import torch
+    from paper_2604_08123_b200.dit import DitError
+    cfg = synth.TINY_SINGLE
+    m = _model(cfg, 2, 16, 8, rank=8, adapters=2)
+    m.register_synthetic_lora(1, rank=8, index=0)
+    m.register_synthetic_lora(2, rank=4, index=1)
+    codes = lambda f: (lambda e: e.code)(pytest.raises(DitError, f).value)
+    assert codes(lambda: m.lora_merge(9)) == 7                       # DIT_ENOENT
+    small = torch.empty(1024, dtype=torch.uint8, device="cuda")
+    assert codes(lambda: m.lora_merge(1, merged=small)) == 2         # DIT_ENOMEM
+    assert codes(lambda: m.lora_unmerge()) == 7                      # nothing merged
+    m.lora_merge(1)
+    assert codes(lambda: m.lora_merge(2)) == 4                       # DIT_EEXIST
+    assert codes(lambda: m.lora_unregister(1)) == 1                  # merged adapter is pinned
+    batch = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=2)
+    batch.adapter_id = np.array([1, 2], dtype=np.int32)
+    assert codes(lambda: m.step(batch)) == 10                        # DIT_EADAPTER
+    m.lora_unmerge()
+    m.lora_unregister(1)
