@@ -149,8 +149,13 @@ int lora_unmerge(dit_ctx* ctx);
 
 /* -------------------------------------------------------------- ControlNet */
 /* Deferred input "controlnet_inputs": register the
- * residual of request `slot` of the NEXT dit_step for double block `block`:
- * after that block, h_img[slot] += cn_scale[slot] * scale * residual.
+ * residual of request `slot` of the NEXT dit_step for block `block`:
+ * block in [0, L_d) = double block `block`, [L_d, L_d + L_s) = single block
+ * `block - L_d` (ControlNets feed "specific layers"; reading
+ * C20).  After that block, h_img[slot] += cn_scale[slot] * scale * residual (for
+ * a single block: the image rows of the joint sequence).  Up to CN_FANIN = 2
+ * residuals may be registered per (slot, block) -- several ControlNets feeding
+ * one block (fan-in); they are summed.
  * residual: device bf16 [Ni_local][D] row-major (this rank's image shard).
  * ready: a cudaEvent_t recorded by the producer, or NULL if already
  * resident.  The step does NOT wait at launch: the wait is enqueued right
@@ -158,7 +163,8 @@ int lora_unmerge(dit_ctx* ctx);
  * available, or blocks until the data arrives").
  * BORROWED and immutable until that dit_step completes.
  * Registrations apply to exactly one dit_step and are then cleared.
- * Errors: DIT_EINVAL (slot >= B_max, block >= L_d, NULL residual). */
+ * Errors: DIT_EINVAL (slot >= B_max, block >= L_d + L_s, NULL or misaligned
+ * residual), DIT_ENOSPC (fan-in limit reached for this slot and block). */
 int controlnet_inject(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
                       float scale, void* ready_event);
 

@@ -239,34 +239,73 @@ def conditioning_vec(W, sigma: float, guidance: float, pooled: np.ndarray,
     return vec + mlp("vector_in", pooled)
 
 
+@dataclasses.dataclass
+class ControlNetInput:
+    """One ControlNet's outputs for one request ("consumed by specific layers").
+
+    double: residual index -> R [Ni, D], consumed after double block i at index
+    floor(i / ceil(L_d / n_res)) (reading C11); single: the same for the single blocks,
+    floor(j / ceil(L_s / n_res_single)), added to the image rows of the joint sequence
+    (reading C20); scale: this ControlNet's conditioning scale.  Several ControlNets feeding
+    one block are summed (fan-in; reading C20)."""
+    double: Dict[int, np.ndarray]
+    single: Dict[int, np.ndarray]
+    n_res: int
+    n_res_single: int
+    scale: float = 1.0
+
+
+def _cn_sum(cns, which: str, blk: int, depth: int) -> Optional[np.ndarray]:
+    """sum_c scale_c * R_c[floor(blk / interval_c)] over the ControlNets that feed block blk."""
+    tot = None
+    for cn in cns:
+        n = cn.n_res if which == "double" else cn.n_res_single
+        res = cn.double if which == "double" else cn.single
+        if not n or not res:
+            continue
+        r = res.get(blk // math.ceil(depth / n))
+        if r is not None:
+            tot = cn.scale * r if tot is None else tot + cn.scale * r
+    return tot
+
+
 def velocity(cfg, W, x: np.ndarray, txt: np.ndarray, pooled: np.ndarray, sigma: float,
              guidance: float, img_h: int, img_w: int,
              adapter: Optional[OracleLoRA] = None,
              residuals: Optional[Dict[int, np.ndarray]] = None, cn_scale: float = 1.0,
-             n_res: int = 0, trace: Optional[list] = None) -> np.ndarray:
+             n_res: int = 0, trace: Optional[list] = None,
+             controlnets: Optional[list] = None) -> np.ndarray:
     """noise_pred = transformer(latents, prompt_embeds, controlnet_inputs) (P:846-850).
 
     x [Ni, C] fp64, txt [Nt, Ct], pooled [Cp].  residuals: double block index ->
     R [Ni, D] (deferred ControlNet input; consumed after double block i,
-    index floor(i / interval), interval = ceil(L_d / n_res): reading C11).
+    index floor(i / interval), interval = ceil(L_d / n_res): reading C11) -- a
+    ControlNet of scale 1 with double-block outputs only.  controlnets: further
+    ControlNetInput objects (single-block outputs, fan-in; reading C20).  Every
+    ControlNet contribution is multiplied by the request's cn_scale.
     """
+    cns = list(controlnets or [])
+    if residuals is not None and n_res:
+        cns.insert(0, ControlNetInput(double=residuals, single={}, n_res=n_res, n_res_single=0))
     H = cfg.heads
     vec = conditioning_vec(W, sigma, guidance, pooled, cfg.guidance_embed)
     img = linear(x, W["img_in.w"], W["img_in.b"])
     tx = linear(txt, W["txt_in.w"], W["txt_in.b"])
     cos, sin = rope_cos_sin(position_ids(txt.shape[0], img_h, img_w), cfg.rope_axes, cfg.rope_theta)
-    interval = math.ceil(cfg.depth_double / n_res) if n_res else 0
     for i in range(cfg.depth_double):
         img, tx = double_block(W, i, H, img, tx, vec, cos, sin, adapter)
-        if residuals is not None and n_res:
-            r = residuals.get(i // interval)
-            if r is not None:
-                img = img + cn_scale * r
+        r = _cn_sum(cns, "double", i, cfg.depth_double)
+        if r is not None:
+            img = img + cn_scale * r
         if trace is not None:
             trace.append(np.concatenate([tx, img]))
     h = np.concatenate([tx, img])
+    nt = txt.shape[0]
     for j in range(cfg.depth_single):
         h = single_block(W, j, H, h, vec, cos, sin, adapter)
+        r = _cn_sum(cns, "single", j, cfg.depth_single)
+        if r is not None:   # image rows of the joint sequence (reading C20)
+            h = np.concatenate([h[:nt], h[nt:] + cn_scale * r])
         if trace is not None:
             trace.append(h)
     img = h[txt.shape[0]:]
@@ -281,11 +320,12 @@ def euler(x: np.ndarray, v: np.ndarray, sigma: float, sigma_next: float) -> np.n
 
 def dit_step(cfg, W, batch, adapters: Optional[Mapping[int, OracleLoRA]] = None,
              controlnet: Optional[Mapping[int, Dict[int, np.ndarray]]] = None,
-             n_res: int = 0, requests=None):
+             n_res: int = 0, requests=None, controlnets: Optional[Mapping[int, list]] = None):
     """One dit_step over a cross-workflow batch, evaluated request by request.
 
     batch: synth.Batch (bf16 bits for txt/pooled, fp32 latents).
-    adapters: adapter_id -> OracleLoRA.  controlnet: request b -> {res index: R fp64}.
+    adapters: adapter_id -> OracleLoRA.  controlnet: request b -> {res index: R fp64}
+    (double blocks, one ControlNet).  controlnets: request b -> [ControlNetInput, ...].
     Returns (latents_out [B, Ni, C], v [B, Ni, C]) fp64.
     """
     B = batch.batch
@@ -298,7 +338,7 @@ def dit_step(cfg, W, batch, adapters: Optional[Mapping[int, OracleLoRA]] = None,
         v = velocity(cfg, W, x, bf16_to_f64(batch.txt[b]), bf16_to_f64(batch.pooled[b]),
                      float(batch.sigma[b]), float(batch.guidance[b]), batch.img_h, batch.img_w,
                      adapter=ad, residuals=(controlnet or {}).get(b), cn_scale=float(batch.cn_scale[b]),
-                     n_res=n_res)
+                     n_res=n_res, controlnets=(controlnets or {}).get(b))
         vs.append(v)
         xs.append(euler(x, v, batch.sigma[b], batch.sigma_next[b]))
     return np.stack(xs), np.stack(vs)

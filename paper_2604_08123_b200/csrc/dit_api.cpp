@@ -146,7 +146,7 @@ struct dit_ctx {
   int merged_adapter = -1;           // lora_merge: adapter patched into tm_m copies (-1: none)
   // ControlNet registrations for the next step
   struct CnReg { const void* ptr; float scale; cudaEvent_t ready; };
-  std::map<std::pair<int, int>, CnReg> cn;   // (slot, block)
+  std::map<std::pair<int, int>, std::vector<CnReg>> cn;   // (slot, block) -> up to CN_FANIN residuals
   // SP
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -175,9 +175,9 @@ struct dit_ctx {
   float* p_cn_scale = nullptr;
   float* p_sigma = nullptr;
   float* p_guid = nullptr;
-  const void** p_cn_ptr = nullptr;   // [Ld][B_max]
+  const void** p_cn_ptr = nullptr;   // [Ld + Ls][CN_FANIN][8]
   float* p_slot_scale = nullptr;     // [max_adapters]
-  float* p_cn_kappa = nullptr;       // [Ld][8] cn_scale_b * inject scale
+  float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][8] cn_scale_b * inject scale
   RowSpace rs[3];                    // 0 txt stream, 1 img stream, 2 joint
   int slot_cap = 1;
   // plan cache key
@@ -273,7 +273,7 @@ Layout layout_of(const dit_config& c) {
   L.xprep = cv.take(8 * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
   L.temb = cv.take(8 * 256 * 2);
   L.segs = cv.take((nseg + 6) * sizeof(SkinnySeg));
-  L.params = cv.take(4096 + (size_t)std::max(c.depth_double, 1) * 8 * (sizeof(void*) + 4) + 2048);
+  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8 * (sizeof(void*) + 4) + 2048);
   L.rowspace = cv.take(3 * (R * 4 + tiles * 8 * 4 + tiles * 4 + tiles * 8 * 8) + 3 * 1024);
   size_t per_slot = 0;
   if (c.max_adapters > 0 && r_alloc > 0) {
@@ -353,8 +353,9 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     c->p_sigma = reinterpret_cast<float*>(p + cv.take(8 * 4));
     c->p_guid = reinterpret_cast<float*>(p + cv.take(8 * 4));
     c->p_slot_scale = reinterpret_cast<float*>(p + cv.take(64 * 4));
-    c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take((size_t)std::max(c->Ld, 1) * 8 * sizeof(void*)));
-    c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take((size_t)std::max(c->Ld, 1) * 8 * 4));
+    const size_t ncn = (size_t)std::max(c->Ld + c->Ls, 1) * CN_FANIN * 8;
+    c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take(ncn * sizeof(void*)));
+    c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take(ncn * 4));
   }
   {
     const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
@@ -754,11 +755,15 @@ extern "C" int controlnet_inject(dit_ctx* c, int32_t slot, int32_t block, const 
                                  void* ready) {
   if (!c) return DIT_EINVAL;
   if (slot < 0 || slot >= c->cfg.max_batch) return c->fail(DIT_EINVAL, "slot %d not in [0, %d)", slot, c->cfg.max_batch);
-  if (block < 0 || block >= c->Ld) return c->fail(DIT_EINVAL, "block %d not in [0, %d)", block, c->Ld);
+  if (block < 0 || block >= c->Ld + c->Ls)
+    return c->fail(DIT_EINVAL, "block %d not in [0, %d) (double blocks, then single blocks)", block, c->Ld + c->Ls);
   if (!residual || (reinterpret_cast<uintptr_t>(residual) & 15))
     return c->fail(DIT_EINVAL, "residual must be a non-NULL 16-byte aligned device pointer");
   if (!std::isfinite(scale)) return c->fail(DIT_EINVAL, "scale must be finite");
-  c->cn[{slot, block}] = {residual, scale, reinterpret_cast<cudaEvent_t>(ready)};
+  auto& lst = c->cn[{slot, block}];
+  if ((int)lst.size() >= CN_FANIN)
+    return c->fail(DIT_ENOSPC, "request %d block %d already has %d ControlNet residuals (fan-in limit)", slot, block, CN_FANIN);
+  lst.push_back({residual, scale, reinterpret_cast<cudaEvent_t>(ready)});
   return DIT_OK;
 }
 
@@ -1142,14 +1147,17 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     std::vector<float> ss(64, 0.f);
     for (size_t i = 0; i < c->slot_scale_h.size() && i < 64; ++i) ss[i] = c->slot_scale_h[i];
     cudaMemcpyAsync(c->p_slot_scale, ss.data(), 64 * 4, cudaMemcpyHostToDevice, s);
-    if (c->Ld > 0) {
-      std::vector<const void*> cp((size_t)c->Ld * 8, nullptr);
-      std::vector<float> kap((size_t)c->Ld * 8, 0.f);
-      for (auto& kv : c->cn) {
-        cp[(size_t)kv.first.second * 8 + kv.first.first] = kv.second.ptr;
-        kap[(size_t)kv.first.second * 8 + kv.first.first] =
-            kv.second.scale * (b->cn_scale ? b->cn_scale[kv.first.first] : 1.f);
-      }
+    if (!c->cn.empty()) {
+      // [block][fan-in k][request] tables of the residuals registered for this step
+      const size_t ncn = (size_t)(c->Ld + c->Ls) * CN_FANIN * 8;
+      std::vector<const void*> cp(ncn, nullptr);
+      std::vector<float> kap(ncn, 0.f);
+      for (auto& kv : c->cn)
+        for (size_t k = 0; k < kv.second.size(); ++k) {
+          const size_t at = ((size_t)kv.first.second * CN_FANIN + k) * 8 + kv.first.first;
+          cp[at] = kv.second[k].ptr;
+          kap[at] = kv.second[k].scale * (b->cn_scale ? b->cn_scale[kv.first.first] : 1.f);
+        }
       cudaMemcpyAsync(c->p_cn_ptr, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(c->p_cn_kappa, kap.data(), kap.size() * 4, cudaMemcpyHostToDevice, s);
     }
@@ -1316,6 +1324,19 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     return run_shrink(c, 2, A, M, Ks, ld, R, mods, base, s);
   };
 
+  // deferred ControlNet inputs of block `blk` (double blocks 0..Ld-1, then single blocks):
+  // wait on their producers' ready events right before the consuming GEMM
+  auto cn_wait = [&](int blk) -> bool {
+    bool any = false;
+    for (auto& kv : c->cn)
+      if (kv.first.second == blk)
+        for (auto& r : kv.second) {
+          any = true;
+          if (r.ready) cudaStreamWaitEvent(s, r.ready, 0);
+        }
+    return any;
+  };
+
   // ---- double-stream blocks
   for (int i = 0; i < c->Ld; ++i) {
     const DoubleStream& I = c->dbl[0][i];
@@ -1382,7 +1403,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       eI.gate_off = mI + goff;
       if (cn_ptr) {
         eI.cn_ptr = cn_ptr;
-        eI.cn_scale = c->p_cn_kappa + (size_t)i * 8;
+        eI.cn_scale = c->p_cn_kappa + (size_t)i * CN_FANIN * 8;
+        eI.cn_row0 = 0;   // the img-stream problem's rows are exactly the residual's rows
       }
       GemmProblem p[2] = {base_problem(c, AT, Mt, K, lda, LT, eT), base_problem(c, AI, Mi, K, lda, LI, eI)};
       if (any_lora) {
@@ -1421,15 +1443,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       CK(run_gemm(c, p, 2, s));
     }
     // deferred ControlNet input of block i: wait right before its consumer
-    bool has_cn = false;
-    for (auto& kv : c->cn)
-      if (kv.first.second == i) {
-        has_cn = true;
-        if (kv.second.ready) cudaStreamWaitEvent(s, kv.second.ready, 0);
-      }
+    const bool has_cn = cn_wait(i);
     CK(shrink2(aT, aI, F, F, T.lora[3], I.lora[3]));
     CK(resid_pair(T.fc2, I.fc2, aT, aI, F, F, 5 * D, T.lora[3], I.lora[3],
-                  has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * 8) : nullptr));
+                  has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * CN_FANIN * 8) : nullptr));
   }
 
   // ---- single-stream blocks on the joint sequence
@@ -1510,6 +1527,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.mod = c->mod;
       e.mod_stride = c->mod_total;
       e.gate_off = mj + 2 * D;
+      if (cn_wait(c->Ld + j)) {   // single-block ControlNet residual on the image rows (reading C20)
+        e.cn_ptr = (const void* const*)(c->p_cn_ptr + (size_t)(c->Ld + j) * CN_FANIN * 8);
+        e.cn_scale = c->p_cn_kappa + (size_t)(c->Ld + j) * CN_FANIN * 8;
+        e.cn_row0 = nt;           // joint rows are [txt; img] per request
+      }
       GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
       if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1], sext_of(c, 0));
       c->gemm_label = 16;

@@ -347,14 +347,16 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
     } else if (E.kind == EPI_RESID) {
       float* hp = E.h + (size_t)jrow * E.D + col;
       const float* gp = E.mod + (size_t)b * E.mod_stride + E.gate_off + col;
-      const bf16* cn = nullptr;
-      float kap = 0.f;
-      if (E.cn_ptr != nullptr) {
-        cn = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
-        if (cn != nullptr) {
-          kap = E.cn_scale[b];
-          cn += (size_t)nloc * E.D + col;
-        }
+      // ControlNet fan-in: up to CN_FANIN residuals per (request, block), rows from cn_row0
+      const bf16* cn0 = nullptr;
+      const bf16* cn1 = nullptr;
+      float kap0 = 0.f, kap1 = 0.f;
+      if (E.cn_ptr != nullptr && nloc >= E.cn_row0) {
+        const size_t roff = (size_t)(nloc - E.cn_row0) * E.D + col;
+        cn0 = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
+        cn1 = reinterpret_cast<const bf16*>(E.cn_ptr[8 + b]);
+        if (cn0 != nullptr) { kap0 = E.cn_scale[b]; cn0 += roff; }
+        if (cn1 != nullptr) { kap1 = E.cn_scale[8 + b]; cn1 += roff; }
       }
       if (valid == 32) {
         float4 h4[8];
@@ -367,12 +369,19 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           h4[q].y += g4.y * y[4 * q + 1];
           h4[q].z += g4.z * y[4 * q + 2];
           h4[q].w += g4.w * y[4 * q + 3];
-          if (cn != nullptr) {
-            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
-            h4[q].x += kap * bf16_lo(c2.x);
-            h4[q].y += kap * bf16_hi(c2.x);
-            h4[q].z += kap * bf16_lo(c2.y);
-            h4[q].w += kap * bf16_hi(c2.y);
+          if (cn0 != nullptr) {
+            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn0) + q);
+            h4[q].x += kap0 * bf16_lo(c2.x);
+            h4[q].y += kap0 * bf16_hi(c2.x);
+            h4[q].z += kap0 * bf16_lo(c2.y);
+            h4[q].w += kap0 * bf16_hi(c2.y);
+          }
+          if (cn1 != nullptr) {
+            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn1) + q);
+            h4[q].x += kap1 * bf16_lo(c2.x);
+            h4[q].y += kap1 * bf16_hi(c2.x);
+            h4[q].z += kap1 * bf16_lo(c2.y);
+            h4[q].w += kap1 * bf16_hi(c2.y);
           }
           reinterpret_cast<float4*>(hp)[q] = h4[q];
         }
@@ -381,7 +390,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         for (int e = 0; e < 32; ++e) {   // static indices keep y in registers
           if (e < valid) {
             float hv = hp[e] + gp[e] * y[e];
-            if (cn != nullptr) hv += kap * __bfloat162float(cn[e]);
+            if (cn0 != nullptr) hv += kap0 * __bfloat162float(cn0[e]);
+            if (cn1 != nullptr) hv += kap1 * __bfloat162float(cn1[e]);
             hp[e] = hv;
           }
         }
@@ -416,12 +426,15 @@ DEVI void prefetch_epilogue_rows(const GemmProblem& P, const TileInfo& ti, int r
   const float* hp = E.h + (size_t)jrow * E.D + col;
 #pragma unroll
   for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(hp + q * 32));
-  if (E.cn_ptr != nullptr) {
-    const bf16* cn = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
-    if (cn != nullptr) {
-      cn += (size_t)nloc * E.D + col;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(cn));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(cn + 64));
+  if (E.cn_ptr != nullptr && nloc >= E.cn_row0) {
+#pragma unroll
+    for (int k = 0; k < CN_FANIN; ++k) {
+      const bf16* cn = reinterpret_cast<const bf16*>(E.cn_ptr[8 * k + b]);
+      if (cn != nullptr) {
+        cn += (size_t)(nloc - E.cn_row0) * E.D + col;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(cn));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(cn + 64));
+      }
     }
   }
 }

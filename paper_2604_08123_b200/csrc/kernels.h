@@ -13,6 +13,7 @@ constexpr int GEMM_TM = 256;      // rows per 2-SM (CTA pair) tile
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_MAX_PROBLEMS = 2;
+constexpr int CN_FANIN = 2;   // ControlNet residuals summed per (request, block) (multi-ControlNet fan-in)
 #ifndef GEMM_GROUP_M_DEF
 #define GEMM_GROUP_M_DEF 16
 #endif
@@ -41,8 +42,9 @@ struct EpiParams {
   int mod_stride;
   int gate_off;              // column offset of the gate vector inside mod rows
   // ControlNet residual (EPI_RESID img stream)
-  const void* const* cn_ptr; // device [B] residual pointers (nullptr = none), bf16 [rows_per_req][D]
-  const float* cn_scale;     // device [B]
+  const void* const* cn_ptr; // device [CN_FANIN][8] residual pointers (nullptr = none), bf16 [rows][D]
+  const float* cn_scale;     // device [CN_FANIN][8] kappa_b * inject scale
+  int cn_row0;               // request-local row of residual row 0 (0: img-stream GEMM; Nt_loc: joint rows)
   // bf16 outputs
   void* out;
   int ld_out;

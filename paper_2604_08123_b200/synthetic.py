@@ -56,11 +56,14 @@ class SyntheticDiT(DiT):
         v = torch.empty_like(lat)
         return lat, txt, pooled, out, v
 
-    def step(self, batch, controlnet: Optional[Dict[int, Dict[int, np.ndarray]]] = None, n_res: int = 0):
+    def step(self, batch, controlnet: Optional[Dict[int, Dict[int, np.ndarray]]] = None, n_res: int = 0,
+             injections=None):
         """Run one dit_step on a synth.Batch; returns (latents_out, v) as numpy fp32.
 
         controlnet: request b -> {double block i -> residual bf16 bits [Ni, D]} (one
         residual per block; n_res mapping is the caller's business).
+        injections: further (request b, block, residual bits [Ni, D], scale) tuples; block
+        counts double blocks then single blocks (controlnet_inject's numbering).
         """
         import torch
         lat, txt, pooled, out, v = self.device_inputs(batch)
@@ -68,6 +71,8 @@ class SyntheticDiT(DiT):
             for b, d in controlnet.items():
                 for blk, bits in d.items():
                     self.controlnet_inject(b, blk, _bits_to_bf16_tensor(bits, self.dev), 1.0)
+        for b, blk, bits, sc in (injections or []):
+            self.controlnet_inject(b, blk, _bits_to_bf16_tensor(bits, self.dev), sc)
         cb = self.make_batch(batch.batch, batch.img_h, batch.img_w, batch.txt_tokens, batch.adapter_id,
                              batch.sigma, batch.sigma_next, batch.guidance, lat, out, txt, pooled, v_out=v,
                              cn_scale=batch.cn_scale)

@@ -236,3 +236,51 @@ def test_attention_kernel_vs_torch_fp32(torch_cuda, B, H, N):
     assert torch.isfinite(got).all()
     assert err < 1e-2, err
     assert cos > 0.9999, cos
+
+
+def test_single_block_controlnet_and_fan_in(torch_cuda):
+    """SURVEY.md §8(f) f4 (reading C20): ControlNet residuals on single blocks (image rows of the
+    joint sequence) and two ControlNets feeding the same blocks (summed), vs the oracle."""
+    from oracle.flux_step import ControlNetInput
+    cfg = synth.TINY_SINGLE
+    m = _model(cfg, 2, 16, 8)
+    batch = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=0)
+    batch.adapter_id = np.array([-1, -1], dtype=np.int32)
+    batch.cn_scale = np.array([0.9, 1.3], dtype=np.float32)
+    ni, D, Ld = batch.img_tokens, cfg.hidden, cfg.depth_double
+    bits = lambda b, i: synth.controlnet_residual_bf16(b, i, ni, D)
+    f64 = lambda x: O.bf16_to_f64(x)
+    inj, cns = [], {}
+    for b in range(2):
+        # ControlNet A: double block 0 and single blocks 0, 1; ControlNet B: double 0 and single 1
+        A = ControlNetInput(double={0: f64(bits(b, 0))}, single={0: f64(bits(b, 1)), 1: f64(bits(b, 2))},
+                            n_res=1, n_res_single=2, scale=0.6)
+        Bc = ControlNetInput(double={0: f64(bits(b, 3))}, single={1: f64(bits(b, 4))},
+                             n_res=1, n_res_single=2, scale=-0.5)
+        cns[b] = [A, Bc]
+        inj += [(b, 0, bits(b, 0), 0.6), (b, Ld + 0, bits(b, 1), 0.6), (b, Ld + 1, bits(b, 2), 0.6),
+                (b, 0, bits(b, 3), -0.5), (b, Ld + 1, bits(b, 4), -0.5)]
+    lat, v = m.step(batch, injections=inj)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = O.dit_step(cfg, W, batch, controlnets=cns)
+    check(v, v_o, "v")
+    check(lat, x_o, "latents")
+    _, v0 = O.dit_step(cfg, W, batch)
+    assert max_rel(v_o, v0) > 1e-2                 # the residuals matter at this scale
+
+
+def test_controlnet_inject_limits(torch_cuda):
+    import torch
+    from paper_2604_08123_b200.dit import DitError
+    cfg = synth.TINY_SINGLE
+    m = _model(cfg, 2, 16, 8)
+    r = torch.zeros(16, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+    blocks = cfg.depth_double + cfg.depth_single
+    m.controlnet_inject(0, blocks - 1, r)                      # last single block: accepted
+    m.controlnet_inject(0, blocks - 1, r)                      # second ControlNet (fan-in 2)
+    with pytest.raises(DitError) as e:
+        m.controlnet_inject(0, blocks - 1, r)                  # a third: DIT_ENOSPC
+    assert e.value.code == 6
+    with pytest.raises(DitError) as e:
+        m.controlnet_inject(0, blocks, r)                      # past the last block: DIT_EINVAL
+    assert e.value.code == 1

@@ -331,3 +331,62 @@ def test_recipe_not_chaotic_full_depth_reduced_tokens():
                O.bf16_to_f64(batch.pooled[0]), float(batch.sigma[0]), 3.5, 4, 4, trace=trace)
     rms = [float(np.sqrt((h ** 2).mean())) for h in trace]
     assert 0.3 < min(rms) and max(rms) < 30, rms
+
+
+# ---------------------------------------------------------------- P13 single-block ControlNet, fan-in
+def _trace_velocity(cfg, W, batch, b, controlnets=None, cn_scale=1.0):
+    from oracle.flux_step import bf16_to_f64
+    tr = []
+    v = O.velocity(cfg, W, batch.latents[b].astype(np.float64), bf16_to_f64(batch.txt[b]),
+                   bf16_to_f64(batch.pooled[b]), float(batch.sigma[b]), float(batch.guidance[b]),
+                   batch.img_h, batch.img_w, trace=tr, controlnets=controlnets, cn_scale=cn_scale)
+    return v, tr
+
+
+def test_p13_single_block_controlnet_injection_point(W_bits):
+    """Reading C20: a single-block residual lands on the IMAGE rows of the joint sequence right
+    after its block -- txt rows and every earlier block untouched, the later blocks see it."""
+    cfg = CFG_S
+    W = _W(W_bits, cfg)
+    batch = _batch(cfg)
+    nt, ni, D = batch.txt_tokens, batch.img_tokens, cfg.hidden
+    R = RNG.standard_normal((ni, D)) * 0.1
+    cn = O.ControlNetInput(double={}, single={1: R}, n_res=0, n_res_single=2, scale=0.5)
+    v0, tr0 = _trace_velocity(cfg, W, batch, 0)
+    v1, tr1 = _trace_velocity(cfg, W, batch, 0, [cn], cn_scale=0.8)
+    Ld = cfg.depth_double
+    for k in range(Ld + 1):                       # double blocks and single block 0: identical
+        np.testing.assert_array_equal(tr1[k], tr0[k])
+    diff = tr1[Ld + 1] - tr0[Ld + 1]              # after single block 1 (index floor(1 / 1) = 1)
+    np.testing.assert_array_equal(diff[:nt], 0.0)
+    np.testing.assert_allclose(diff[nt:], 0.8 * 0.5 * R, rtol=0, atol=1e-12)
+    # the last block's residual reaches v through the final layer alone
+    h = tr1[-1][nt:]
+    shf, scf = np.split(O.linear(O.silu(O.conditioning_vec(W, float(batch.sigma[0]), float(batch.guidance[0]),
+                                                           O.bf16_to_f64(batch.pooled[0]), cfg.guidance_embed)),
+                                 W["final.mod.w"], W["final.mod.b"]), 2)
+    v_manual = O.linear((1.0 + scf) * O.layer_norm(h) + shf, W["final.linear.w"], W["final.linear.b"])
+    np.testing.assert_allclose(v1, v_manual, rtol=0, atol=1e-12)
+    # zero residual -> bitwise the bare model (P3 for single blocks)
+    cz = O.ControlNetInput(double={}, single={1: np.zeros_like(R)}, n_res=0, n_res_single=2)
+    vz, _ = _trace_velocity(cfg, W, batch, 0, [cz])
+    np.testing.assert_array_equal(vz, v0)
+    assert max_rel(v1, v0) > 1e-3                 # and it matters
+
+
+def test_p13_controlnet_fan_in_is_additive(W_bits):
+    """Fan-in: two ControlNets feeding the same blocks act like one whose residual
+    is the scaled sum (the step is affine in the residual at its injection point)."""
+    cfg = CFG_S
+    W = _W(W_bits, cfg)
+    batch = _batch(cfg)
+    ni, D = batch.img_tokens, cfg.hidden
+    R1, R2, S1 = (RNG.standard_normal((ni, D)) * 0.1 for _ in range(3))
+    a = O.ControlNetInput(double={0: R1}, single={0: S1}, n_res=1, n_res_single=1, scale=0.7)
+    b = O.ControlNetInput(double={0: R2}, single={}, n_res=1, n_res_single=0, scale=-0.4)
+    both = O.ControlNetInput(double={0: 0.7 * R1 - 0.4 * R2}, single={0: 0.7 * S1}, n_res=1, n_res_single=1)
+    v_ab, _ = _trace_velocity(cfg, W, batch, 0, [a, b])
+    v_one, _ = _trace_velocity(cfg, W, batch, 0, [both])
+    np.testing.assert_allclose(v_ab, v_one, rtol=0, atol=1e-12 * np.abs(v_one).max())
+    v_a, _ = _trace_velocity(cfg, W, batch, 0, [a])
+    assert max_rel(v_ab, v_a) > 1e-3              # the second ControlNet is not dropped
