@@ -117,6 +117,18 @@ DEVI void store_bf16_32(bf16* dst, const float (&x)[32], int valid) {
   }
 }
 
+// h4[0..7] (32 fp32) += kap * R[0..31] (bf16)
+DEVI void cn_add8(float4 (&h4)[8], const bf16* cn, float kap) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
+    h4[q].x += kap * bf16_lo(c2.x);
+    h4[q].y += kap * bf16_hi(c2.x);
+    h4[q].z += kap * bf16_lo(c2.y);
+    h4[q].w += kap * bf16_hi(c2.y);
+  }
+}
+
 // d = 128 QKV epilogue helpers: 64 accumulator columns + bias -> y (fp32)
 DEVI void load_head_half(uint32_t taddr, const bf16* bias, float (&y)[64]) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&y[0]));
@@ -369,22 +381,11 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           h4[q].y += g4.y * y[4 * q + 1];
           h4[q].z += g4.z * y[4 * q + 2];
           h4[q].w += g4.w * y[4 * q + 3];
-          if (cn0 != nullptr) {
-            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn0) + q);
-            h4[q].x += kap0 * bf16_lo(c2.x);
-            h4[q].y += kap0 * bf16_hi(c2.x);
-            h4[q].z += kap0 * bf16_lo(c2.y);
-            h4[q].w += kap0 * bf16_hi(c2.y);
-          }
-          if (cn1 != nullptr) {
-            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn1) + q);
-            h4[q].x += kap1 * bf16_lo(c2.x);
-            h4[q].y += kap1 * bf16_hi(c2.x);
-            h4[q].z += kap1 * bf16_lo(c2.y);
-            h4[q].w += kap1 * bf16_hi(c2.y);
-          }
-          reinterpret_cast<float4*>(hp)[q] = h4[q];
         }
+        if (cn0 != nullptr) cn_add8(h4, cn0, kap0);
+        if (cn1 != nullptr) cn_add8(h4, cn1, kap1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) reinterpret_cast<float4*>(hp)[q] = h4[q];
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) {   // static indices keep y in registers
