@@ -168,6 +168,20 @@ int lora_unmerge(dit_ctx* ctx);
 int controlnet_inject(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
                       float scale, void* ready_event);
 
+/* controlnet_inject with the readiness carried by a DEVICE FLAG instead of a
+ * CUDA event -- the data engine's deferred fetch done in hardware
+ * (SURVEY.md §8(f) f2): the producer (another stream, or
+ * another GPU writing `residual` into this GPU's memory over NVLink) writes the
+ * residual and then stores *flag = value >= expect with release semantics at
+ * system scope; the consuming GEMM epilogue acquires *flag >= expect before it
+ * reads the residual (no host synchronisation, no event).  flag: 4-byte aligned
+ * device (or peer / host-mapped) memory, read with ld.acquire.sys.  A flag that
+ * never reaches `expect` traps after a few seconds (sticky DIT_ECUDA) rather
+ * than hanging.  The producer must not depend on this step.
+ * Errors: as controlnet_inject, plus DIT_EINVAL (NULL / misaligned flag). */
+int controlnet_inject_flag(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
+                           float scale, const uint32_t* flag, uint32_t expect);
+
 /* ------------------------------------------------------ sequence parallel */
 /* Parallelism descriptor: this context is rank `rank` of
  * `world` GPUs running one dit_step together with Ulysses sequence
@@ -248,6 +262,12 @@ int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, 
  * tcgen05 attention kernel into buf (device int64 [20 events][64 kv tiles]);
  * NULL disables (the default). */
 int dit_debug_attention_trace(void* buf);
+
+/* Test-only stand-in for a remote ControlNet producer: after `delay_ns`, one CTA
+ * copies `bytes` (multiple of 16, 16-byte aligned) from src to dst and then
+ * publishes *flag = value (st.release.sys).  Enqueued on `stream`. */
+int dit_debug_delayed_publish(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                              uint64_t delay_ns, void* stream);
 
 /* ncclGetUniqueId for sp_init (rank 0 calls it, the caller broadcasts the 128 bytes). */
 int dit_nccl_unique_id(void* out128);

@@ -145,7 +145,7 @@ struct dit_ctx {
   std::vector<cudaEvent_t> slot_last_use;
   int merged_adapter = -1;           // lora_merge: adapter patched into tm_m copies (-1: none)
   // ControlNet registrations for the next step
-  struct CnReg { const void* ptr; float scale; cudaEvent_t ready; };
+  struct CnReg { const void* ptr; float scale; cudaEvent_t ready; const uint32_t* flag; uint32_t expect; };
   std::map<std::pair<int, int>, std::vector<CnReg>> cn;   // (slot, block) -> up to CN_FANIN residuals
   // SP
   int world = 1, rank = 0;
@@ -178,6 +178,9 @@ struct dit_ctx {
   const void** p_cn_ptr = nullptr;   // [Ld + Ls][CN_FANIN][8]
   float* p_slot_scale = nullptr;     // [max_adapters]
   float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][8] cn_scale_b * inject scale
+  const uint32_t** p_cn_flag = nullptr;   // [Ld + Ls][CN_FANIN][8] device ready flags (controlnet_inject_flag)
+  uint32_t* p_cn_expect = nullptr;        // [Ld + Ls][CN_FANIN][8]
+  bool cn_flags = false;                  // any flag registration in the current step
   RowSpace rs[3];                    // 0 txt stream, 1 img stream, 2 joint
   int slot_cap = 1;
   // plan cache key
@@ -273,7 +276,7 @@ Layout layout_of(const dit_config& c) {
   L.xprep = cv.take(8 * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
   L.temb = cv.take(8 * 256 * 2);
   L.segs = cv.take((nseg + 6) * sizeof(SkinnySeg));
-  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8 * (sizeof(void*) + 4) + 2048);
+  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8 * 2 * (sizeof(void*) + 4) + 2048);
   L.rowspace = cv.take(3 * (R * 4 + tiles * 8 * 4 + tiles * 4 + tiles * 8 * 8) + 3 * 1024);
   size_t per_slot = 0;
   if (c.max_adapters > 0 && r_alloc > 0) {
@@ -356,6 +359,8 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     const size_t ncn = (size_t)std::max(c->Ld + c->Ls, 1) * CN_FANIN * 8;
     c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take(ncn * sizeof(void*)));
     c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take(ncn * 4));
+    c->p_cn_flag = reinterpret_cast<const uint32_t**>(p + cv.take(ncn * sizeof(void*)));
+    c->p_cn_expect = reinterpret_cast<uint32_t*>(p + cv.take(ncn * 4));
   }
   {
     const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
@@ -763,8 +768,26 @@ extern "C" int controlnet_inject(dit_ctx* c, int32_t slot, int32_t block, const 
   auto& lst = c->cn[{slot, block}];
   if ((int)lst.size() >= CN_FANIN)
     return c->fail(DIT_ENOSPC, "request %d block %d already has %d ControlNet residuals (fan-in limit)", slot, block, CN_FANIN);
-  lst.push_back({residual, scale, reinterpret_cast<cudaEvent_t>(ready)});
+  lst.push_back({residual, scale, reinterpret_cast<cudaEvent_t>(ready), nullptr, 0});
   return DIT_OK;
+}
+
+extern "C" int controlnet_inject_flag(dit_ctx* c, int32_t slot, int32_t block, const void* residual, float scale,
+                                      const uint32_t* flag, uint32_t expect) {
+  if (!c) return DIT_EINVAL;
+  if (!flag || (reinterpret_cast<uintptr_t>(flag) & 3)) return c->fail(DIT_EINVAL, "flag must be a 4-byte aligned device pointer");
+  const int r = controlnet_inject(c, slot, block, residual, scale, nullptr);
+  if (r != DIT_OK) return r;
+  auto& e = c->cn[{slot, block}].back();
+  e.flag = flag;
+  e.expect = expect;
+  return DIT_OK;
+}
+
+extern "C" int dit_debug_delayed_publish(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                                         uint64_t delay_ns, void* stream) {
+  return delayed_publish_launch(dst, src, bytes, flag, value, delay_ns, reinterpret_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? DIT_OK : DIT_ECUDA;
 }
 
 // ------------------------------------------------------------------ SP
@@ -1147,19 +1170,30 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     std::vector<float> ss(64, 0.f);
     for (size_t i = 0; i < c->slot_scale_h.size() && i < 64; ++i) ss[i] = c->slot_scale_h[i];
     cudaMemcpyAsync(c->p_slot_scale, ss.data(), 64 * 4, cudaMemcpyHostToDevice, s);
+    c->cn_flags = false;
     if (!c->cn.empty()) {
       // [block][fan-in k][request] tables of the residuals registered for this step
       const size_t ncn = (size_t)(c->Ld + c->Ls) * CN_FANIN * 8;
       std::vector<const void*> cp(ncn, nullptr);
       std::vector<float> kap(ncn, 0.f);
+      std::vector<const uint32_t*> fl(ncn, nullptr);
+      std::vector<uint32_t> ex(ncn, 0);
+      c->cn_flags = false;
       for (auto& kv : c->cn)
         for (size_t k = 0; k < kv.second.size(); ++k) {
           const size_t at = ((size_t)kv.first.second * CN_FANIN + k) * 8 + kv.first.first;
           cp[at] = kv.second[k].ptr;
           kap[at] = kv.second[k].scale * (b->cn_scale ? b->cn_scale[kv.first.first] : 1.f);
+          fl[at] = kv.second[k].flag;
+          ex[at] = kv.second[k].expect;
+          c->cn_flags |= kv.second[k].flag != nullptr;
         }
       cudaMemcpyAsync(c->p_cn_ptr, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(c->p_cn_kappa, kap.data(), kap.size() * 4, cudaMemcpyHostToDevice, s);
+      if (c->cn_flags) {
+        cudaMemcpyAsync(c->p_cn_flag, fl.data(), fl.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(c->p_cn_expect, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice, s);
+      }
     }
   }
   if (c->segs_dirty) {
@@ -1405,6 +1439,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         eI.cn_ptr = cn_ptr;
         eI.cn_scale = c->p_cn_kappa + (size_t)i * CN_FANIN * 8;
         eI.cn_row0 = 0;   // the img-stream problem's rows are exactly the residual's rows
+        if (c->cn_flags) {
+          eI.cn_flag = c->p_cn_flag + (size_t)i * CN_FANIN * 8;
+          eI.cn_expect = c->p_cn_expect + (size_t)i * CN_FANIN * 8;
+        }
       }
       GemmProblem p[2] = {base_problem(c, AT, Mt, K, lda, LT, eT), base_problem(c, AI, Mi, K, lda, LI, eI)};
       if (any_lora) {
@@ -1531,6 +1569,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         e.cn_ptr = (const void* const*)(c->p_cn_ptr + (size_t)(c->Ld + j) * CN_FANIN * 8);
         e.cn_scale = c->p_cn_kappa + (size_t)(c->Ld + j) * CN_FANIN * 8;
         e.cn_row0 = nt;           // joint rows are [txt; img] per request
+        if (c->cn_flags) {
+          e.cn_flag = c->p_cn_flag + (size_t)(c->Ld + j) * CN_FANIN * 8;
+          e.cn_expect = c->p_cn_expect + (size_t)(c->Ld + j) * CN_FANIN * 8;
+        }
       }
       GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
       if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1], sext_of(c, 0));

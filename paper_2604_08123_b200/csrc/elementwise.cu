@@ -196,6 +196,35 @@ cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ deferred-fetch test producer
+__global__ void delayed_publish_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n16,
+                                       uint32_t* flag, uint32_t value, uint64_t delay_ns) {
+  if (threadIdx.x == 0) {
+    uint64_t t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      __nanosleep(1000);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    } while (t1 - t0 < delay_ns);
+  }
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+  }
+}
+
+cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                                   uint64_t delay_ns, cudaStream_t s) {
+  if (bytes % 16 || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
+    return cudaErrorInvalidValue;
+  delayed_publish_kernel<<<1, 1024, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16,
+                                            flag, value, delay_ns);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ merged LoRA
 // Weight patching: W' = bf16(W + s * B A) for one adapted linear.
 // A 128 x 128 output tile per CTA, 8 warps x 16 rows; the rank-r product runs on

@@ -117,11 +117,26 @@ DEVI void store_bf16_32(bf16* dst, const float (&x)[32], int valid) {
   }
 }
 
-// h4[0..7] (32 fp32) += kap * R[0..31] (bf16)
+// Block until a ControlNet producer (another stream or another GPU writing into this GPU's
+// memory) has published its residual: *flag >= expect, system-scope acquire.  Bounded spin:
+// a producer that never publishes traps instead of hanging the GPU.
+DEVI void cn_acquire(const uint32_t* flag, uint32_t expect) {
+  if (flag == nullptr) return;
+  uint32_t v, spins = 0;
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= expect) break;
+    __nanosleep(256);
+    if (++spins > (1u << 24)) __trap();
+  }
+}
+
+// h4[0..7] (32 fp32) += kap * R[0..31] (bf16).  L2-coherent loads (ld.cg): the residual may
+// have been written by a producer after this kernel started.
 DEVI void cn_add8(float4 (&h4)[8], const bf16* cn, float kap) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cn) + q);
+    const uint2 c2 = __ldcg(reinterpret_cast<const uint2*>(cn) + q);
     h4[q].x += kap * bf16_lo(c2.x);
     h4[q].y += kap * bf16_hi(c2.x);
     h4[q].z += kap * bf16_lo(c2.y);
@@ -369,6 +384,10 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         cn1 = reinterpret_cast<const bf16*>(E.cn_ptr[8 + b]);
         if (cn0 != nullptr) { kap0 = E.cn_scale[b]; cn0 += roff; }
         if (cn1 != nullptr) { kap1 = E.cn_scale[8 + b]; cn1 += roff; }
+        if (E.cn_flag != nullptr) {   // deferred fetch with device flags
+          cn_acquire(E.cn_flag[b], E.cn_expect[b]);
+          cn_acquire(E.cn_flag[8 + b], E.cn_expect[8 + b]);
+        }
       }
       if (valid == 32) {
         float4 h4[8];
@@ -391,8 +410,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         for (int e = 0; e < 32; ++e) {   // static indices keep y in registers
           if (e < valid) {
             float hv = hp[e] + gp[e] * y[e];
-            if (cn0 != nullptr) hv += kap0 * __bfloat162float(cn0[e]);
-            if (cn1 != nullptr) hv += kap1 * __bfloat162float(cn1[e]);
+            if (cn0 != nullptr) hv += kap0 * __bfloat162float(__ldcg(cn0 + e));
+            if (cn1 != nullptr) hv += kap1 * __bfloat162float(__ldcg(cn1 + e));
             hp[e] = hv;
           }
         }

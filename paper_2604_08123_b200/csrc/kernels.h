@@ -45,6 +45,8 @@ struct EpiParams {
   const void* const* cn_ptr; // device [CN_FANIN][8] residual pointers (nullptr = none), bf16 [rows][D]
   const float* cn_scale;     // device [CN_FANIN][8] kappa_b * inject scale
   int cn_row0;               // request-local row of residual row 0 (0: img-stream GEMM; Nt_loc: joint rows)
+  const uint32_t* const* cn_flag;  // device [CN_FANIN][8] ready flags (nullptr = resident / event-ordered)
+  const uint32_t* cn_expect;       // device [CN_FANIN][8] value the flag must reach
   // bf16 outputs
   void* out;
   int ld_out;
@@ -189,6 +191,11 @@ cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s);
 
 // Merged LoRA (weight patching): out[o][i] = bf16(W[o][i] + scale * sum_k Bm[o][k] A[k][i]),
 // W / out bf16 [rows][cols], Bm bf16 [rows][ra], A bf16 [ra][cols], ra a multiple of 16 (<= 128).
+// Test/bench helper standing in for a remote ControlNet producer: after spinning `delay_ns`,
+// copy `bytes` (multiple of 16) from src to dst and publish *flag = value with a system-scope
+// release (so a consumer that acquires the flag sees the data).  One CTA.
+cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                                   uint64_t delay_ns, cudaStream_t s);
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 

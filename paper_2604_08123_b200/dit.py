@@ -56,6 +56,10 @@ EXPORTS = {
     "lora_merge": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p]),
     "lora_unmerge": (C.c_int, [C.c_void_p]),
     "controlnet_inject": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p]),
+    "controlnet_inject_flag": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p,
+                                         C.c_uint32]),
+    "dit_debug_delayed_publish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_uint64,
+                                            C.c_void_p]),
     "sp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
@@ -208,6 +212,12 @@ class DiT:
         self._keep.append(residual)
         ev = ready_event.cuda_event if ready_event is not None else None
         _check(self.lib.controlnet_inject(self.ctx, slot, block, residual.data_ptr(), scale, ev), self.ctx)
+
+    def controlnet_inject_flag(self, slot: int, block: int, residual, flag, expect: int, scale: float = 1.0):
+        """Deferred residual published by a device flag (a uint32 device tensor; *flag >= expect)."""
+        self._keep += [residual, flag]
+        _check(self.lib.controlnet_inject_flag(self.ctx, slot, block, residual.data_ptr(), scale, flag.data_ptr(),
+                                               expect), self.ctx)
 
     def sp_init(self, world: int, rank: int, nccl_uid: Optional[bytes] = None):
         buf = C.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None

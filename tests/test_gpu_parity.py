@@ -284,3 +284,36 @@ def test_controlnet_inject_limits(torch_cuda):
     with pytest.raises(DitError) as e:
         m.controlnet_inject(0, blocks, r)                      # past the last block: DIT_EINVAL
     assert e.value.code == 1
+
+
+def test_controlnet_device_flag_deferred_fetch(torch_cuda):
+    """SURVEY.md §8(f) f2, consumer side: a residual published by a device flag.
+    A producer on another stream writes the residual ~3 ms AFTER the step is enqueued (no event,
+    no host sync); the consuming epilogue must acquire the flag and see the data: the result equals,
+    bit for bit, the step with the residual resident from the start."""
+    import ctypes as C
+    import torch
+    from paper_2604_08123_b200.synthetic import _bits_to_bf16_tensor
+    cfg = synth.TINY_SINGLE
+    m = _model(cfg, 2, 16, 8)
+    batch = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=0)
+    batch.adapter_id = np.array([-1, -1], dtype=np.int32)
+    ni, D, Ld = batch.img_tokens, cfg.hidden, cfg.depth_double
+    src = [_bits_to_bf16_tensor(synth.controlnet_residual_bf16(b, 7, ni, D), "cuda") for b in range(2)]
+    # reference: residuals resident (request 0 on double block 0, request 1 on single block 1)
+    ref_lat, ref_v = m.step(batch, injections=[(0, 0, synth.controlnet_residual_bf16(0, 7, ni, D), 0.8),
+                                               (1, Ld + 1, synth.controlnet_residual_bf16(1, 7, ni, D), 0.8)])
+    for delay_ns in (3_000_000, 0):
+        dst = [torch.full_like(s, 1000.0) for s in src]        # garbage until published
+        flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+        side = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        for b in range(2):
+            assert m.lib.dit_debug_delayed_publish(dst[b].data_ptr(), src[b].data_ptr(), src[b].numel() * 2,
+                                                   C.c_void_p(flag.data_ptr() + 4 * b), 5, delay_ns,
+                                                   C.c_void_p(side.cuda_stream)) == 0
+        m.controlnet_inject_flag(0, 0, dst[0], flag[0:1], 5, scale=0.8)
+        m.controlnet_inject_flag(1, Ld + 1, dst[1], flag[1:2], 5, scale=0.8)
+        lat, v = m.step(batch)
+        np.testing.assert_array_equal(v, ref_v)
+        np.testing.assert_array_equal(lat, ref_lat)
