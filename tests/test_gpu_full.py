@@ -217,3 +217,51 @@ def test_nccl_sp_path_world1_bitwise(torch_cuda):
     finally:
         del os.environ["DIT_FORCE_SP"]
     np.testing.assert_array_equal(v2, v1)
+
+
+def test_flux_width_merged_lora_single_block_controlnet(torch_cuda):
+    """Flux width (D=3072, 24x128 heads, 4608 tokens), 1 double + 1 single block: a merged
+    rank-64 adapter, two ControlNets feeding the double block and one feeding
+    the single block (f4, reading C20), vs the fp64 oracle; merged weights of the widest
+    module (single linear1, 21504 x 3072) checked on sampled rows against numpy."""
+    from oracle.flux_step import ControlNetInput
+    cfg = synth.flux_reduced(1, 1)
+    hh, ww, nt = 64, 64, 512
+    ni, D = hh * ww, cfg.hidden
+    m = _model(cfg, 1, ni, nt, rank=64, adapters=1)
+    m.register_synthetic_lora(4, rank=64, index=0, scale=0.5)
+    m.lora_merge(4)
+    batch = synth.make_batch(cfg, 1, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([4], dtype=np.int32)
+    R = [synth.controlnet_residual_bf16(0, i, ni, D) for i in range(3)]
+    inj = [(0, 0, R[0], 0.7), (0, 0, R[1], -0.3), (0, 1, R[2], 0.5)]
+    lat, v = m.step(batch, injections=inj)
+    f = O.bf16_to_f64
+    cns = {0: [ControlNetInput(double={0: f(R[0])}, single={}, n_res=1, n_res_single=0, scale=0.7),
+               ControlNetInput(double={0: f(R[1])}, single={}, n_res=1, n_res_single=0, scale=-0.3),
+               ControlNetInput(double={}, single={0: f(R[2])}, n_res=0, n_res_single=1, scale=0.5)]}
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = O.dit_step(cfg, W, batch, {4: oracle_adapter(cfg, 64, 0, scale=0.5)[0]}, controlnets=cns)
+    check(v, v_o, "v")
+    check(lat, x_o, "latents")
+    # merged copy of single.0.linear1 on 64 sampled rows
+    Wb = synth.make_weights_bf16(cfg)
+    L = synth.make_lora_bf16(cfg, 64, 0)
+    buf = m._merged
+    pad = (-buf.data_ptr()) % 256
+    off = 0
+    for mod, _, _ in synth.lora_targets(cfg):
+        o, i = Wb[mod + ".w"].shape
+        if mod == "single.0.linear1":
+            break
+        off = (off + o * i * 2 + 255) // 256 * 256
+    rows = np.random.default_rng(0).choice(o, 64, replace=False)
+    raw = buf[pad + off:pad + off + o * i * 2].view(torch_cuda.int16).view(o, i)[torch_cuda.as_tensor(rows, device="cuda")]
+    got = raw.cpu().numpy().view(np.uint16)
+    ref = f(Wb[mod + ".w"][rows]) + 0.5 * f(L[mod + ".lora_B"][rows]) @ f(L[mod + ".lora_A"])
+    want = (((np.asarray(ref, np.float32).view(np.uint32).astype(np.uint64) + 0x7FFF
+              + ((np.asarray(ref, np.float32).view(np.uint32).astype(np.uint64) >> 16) & 1)) >> 16)
+            .astype(np.uint16))
+    ulp = np.abs(got.astype(np.int64) - want.astype(np.int64))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.99
+    m.lora_unmerge()
