@@ -231,7 +231,7 @@ cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uin
 // mma.sync m16n8k16 (r <= 128: 8 K-steps at most) with the B rows (A operand) and the
 // A columns (B operand, ldmatrix .trans from its [k][n] storage) staged in shared memory.
 // Bandwidth-bound: 2 bytes read + 2 written per weight (+ the tiny factors).
-constexpr int LM_TILE = 128, LM_PAD = 8, LM_MAXR = 128;
+constexpr int LM_TILE = 128, LM_ROWS = 64, LM_PAD = 8, LM_MAXR = 128;   // tile: LM_ROWS x LM_TILE
 
 DEVI void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -242,46 +242,51 @@ DEVI void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uin
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
 }
 
-__global__ void __launch_bounds__(256) lora_merge_kernel(const bf16* __restrict__ W, const bf16* __restrict__ A,
+__global__ void __launch_bounds__(LM_ROWS * 2, 6) lora_merge_kernel(const bf16* __restrict__ W, const bf16* __restrict__ A,
                                                          const bf16* __restrict__ Bm, bf16* __restrict__ out, int rows,
                                                          int cols, int ra, float scale) {
+  // smem: W tile [LM_ROWS][128 + PAD] (staged in and out with 16-byte coalesced copies), B rows of
+  // the tile [128][ra + PAD], A columns of the tile [ra][128 + PAD]
   extern __shared__ __align__(16) uint8_t lm_smem[];
-  bf16* sB = reinterpret_cast<bf16*>(lm_smem);                        // [128][ra + PAD]   (B rows of the tile)
-  bf16* sA = sB + LM_TILE * (ra + LM_PAD);                            // [ra][128 + PAD]   (A columns of the tile)
-  const int row0 = blockIdx.y * LM_TILE, col0 = blockIdx.x * LM_TILE;
+  constexpr int LDW = LM_TILE + LM_PAD;
+  bf16* sW = reinterpret_cast<bf16*>(lm_smem);
+  bf16* sB = sW + LM_ROWS * LDW;
+  bf16* sA = sB + LM_ROWS * (ra + LM_PAD);
+  const int row0 = blockIdx.y * LM_ROWS, col0 = blockIdx.x * LM_TILE;
   const int t = threadIdx.x, warp = t / 32, lane = t % 32;
   const int ldb = ra + LM_PAD, lda = LM_TILE + LM_PAD;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int r0 = row0 + warp * 16 + gid;
-  // W pairs at this thread's accumulator positions, loaded first so the HBM latency overlaps
-  // the factor staging and the MMAs
-  uint32_t w2[16][2];
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = r0 + h * 8, col = col0 + j * 8 + 2 * tig;
-      w2[j][h] = (r < rows && col + 1 < cols) ? __ldcs(reinterpret_cast<const unsigned int*>(W + (size_t)r * cols + col)) : 0u;
+  const bool full = row0 + LM_ROWS <= rows && col0 + LM_TILE <= cols && (cols % 8) == 0;
+  // 1. everything in flight at once: W tile, B rows, A columns (cp.async, 16 B per request)
+  if (full) {
+    for (int i = t; i < LM_ROWS * (LM_TILE / 8); i += blockDim.x) {
+      const int r = i / (LM_TILE / 8), c8 = (i % (LM_TILE / 8)) * 8;
+      cp_async16(smem_u32(sW + r * LDW + c8), W + (size_t)(row0 + r) * cols + col0 + c8, true);
     }
-  for (int i = t; i < LM_TILE * (ra / 8); i += blockDim.x) {   // 16-byte chunks of B rows
+  } else {
+    for (int i = t; i < LM_ROWS * LM_TILE; i += blockDim.x) {
+      const int r = i / LM_TILE, c = i % LM_TILE;
+      sW[r * LDW + c] = (row0 + r < rows && col0 + c < cols) ? W[(size_t)(row0 + r) * cols + col0 + c]
+                                                             : __float2bfloat16_rn(0.f);
+    }
+  }
+  for (int i = t; i < LM_ROWS * (ra / 8); i += blockDim.x) {
     const int r = i / (ra / 8), k8 = (i - r * (ra / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row0 + r < rows) v = __ldg(reinterpret_cast<const uint4*>(Bm + (size_t)(row0 + r) * ra + k8));
-    *reinterpret_cast<uint4*>(sB + r * ldb + k8) = v;
+    const bool ok = row0 + r < rows;
+    cp_async16(smem_u32(sB + r * ldb + k8), Bm + (size_t)(ok ? row0 + r : 0) * ra + k8, ok);
   }
-  for (int i = t; i < ra * (LM_TILE / 8); i += blockDim.x) {   // 16-byte chunks of A rows
+  for (int i = t; i < ra * (LM_TILE / 8); i += blockDim.x) {
     const int k = i / (LM_TILE / 8), c8 = (i - k * (LM_TILE / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (col0 + c8 + 8 <= cols) {
-      v = __ldg(reinterpret_cast<const uint4*>(A + (size_t)k * cols + col0 + c8));
-    } else if (col0 + c8 < cols) {
-      bf16 e[8];
-      for (int q = 0; q < 8; ++q) e[q] = col0 + c8 + q < cols ? A[(size_t)k * cols + col0 + c8 + q] : __float2bfloat16_rn(0.f);
-      v = *reinterpret_cast<uint4*>(e);
+    if (col0 + c8 + 8 <= cols && (cols % 8) == 0) {
+      cp_async16(smem_u32(sA + k * lda + c8), A + (size_t)k * cols + col0 + c8, true);
+    } else {
+      for (int q = 0; q < 8; ++q)
+        sA[k * lda + c8 + q] = col0 + c8 + q < cols ? A[(size_t)k * cols + col0 + c8 + q] : __float2bfloat16_rn(0.f);
     }
-    *reinterpret_cast<uint4*>(sA + k * lda + c8) = v;
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
+  // 2. the rank-r product on mma.sync (LM_ROWS / 16 warps x 16 rows x 128 columns)
   float acc[16][4];
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -299,22 +304,28 @@ __global__ void __launch_bounds__(256) lora_merge_kernel(const bf16* __restrict_
       mma_bf16_16816(acc[j + 1], a, b1);
     }
   }
-  // C fragment: (row gid, cols 2 tig, 2 tig + 1) and (row gid + 8, same cols) of each n-block
+  // 3. W' = bf16(W + s * acc) in place in smem (fragment: rows gid / gid + 8, cols 2 tig, 2 tig + 1)
+  const int gid = lane >> 2, tig = lane & 3;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int col = col0 + j * 8 + 2 * tig;
-    if (col >= cols) continue;
+  for (int j = 0; j < 16; ++j)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = r0 + h * 8;
-      if (r >= rows) continue;
-      const size_t off = (size_t)r * cols + col;
-      if (col + 1 < cols) {
-        __stcs(reinterpret_cast<unsigned int*>(out + off),
-               pack_bf16(bf16_lo(w2[j][h]) + scale * acc[j][2 * h], bf16_hi(w2[j][h]) + scale * acc[j][2 * h + 1]));
-      } else {
-        out[off] = __float2bfloat16_rn(__bfloat162float(W[off]) + scale * acc[j][2 * h]);
-      }
+      uint32_t* p = reinterpret_cast<uint32_t*>(sW + (warp * 16 + gid + h * 8) * LDW + j * 8 + 2 * tig);
+      const uint32_t w2 = *p;
+      *p = pack_bf16(bf16_lo(w2) + scale * acc[j][2 * h], bf16_hi(w2) + scale * acc[j][2 * h + 1]);
+    }
+  __syncthreads();
+  // 4. coalesced write-out
+  if (full) {
+    for (int i = t; i < LM_ROWS * (LM_TILE / 8); i += blockDim.x) {
+      const int r = i / (LM_TILE / 8), c8 = (i % (LM_TILE / 8)) * 8;
+      __stcs(reinterpret_cast<uint4*>(out + (size_t)(row0 + r) * cols + col0 + c8),
+             *reinterpret_cast<const uint4*>(sW + r * LDW + c8));
+    }
+  } else {
+    for (int i = t; i < LM_ROWS * LM_TILE; i += blockDim.x) {
+      const int r = i / LM_TILE, c = i % LM_TILE;
+      if (row0 + r < rows && col0 + c < cols) out[(size_t)(row0 + r) * cols + col0 + c] = sW[r * LDW + c];
     }
   }
 }
@@ -322,16 +333,17 @@ __global__ void __launch_bounds__(256) lora_merge_kernel(const bf16* __restrict_
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s) {
   if (rows <= 0 || cols <= 0 || ra <= 0 || ra % 16 || ra > LM_MAXR || cols % 2) return cudaErrorInvalidValue;
-  const int smem = (LM_TILE * (ra + LM_PAD) + ra * (LM_TILE + LM_PAD)) * 2;
+  const int smem = (LM_ROWS * (LM_TILE + LM_PAD) + LM_ROWS * (ra + LM_PAD) + ra * (LM_TILE + LM_PAD)) * 2;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(lora_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (LM_TILE * (LM_MAXR + LM_PAD) + LM_MAXR * (LM_TILE + LM_PAD)) * 2);
+                                         (LM_ROWS * (LM_TILE + LM_PAD) + LM_ROWS * (LM_MAXR + LM_PAD) +
+                                          LM_MAXR * (LM_TILE + LM_PAD)) * 2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((cols + LM_TILE - 1) / LM_TILE, (rows + LM_TILE - 1) / LM_TILE);
-  lora_merge_kernel<<<grid, 256, smem, s>>>(static_cast<const bf16*>(W), static_cast<const bf16*>(A),
+  dim3 grid((cols + LM_TILE - 1) / LM_TILE, (rows + LM_ROWS - 1) / LM_ROWS);
+  lora_merge_kernel<<<grid, LM_ROWS * 2, smem, s>>>(static_cast<const bf16*>(W), static_cast<const bf16*>(A),
                                             static_cast<const bf16*>(Bm), static_cast<bf16*>(out), rows, cols, ra, scale);
   return cudaGetLastError();
 }
