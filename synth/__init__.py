@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
@@ -47,6 +47,12 @@ class ModelCfg:
     rope_axes: Tuple[int, int, int] = (16, 56, 56)
     rope_theta: float = 10000.0
     guidance_embed: bool = True
+    # "flux": double + single blocks, 3-axis RoPE (reading C1).  "sd3": SD3 / SD3.5 MMDiT
+    # (joint blocks only, 2-D sincos position table, last block context_pre_only; reading C21).
+    arch: str = "flux"
+    qk_norm: bool = True        # sd3 only: SD3.5 has QK-RMSNorm, SD3(-medium) has none
+    pos_embed_max: int = 192    # sd3: side of the sincos position grid (centre-cropped)
+    pos_embed_base: int = 64    # sd3: base size of the grid (positions = arange * base / max)
 
     @property
     def head_dim(self) -> int:
@@ -65,6 +71,21 @@ TINY_SINGLE = dataclasses.replace(TINY, depth_double=1, depth_single=2)
 # Flux-Dev shape (configs[1..4]) [ext].
 FLUX = ModelCfg(hidden=3072, heads=24, depth_double=19, depth_single=38,
                 in_channels=64, txt_dim=4096, pooled_dim=768)
+
+
+# SD3 family (PAPER.md:289, :1305, :1330-1331 name SD3 and SD3.5-Large) [ext]:
+# SD3-medium 24 joint blocks, D = 1536 (24 heads x 64), no QK-norm; SD3.5-Large 38 joint
+# blocks, D = 2432 (38 x 64), QK-RMSNorm.  Packed latents 16 ch x 2 x 2 = 64, T5 width 4096,
+# pooled CLIP-L + CLIP-G = 2048, text tokens 77 (CLIP) + 256 (T5) = 333.
+SD3_MEDIUM = ModelCfg(hidden=1536, heads=24, depth_double=24, depth_single=0, in_channels=64,
+                      txt_dim=4096, pooled_dim=2048, rope_axes=(0, 0, 0), guidance_embed=False,
+                      arch="sd3", qk_norm=False)
+SD35_LARGE = dataclasses.replace(SD3_MEDIUM, hidden=2432, heads=38, depth_double=38, qk_norm=True)
+SD3_TXT_TOKENS = 333
+# Tiny SD3: 2 joint blocks (the second context_pre_only), d = 32, an 8 x 8 position grid.
+SD3_TINY = ModelCfg(hidden=64, heads=2, depth_double=2, depth_single=0, in_channels=16, txt_dim=32,
+                    pooled_dim=16, rope_axes=(0, 0, 0), guidance_embed=False, arch="sd3",
+                    qk_norm=True, pos_embed_max=8, pos_embed_base=4)
 
 
 def flux_reduced(depth_double: int, depth_single: int) -> ModelCfg:
@@ -120,6 +141,12 @@ def _mod(name: str, out_f: int, in_f: int):
     return [(name + ".w", (out_f, in_f), MOD_W, in_f), (name + ".b", (out_f,), MOD_B, in_f)]
 
 
+def context_pre_only(cfg: ModelCfg, block: int, stream: str) -> bool:
+    """SD3: the last joint block's text stream only feeds attention (no proj / MLP; its
+    modulation is the 2-chunk AdaLayerNormContinuous) [ext], reading C21."""
+    return cfg.arch == "sd3" and stream == "txt" and block == cfg.depth_double - 1
+
+
 def weight_manifest(cfg: ModelCfg) -> List[TensorSpec]:
     """Every base-model tensor, in canonical order (tensor_id = position).
 
@@ -138,9 +165,13 @@ def weight_manifest(cfg: ModelCfg) -> List[TensorSpec]:
     for i in range(cfg.depth_double):
         for s in ("img", "txt"):
             p = f"double.{i}.{s}."
-            ent += _mod(p + "mod", 6 * D, D)
+            pre_only = context_pre_only(cfg, i, s)
+            ent += _mod(p + "mod", (2 if pre_only else 6) * D, D)
             ent += _lin(p + "qkv", 3 * D, D)
-            ent += [(p + "q_norm", (d,), GAMMA, d), (p + "k_norm", (d,), GAMMA, d)]
+            if cfg.arch == "flux" or cfg.qk_norm:
+                ent += [(p + "q_norm", (d,), GAMMA, d), (p + "k_norm", (d,), GAMMA, d)]
+            if pre_only:
+                continue
             ent += _lin(p + "proj", D, D)
             ent += _lin(p + "fc1", F, D)
             ent += _lin(p + "fc2", D, F)
@@ -170,7 +201,9 @@ def lora_targets(cfg: ModelCfg) -> List[Tuple[str, int, int]]:
     for i in range(cfg.depth_double):
         for s in ("img", "txt"):
             p = f"double.{i}.{s}."
-            t += [(p + "qkv", D, 3 * D), (p + "proj", D, D), (p + "fc1", D, F), (p + "fc2", F, D)]
+            t += [(p + "qkv", D, 3 * D)]
+            if not context_pre_only(cfg, i, s):
+                t += [(p + "proj", D, D), (p + "fc1", D, F), (p + "fc2", F, D)]
     for j in range(cfg.depth_single):
         p = f"single.{j}."
         t += [(p + "linear1", D, 3 * D + F), (p + "linear2", D + F, D)]
@@ -325,6 +358,10 @@ class Batch:
     guidance: np.ndarray       # fp32 [B]
     adapter_id: np.ndarray     # int32 [B], -1 = none
     cn_scale: np.ndarray       # fp32 [B]
+    # classifier-free guidance (reading C22): None = one pass per request
+    cfg_scale: Optional[np.ndarray] = None   # fp32 [B]
+    txt_neg: Optional[np.ndarray] = None     # uint16 bf16 bits [B, Nt, Ct] (unconditional branch)
+    pooled_neg: Optional[np.ndarray] = None  # uint16 bf16 bits [B, Cp]
 
     @property
     def batch(self) -> int:
@@ -335,11 +372,32 @@ class Batch:
         return self.img_h * self.img_w
 
 
+def negative_txt_bf16(b_seed_index: int, nt: int, ct: int) -> np.ndarray:
+    """Unconditional-branch text embeddings ~ N(0, 1) bf16 bits, seed 6000 + b."""
+    x = np.random.default_rng(6000 + b_seed_index).standard_normal((nt, ct)).astype(np.float32)
+    return fp32_to_bf16_bits(x)
+
+
+def negative_pooled_bf16(b_seed_index: int, cp: int) -> np.ndarray:
+    x = np.random.default_rng(6500 + b_seed_index).standard_normal((cp,)).astype(np.float32)
+    return fp32_to_bf16_bits(x)
+
+
 def make_batch(cfg: ModelCfg, batch: int, img_h: int, img_w: int, txt_tokens: int,
-               n_adapters: int = 0, guidance: float = 3.5, first_request: int = 0) -> Batch:
+               n_adapters: int = 0, guidance: float = 3.5, first_request: int = 0,
+               cfg_scale: Optional[float] = None) -> Batch:
+    """cfg_scale: classifier-free guidance scale (SD3 default 7.0 [ext]); None = no CFG."""
     ni = img_h * img_w
     sig = flux_sigmas(28, ni)
     k = step_indices(batch)
+    neg = {}
+    if cfg_scale is not None:
+        neg = dict(
+            cfg_scale=np.full(batch, cfg_scale, dtype=np.float32),
+            txt_neg=np.stack([negative_txt_bf16(first_request + b, txt_tokens, cfg.txt_dim)
+                              for b in range(batch)]),
+            pooled_neg=np.stack([negative_pooled_bf16(first_request + b, cfg.pooled_dim)
+                                 for b in range(batch)]))
     return Batch(
         img_h=img_h, img_w=img_w, txt_tokens=txt_tokens,
         latents=np.stack([latents(first_request + b, ni, cfg.in_channels) for b in range(batch)]),
@@ -350,4 +408,5 @@ def make_batch(cfg: ModelCfg, batch: int, img_h: int, img_w: int, txt_tokens: in
         guidance=np.full(batch, guidance, dtype=np.float32),
         adapter_id=adapter_ids(batch, n_adapters),
         cn_scale=np.ones(batch, dtype=np.float32),
+        **neg,
     )
