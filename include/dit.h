@@ -70,7 +70,24 @@ typedef struct dit_config {
   int32_t max_txt_tokens;  /* largest Nt (global, before sharding)                */
   int32_t max_rank;        /* largest LoRA rank (<= 128)                          */
   int32_t max_adapters;    /* adapter-pool slots (registered adapters)            */
+  /* Model family (readings C1 / C21; the paper serves Flux-Dev, SD3 and
+   * SD3.5-Large workflows, and loads
+   * SD3Transformer2DModel at PAPER.md:841):
+   *   DIT_ARCH_FLUX: depth_double double + depth_single single blocks, 3-axis RoPE.
+   *   DIT_ARCH_SD3:  depth_double joint blocks (depth_single must be 0, no guidance
+   *   embedding, rope_axes ignored); a 2-D sincos position table over a
+   *   pos_embed_max^2 grid (positions * pos_embed_base / pos_embed_max, centre-
+   *   cropped) is added to the embedded image tokens; the last block's text stream
+   *   is context_pre_only (2-chunk (scale, shift) modulation, feeds attention only);
+   *   final modulation (scale, shift).  qk_norm: 1 = per-head QK-RMSNorm with
+   *   learned gamma (SD3.5), 0 = none (SD3-medium).  Ignored for Flux (always on). */
+  int32_t arch;
+  int32_t qk_norm;
+  int32_t pos_embed_max;   /* 192 for SD3 / SD3.5                                 */
+  int32_t pos_embed_base;  /* 64 for SD3 / SD3.5                                  */
 } dit_config;
+
+enum { DIT_ARCH_FLUX = 0, DIT_ARCH_SD3 = 1 };
 
 typedef struct dit_ctx dit_ctx;
 
@@ -193,6 +210,22 @@ int controlnet_inject_flag(dit_ctx* ctx, int32_t slot, int32_t block, const void
  * Errors: DIT_EPARALLEL (world does not divide H), DIT_ENCCL, DIT_EINVAL. */
 int sp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_id);
 
+/* ------------------------------------------------------ latent parallelism */
+/* Latent (CFG) parallelism (the conditional and unconditional
+ * passes of classifier-free guidance on separate GPUs, with a scatter-gather of the
+ * partial results at every denoising step).  This context becomes rank `rank` of
+ * `world` = 2 GPUs: rank 0 computes every request's conditional pass, rank 1 its
+ * unconditional pass; after the final layer the two ranks exchange their v
+ * (ncclAllGather, B*Ni*C fp32 per rank) and BOTH apply the guided Euler update, so
+ * latents_out is identical on both ranks.  Each rank passes the full latents and
+ * its own branch's txt / pooled; batch.cfg_scale must be non-NULL.  Collective:
+ * both ranks call it and then every dit_step together.  Exclusive with sp_init.
+ * Errors: DIT_EPARALLEL (world != 2, or sp_init already active), DIT_ENCCL,
+ * DIT_EINVAL. */
+int lp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_id);
+/* Test analogue of lp_init over an in-process group (dit_local_group_create(2)). */
+int lp_init_local(dit_ctx* ctx, void* group, int32_t rank);
+
 /* -------------------------------------------------------------------- step */
 typedef struct dit_batch {
   int32_t batch;              /* B (1 .. B_max)                                  */
@@ -208,13 +241,26 @@ typedef struct dit_batch {
   const void* txt;            /* device bf16 [B][Nt/P][Ct]                       */
   const void* pooled;         /* device bf16 [B][Cp]                             */
   float* v_out;               /* device fp32 [B][Ni/P][C] noise_pred; nullable   */
+  /* Classifier-free guidance (reading C22).  NULL = one
+   * pass per request.  Non-NULL: host [B] guidance scales g_b; every request runs a
+   * conditional and an unconditional SEQUENCE and
+   *   v_b = v_uncond + g_b (v_cond - v_uncond),  latents_out = latents_in + dsig v_b.
+   * Without latent parallelism the step runs 2B sequences (2B <= B_max, else
+   * DIT_EBATCH): txt is then [2B][Nt][Ct] and pooled [2B][Cp] -- the B conditional
+   * prompts, then the B unconditional ones -- and ControlNet slot s < B feeds request
+   * s's conditional pass, slot B + s its unconditional pass.  Under lp_init (one
+   * branch per GPU) txt / pooled are [B] rows of THIS rank's branch (rank 0
+   * conditional, rank 1 unconditional) and slots are request indices.  v_out, when
+   * given, receives the guided v. */
+  const float* cfg_scale;
 } dit_batch;
 
 /* execute() + denoise(): one flow-matching Euler step
  * latents_out = latents_in + (sigma_next - sigma) * v for every request,
  * asynchronously on `stream` (a cudaStream_t).  All pointers are borrowed.
- * Errors: DIT_EBATCH, DIT_ESHAPE, DIT_EADAPTER, DIT_EALIAS, DIT_EINVAL,
- * DIT_ENOWEIGHTS, DIT_ECUDA, DIT_ENCCL. */
+ * Errors: DIT_EBATCH, DIT_ESHAPE (also: an SD3 token grid larger than
+ * pos_embed_max), DIT_EADAPTER, DIT_EALIAS, DIT_EINVAL (also: lp_init active and
+ * cfg_scale NULL), DIT_ENOWEIGHTS, DIT_ECUDA, DIT_ENCCL. */
 int dit_step(dit_ctx* ctx, const dit_batch* batch, void* stream);
 
 /* Algorithmic tensor FLOPs of one dit_step on `batch` (DESIGN.md §5 formula:

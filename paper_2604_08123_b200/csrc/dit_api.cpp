@@ -119,6 +119,22 @@ struct LocalGroup {
     for (int r = 0; r < world; ++r) cudaStreamWaitEvent(s, done[r], 0);
     barrier();
   }
+  // in-place all-gather: rank r's chunk lives at buf + r * bytes in every rank's buf
+  void allgather(int rank, void* buf, size_t bytes, cudaStream_t s) {
+    cudaEventRecord(ready[rank], s);
+    send[rank] = buf;
+    barrier();
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) continue;
+      cudaStreamWaitEvent(s, ready[r], 0);
+      cudaMemcpyAsync(static_cast<uint8_t*>(buf) + (size_t)r * bytes,
+                      static_cast<const uint8_t*>(send[r]) + (size_t)r * bytes, bytes, cudaMemcpyDeviceToDevice, s);
+    }
+    cudaEventRecord(done[rank], s);
+    barrier();
+    for (int r = 0; r < world; ++r) cudaStreamWaitEvent(s, done[r], 0);
+    barrier();
+  }
 };
 
 struct dit_ctx {
@@ -152,6 +168,10 @@ struct dit_ctx {
   ncclComm_t comm = nullptr;
   LocalGroup* local_group = nullptr;
   bool force_sp = false;             // test-only: SP data path at world == 1 (DIT_FORCE_SP)
+  // latent (CFG) parallelism: rank 0 conditional, rank 1 unconditional branch
+  int lp_world = 1, lp_rank = 0;
+  ncclComm_t lp_comm = nullptr;
+  LocalGroup* lp_group = nullptr;
   bf16_t* sp = nullptr;              // [send1 | recv1 | send2 | recv2] at P > 1
   bf16_t* qkv = nullptr;             // attention layout [3][B][H/P][N][d]
   // workspace carve-outs
@@ -161,6 +181,7 @@ struct dit_ctx {
   bf16_t* cat = nullptr;
   bf16_t* sext = nullptr;
   bf16_t* xb = nullptr;
+  float* vcfg = nullptr;             // CFG: v of every sequence [2][B][ni][C] (cond block, uncond block)
   float2* rope = nullptr;
   float* mod = nullptr;
   float* vec = nullptr;
@@ -175,6 +196,7 @@ struct dit_ctx {
   float* p_cn_scale = nullptr;
   float* p_sigma = nullptr;
   float* p_guid = nullptr;
+  float* p_cfg = nullptr;            // [8] CFG scale per request
   const void** p_cn_ptr = nullptr;   // [Ld + Ls][CN_FANIN][8]
   float* p_slot_scale = nullptr;     // [max_adapters]
   float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][8] cn_scale_b * inject scale
@@ -224,6 +246,11 @@ struct Carve {
 
 int n_lora_modules(const dit_config& c) { return c.depth_double * 2 * 4 + c.depth_single * 2; }
 
+// SD3: the last joint block's text stream is context_pre_only (no proj / fc1 / fc2; reading C21).
+bool pre_only(const dit_config& c, int block, int stream) {
+  return c.arch == DIT_ARCH_SD3 && stream == 1 && block == c.depth_double - 1;
+}
+
 bool cfg_valid(const dit_config* c, std::string* why) {
   auto bad = [&](const char* s) { if (why) *why = s; return false; };
   if (!c) return bad("cfg is NULL");
@@ -232,8 +259,18 @@ bool cfg_valid(const dit_config* c, std::string* why) {
   if (d != 32 && d != 64 && d != 128) return bad("head dim must be 32, 64 or 128");
   if (c->hidden % 64) return bad("hidden must be a multiple of 64");
   if (c->hidden > 3072 * 1) { if (c->hidden / 4 > 24 * 32) return bad("hidden > 3072 unsupported"); }
-  if (c->rope_axes[0] + c->rope_axes[1] + c->rope_axes[2] != d) return bad("rope axes must sum to head dim");
-  if (c->rope_axes[0] % 2 || c->rope_axes[1] % 2 || c->rope_axes[2] % 2) return bad("rope axes must be even");
+  if (c->arch != DIT_ARCH_FLUX && c->arch != DIT_ARCH_SD3) return bad("arch must be DIT_ARCH_FLUX or DIT_ARCH_SD3");
+  if (c->arch == DIT_ARCH_FLUX) {
+    if (c->rope_axes[0] + c->rope_axes[1] + c->rope_axes[2] != d) return bad("rope axes must sum to head dim");
+    if (c->rope_axes[0] % 2 || c->rope_axes[1] % 2 || c->rope_axes[2] % 2) return bad("rope axes must be even");
+  } else {
+    if (c->depth_single != 0) return bad("SD3 has no single-stream blocks (depth_single must be 0)");
+    if (c->depth_double < 1) return bad("SD3 needs at least one joint block");
+    if (c->guidance_embed) return bad("SD3 has no guidance embedding");
+    if (c->hidden % 4) return bad("SD3 position table needs hidden % 4 == 0");
+    if (c->pos_embed_max < 1 || c->pos_embed_base < 1) return bad("pos_embed_max / pos_embed_base must be positive");
+    if (c->qk_norm != 0 && c->qk_norm != 1) return bad("qk_norm must be 0 or 1");
+  }
   if (c->depth_double < 0 || c->depth_single < 0) return bad("negative depth");
   if (c->in_channels <= 0 || c->in_channels % 8) return bad("in_channels must be a positive multiple of 8");
   if (c->txt_dim <= 0 || c->txt_dim % 8) return bad("txt_dim must be a positive multiple of 8");
@@ -247,7 +284,7 @@ bool cfg_valid(const dit_config* c, std::string* why) {
 }
 
 struct Layout {
-  size_t h, u, qkv, sp, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, total;
+  size_t h, u, qkv, sp, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, vcfg, total;
   size_t pool_bytes_per_slot;
 };
 
@@ -269,6 +306,7 @@ Layout layout_of(const dit_config& c) {
   L.cat = cv.take(R * (D + F) * 2);
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
   L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
+  L.vcfg = cv.take(2 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);   // CFG: v of both branches
   L.rope = cv.take(N * (d / 2) * 8);
   L.mod = cv.take(8 * mod_total * 4);
   L.vec = cv.take(8 * D * 4);
@@ -341,6 +379,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   c->cat = reinterpret_cast<bf16_t*>(w + L.cat);
   c->sext = reinterpret_cast<bf16_t*>(w + L.sext);
   c->xb = reinterpret_cast<bf16_t*>(w + L.xb);
+  c->vcfg = reinterpret_cast<float*>(w + L.vcfg);
   c->rope = reinterpret_cast<float2*>(w + L.rope);
   c->mod = reinterpret_cast<float*>(w + L.mod);
   c->vec = reinterpret_cast<float*>(w + L.vec);
@@ -355,6 +394,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     c->p_cn_scale = reinterpret_cast<float*>(p + cv.take(8 * 4));
     c->p_sigma = reinterpret_cast<float*>(p + cv.take(8 * 4));
     c->p_guid = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_cfg = reinterpret_cast<float*>(p + cv.take(8 * 4));
     c->p_slot_scale = reinterpret_cast<float*>(p + cv.take(64 * 4));
     const size_t ncn = (size_t)std::max(c->Ld + c->Ls, 1) * CN_FANIN * 8;
     c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take(ncn * sizeof(void*)));
@@ -429,6 +469,7 @@ extern "C" void dit_destroy(dit_ctx* c) {
   for (auto& e : c->slot_last_use)
     if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->lp_comm) ncclCommDestroy(c->lp_comm);
   delete c;
 }
 
@@ -458,13 +499,18 @@ void expected_tensors(const dit_ctx* c, std::vector<Expect>& e) {
   if (c->cfg.guidance_embed) { lin("guidance_in.in", D, 256); lin("guidance_in.out", D, D); }
   lin("vector_in.in", D, Cp);
   lin("vector_in.out", D, D);
+  const bool norms = c->cfg.arch == DIT_ARCH_FLUX || c->cfg.qk_norm;
   for (int i = 0; i < c->Ld; ++i)
-    for (const char* s : {"img", "txt"}) {
-      std::string p = "double." + std::to_string(i) + "." + s + ".";
-      lin(p + "mod", 6 * D, D);
+    for (int st = 0; st < 2; ++st) {
+      std::string p = "double." + std::to_string(i) + (st == 0 ? ".img." : ".txt.");
+      const bool po = pre_only(c->cfg, i, st);
+      lin(p + "mod", (po ? 2 : 6) * D, D);
       lin(p + "qkv", 3 * D, D);
-      e.push_back({p + "q_norm", d, -1});
-      e.push_back({p + "k_norm", d, -1});
+      if (norms) {
+        e.push_back({p + "q_norm", d, -1});
+        e.push_back({p + "k_norm", d, -1});
+      }
+      if (po) continue;
       lin(p + "proj", D, D);
       lin(p + "fc1", F, D);
       lin(p + "fc2", D, F);
@@ -514,11 +560,16 @@ int bind_all(dit_ctx* c) {
       DoubleStream& B = c->dbl[s][i];
       ok &= bind_lin(c, B.mod, p + "mod");
       ok &= bind_lin(c, B.qkv, p + "qkv");
-      ok &= bind_lin(c, B.proj, p + "proj");
-      ok &= bind_lin(c, B.fc1, p + "fc1");
-      ok &= bind_lin(c, B.fc2, p + "fc2");
-      B.qn = c->tensors[p + "q_norm"].ptr;
-      B.kn = c->tensors[p + "k_norm"].ptr;
+      if (!pre_only(c->cfg, i, s)) {
+        ok &= bind_lin(c, B.proj, p + "proj");
+        ok &= bind_lin(c, B.fc1, p + "fc1");
+        ok &= bind_lin(c, B.fc2, p + "fc2");
+      }
+      B.qn = B.kn = nullptr;   // SD3-medium: no QK-norm (the epilogue skips it)
+      if (c->cfg.arch == DIT_ARCH_FLUX || c->cfg.qk_norm) {
+        B.qn = c->tensors[p + "q_norm"].ptr;
+        B.kn = c->tensors[p + "k_norm"].ptr;
+      }
     }
   for (int j = 0; j < c->Ls; ++j) {
     std::string p = "single." + std::to_string(j) + ".";
@@ -593,7 +644,7 @@ extern "C" int lora_register(dit_ctx* c, int32_t adapter_id, int32_t rank, float
   for (int i = 0; i < c->Ld; ++i)
     for (int s = 0; s < 2; ++s) {
       const char* names[4] = {"qkv", "proj", "fc1", "fc2"};
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < (pre_only(c->cfg, i, s) ? 1 : 4); ++q)
         modidx["double." + std::to_string(i) + (s == 0 ? ".img." : ".txt.") + names[q]] = c->dbl[s][i].lora[q];
     }
   for (int j = 0; j < c->Ls; ++j) {
@@ -669,6 +720,7 @@ void adapted_shapes(const dit_config& cfg, std::vector<std::pair<int, int>>& v) 
   for (int i = 0; i < cfg.depth_double; ++i)
     for (int s = 0; s < 2; ++s) {
       v.push_back({3 * D, D});
+      if (pre_only(cfg, i, s)) continue;
       v.push_back({D, D});
       v.push_back({F, D});
       v.push_back({D, F});
@@ -684,7 +736,7 @@ std::vector<std::pair<Lin*, int>> adapted_lins(dit_ctx* c) {
     for (int s = 0; s < 2; ++s) {
       DoubleStream& X = c->dbl[s][i];
       Lin* L[4] = {&X.qkv, &X.proj, &X.fc1, &X.fc2};
-      for (int q = 0; q < 4; ++q) v.push_back({L[q], X.lora[q]});
+      for (int q = 0; q < (pre_only(c->cfg, i, s) ? 1 : 4); ++q) v.push_back({L[q], X.lora[q]});
     }
   for (int j = 0; j < c->Ls; ++j) {
     v.push_back({&c->sgl[j].l1, c->sgl[j].lora[0]});
@@ -818,6 +870,7 @@ extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   LocalGroup* g = static_cast<LocalGroup*>(grp);
   if (!g || rank < 0 || rank >= g->world) return c->fail(DIT_EINVAL, "bad local group / rank");
   if (c->H % g->world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", g->world, c->H);
+  if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   c->local_group = g;
   c->world = g->world;
   c->rank = rank;
@@ -830,6 +883,7 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   if (!c) return DIT_EINVAL;
   if (world < 1 || rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad world/rank %d/%d", world, rank);
   if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
+  if (c->lp_world > 1 && world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   // DIT_FORCE_SP=1 (test-only): a 1-rank NCCL communicator drives the full
   // sequence-parallel data path (all-to-alls + gather/scatter) at world == 1.
   const char* force = getenv("DIT_FORCE_SP");
@@ -855,6 +909,40 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   c->rank = rank;
   c->plan_B = -1;
   c->rope_key[0] = -1;
+  return DIT_OK;
+}
+
+// ------------------------------------------------------------------ latent parallelism
+extern "C" int lp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
+  if (!c) return DIT_EINVAL;
+  if (world != 2) return c->fail(DIT_EPARALLEL, "latent parallelism splits the 2 CFG branches: world must be 2, got %d", world);
+  if (rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad rank %d", rank);
+  if (c->world > 1 || c->force_sp) return c->fail(DIT_EPARALLEL, "sequence parallelism is active (sp_init)");
+  if (!uid) return c->fail(DIT_EINVAL, "nccl unique id is NULL");
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  cudaSetDevice(c->device);
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  if (c->lp_comm) ncclCommDestroy(c->lp_comm);
+  c->lp_comm = comm;
+  c->lp_group = nullptr;
+  c->lp_world = world;
+  c->lp_rank = rank;
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
+extern "C" int lp_init_local(dit_ctx* c, void* grp, int32_t rank) {
+  if (!c) return DIT_EINVAL;
+  LocalGroup* g = static_cast<LocalGroup*>(grp);
+  if (!g || g->world != 2 || rank < 0 || rank >= 2) return c->fail(DIT_EPARALLEL, "latent parallelism needs a 2-rank group");
+  if (c->world > 1 || c->force_sp) return c->fail(DIT_EPARALLEL, "sequence parallelism is active (sp_init)");
+  c->lp_group = g;
+  c->lp_world = 2;
+  c->lp_rank = rank;
+  c->plan_B = -1;
   return DIT_OK;
 }
 
@@ -1035,23 +1123,29 @@ int run_shrink(dit_ctx* c, int np, const void* const* A, const int* M, const int
 // ------------------------------------------------------------------ step
 extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
   if (!c || !b) return 0.0;
-  const double B = b->batch, Ni = (double)b->img_h * b->img_w, Nt = b->txt_tokens, N = Ni + Nt;
+  // sequences computed on this GPU: CFG doubles the batch unless latent parallelism splits it
+  const double seq = (b->cfg_scale && c->lp_world == 1) ? 2.0 * b->batch : (double)b->batch;
+  const double B = seq, Ni = (double)b->img_h * b->img_w, Nt = b->txt_tokens, N = Ni + Nt;
   const double D = c->D, F = c->F, C = c->C, Ct = c->Ct;
+  const bool sd3 = c->cfg.arch == DIT_ARCH_SD3;
   double f = 0;
   // embedders (the conditioning MLPs are included as 2MNK with M = B)
   f += 2 * B * Ni * D * C + 2 * B * Nt * D * Ct;
   // double blocks: qkv, proj, fc1, fc2 per stream + attention
   f += c->Ld * (2 * B * N * D * (3 * D) + 2 * B * N * D * D + 2 * 2 * B * N * D * F + 4 * B * N * N * D);
+  // SD3: the context_pre_only last block has no text proj / MLP
+  if (sd3) f -= 2 * B * Nt * D * D + 2 * 2 * B * Nt * D * F;
   // single blocks
   f += c->Ls * (2 * B * N * D * (3 * D + F) + 2 * B * N * (D + F) * D + 4 * B * N * N * D);
   // final
   f += 2 * B * Ni * D * C;
   // LoRA: 2 r (in + out) per row per adapted linear, rows of adapted requests only
-  for (int i = 0; i < b->batch; ++i) {
-    int aid = b->adapter_id ? b->adapter_id[i] : -1;
+  for (int q = 0; q < (int)seq; ++q) {
+    int aid = b->adapter_id ? b->adapter_id[q % b->batch] : -1;
     if (aid < 0 || c->merged_adapter >= 0) continue;   // merged: the delta is inside the base GEMMs
     double r = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
     f += c->Ld * 2 * r * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
+    if (sd3) f -= 2 * r * Nt * ((D + D) + (D + F) + (F + D));
     f += c->Ls * 2 * r * N * ((D + 3 * D + F) + (D + F + D));
   }
   return f;
@@ -1078,12 +1172,26 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   if (!c) return DIT_EINVAL;
   if (!b) return c->fail(DIT_EINVAL, "batch is NULL");
   if (!c->weights_ready) return c->fail(DIT_ENOWEIGHTS, "base weights not (fully) loaded");
-  const int B = b->batch;
+  const int B = b->batch;   // requests
   if (B < 1 || B > c->cfg.max_batch) return c->fail(DIT_EBATCH, "batch %d not in [1, %d]", B, c->cfg.max_batch);
+  // classifier-free guidance (reading C22): S sequences run here -- 2B (cond, then uncond)
+  // on one GPU, B (this rank's branch) under latent parallelism
+  const bool cfgon = b->cfg_scale != nullptr;
+  const bool lpar = c->lp_world > 1;   // latent parallelism
+  if (lpar && !cfgon) return c->fail(DIT_EINVAL, "latent parallelism (lp_init) needs cfg_scale");
+  const int S = (cfgon && !lpar) ? 2 * B : B;
+  if (S > c->cfg.max_batch)
+    return c->fail(DIT_EBATCH, "CFG doubles the batch: %d sequences > B_max %d", S, c->cfg.max_batch);
+  if (cfgon)
+    for (int i = 0; i < B; ++i)
+      if (!std::isfinite(b->cfg_scale[i])) return c->fail(DIT_EINVAL, "cfg_scale[%d] is not finite", i);
   if (b->img_h < 1 || b->img_w < 1 || b->txt_tokens < 1) return c->fail(DIT_ESHAPE, "empty token grid");
   const int Ni = b->img_h * b->img_w, Nt = b->txt_tokens;
   if (Ni > c->cfg.max_img_tokens || Nt > c->cfg.max_txt_tokens)
     return c->fail(DIT_ESHAPE, "tokens (%d img, %d txt) exceed the configured maxima", Ni, Nt);
+  if (c->cfg.arch == DIT_ARCH_SD3 && (b->img_h > c->cfg.pos_embed_max || b->img_w > c->cfg.pos_embed_max))
+    return c->fail(DIT_ESHAPE, "token grid %dx%d exceeds the %d^2 position table", b->img_h, b->img_w,
+                   c->cfg.pos_embed_max);
   const int P = c->world;
   if (Ni % P || Nt % P) return c->fail(DIT_EPARALLEL, "world %d does not divide Ni=%d / Nt=%d", P, Ni, Nt);
   if (P > 1 && !c->comm && !c->local_group) return c->fail(DIT_EPARALLEL, "sp_init not called");
@@ -1097,9 +1205,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     if (a0 < b0 + lat_bytes && b0 < a0 + lat_bytes) return c->fail(DIT_EALIAS, "latents_out aliases latents_in");
   }
   if ((reinterpret_cast<uintptr_t>(b->txt) & 15)) return c->fail(DIT_EINVAL, "txt must be 16-byte aligned");
-  std::vector<int> req_slot(B, -1);
-  for (int i = 0; i < B; ++i) {
-    const int aid = b->adapter_id[i];
+  std::vector<int> req_slot(S, -1);   // pool slot of every sequence
+  for (int i = 0; i < S; ++i) {
+    const int aid = b->adapter_id[i % B];
     if (c->merged_adapter >= 0) {   // patched replica: specialised to its adapter
       if (aid != c->merged_adapter)
         return c->fail(DIT_EADAPTER, "adapter %d is merged; request %d uses %d", c->merged_adapter, i, aid);
@@ -1111,7 +1219,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     req_slot[i] = it->second;
   }
   for (auto& kv : c->cn)
-    if (kv.first.first >= B) return c->fail(DIT_EINVAL, "ControlNet registered for slot %d >= batch %d", kv.first.first, B);
+    if (kv.first.first >= S) return c->fail(DIT_EINVAL, "ControlNet registered for slot %d >= sequences %d", kv.first.first, S);
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
@@ -1122,12 +1230,12 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   c->launches = 0;
   const int D = c->D, H = c->H, d = c->d, F = c->F, C = c->C, Ct = c->Ct;
   const int nt = Nt / P, ni = Ni / P, N = nt + ni;
-  const int Mt = B * nt, Mi = B * ni, Mj = B * N;
+  const int Mt = S * nt, Mi = S * ni, Mj = S * N;
 
   // ---- plan (cached by shape + adapter slots)
   bool any_lora = false;
-  for (int i = 0; i < B; ++i) any_lora |= req_slot[i] >= 0;
-  if (c->plan_B != B || c->plan_h != b->img_h || c->plan_w != b->img_w || c->plan_nt != Nt || c->plan_slots != req_slot) {
+  for (int i = 0; i < S; ++i) any_lora |= req_slot[i] >= 0;
+  if (c->plan_B != S || c->plan_h != b->img_h || c->plan_w != b->img_w || c->plan_nt != Nt || c->plan_slots != req_slot) {
     std::vector<int> ht, hc;
     std::vector<int2> hs;
     const int Ms[3] = {Mt, Mi, Mj}, rpr[3] = {nt, ni, N};
@@ -1141,28 +1249,35 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     }
     if (!any_lora)
       for (int r = 0; r < 3; ++r) c->rs[r].n_shrink = 0;
-    c->plan_B = B;
+    c->plan_B = S;
     c->plan_h = b->img_h;
     c->plan_w = b->img_w;
     c->plan_nt = Nt;
     c->plan_slots = req_slot;
   }
   if (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w) {
-    CKC(rope_table_launch(c->rope, nt, ni, c->rank * nt, c->rank * ni, b->img_w, c->cfg.rope_axes[0],
-                          c->cfg.rope_axes[1], c->cfg.rope_axes[2], c->cfg.rope_theta, s));
+    if (c->cfg.arch == DIT_ARCH_SD3)   // no RoPE: the QKV epilogue rotates by angle 0 (exact identity)
+      CKC(rope_table_launch(c->rope, nt, ni, 0, 0, 1, 0, 0, d, 1.f, s));   // theta 1, width 1: angle 0
+    else
+      CKC(rope_table_launch(c->rope, nt, ni, c->rank * nt, c->rank * ni, b->img_w, c->cfg.rope_axes[0],
+                            c->cfg.rope_axes[1], c->cfg.rope_axes[2], c->cfg.rope_theta, s));
     c->rope_key[0] = nt;
     c->rope_key[1] = ni;
     c->rope_key[2] = b->img_w;
   }
   // ---- per-step parameter block (pageable source: safe to reuse after return)
   {
-    std::vector<float> pf(8 * 4 + 64, 0.f);
-    for (int i = 0; i < B; ++i) {
-      pf[i] = b->sigma_next[i] - b->sigma[i];
-      pf[8 + i] = b->cn_scale ? b->cn_scale[i] : 1.f;
-      pf[16 + i] = b->sigma[i];
-      pf[24 + i] = b->guidance[i];
+    // per SEQUENCE (CFG: sequence q belongs to request q % B), CFG scale per request
+    std::vector<float> pf(8 * 5 + 64, 0.f);
+    for (int q = 0; q < S; ++q) {
+      const int i = q % B;
+      pf[q] = b->sigma_next[i] - b->sigma[i];
+      pf[8 + q] = b->cn_scale ? b->cn_scale[i] : 1.f;
+      pf[16 + q] = b->sigma[i];
+      pf[24 + q] = b->guidance[i];
     }
+    for (int i = 0; i < B && cfgon; ++i) pf[32 + i] = b->cfg_scale[i];
+    cudaMemcpyAsync(c->p_cfg, pf.data() + 32, 8 * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(c->p_dsig, pf.data(), 8 * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(c->p_cn_scale, pf.data() + 8, 8 * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(c->p_sigma, pf.data() + 16, 8 * 4, cudaMemcpyHostToDevice, s);
@@ -1183,7 +1298,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         for (size_t k = 0; k < kv.second.size(); ++k) {
           const size_t at = ((size_t)kv.first.second * CN_FANIN + k) * 8 + kv.first.first;
           cp[at] = kv.second[k].ptr;
-          kap[at] = kv.second[k].scale * (b->cn_scale ? b->cn_scale[kv.first.first] : 1.f);
+          kap[at] = kv.second[k].scale * (b->cn_scale ? b->cn_scale[kv.first.first % B] : 1.f);
           fl[at] = kv.second[k].flag;
           ex[at] = kv.second[k].expect;
           c->cn_flags |= kv.second[k].flag != nullptr;
@@ -1223,27 +1338,29 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
 
   // ---- conditioning vec (tail segments nsegs+0..5) and all modulations (one launch)
   SkinnySeg* cs = c->segs + c->nsegs;
-  CKC(temb_launch(c->p_sigma, B, c->temb, s));
-  CKC(skinny_launch(c->temb, 256, cs + 0, 1, D, c->h1, D, B, 0, s));
-  CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
-  CKC(skinny_launch(c->xprep, D, cs + 1, 1, D, c->vec, D, B, 0, s));
+  CKC(temb_launch(c->p_sigma, S, c->temb, s));
+  CKC(skinny_launch(c->temb, 256, cs + 0, 1, D, c->h1, D, S, 0, s));
+  CKC(prep_x_launch(c->h1, S, D, 1, c->xprep, s));
+  CKC(skinny_launch(c->xprep, D, cs + 1, 1, D, c->vec, D, S, 0, s));
   if (c->cfg.guidance_embed) {
-    CKC(temb_launch(c->p_guid, B, c->temb, s));
-    CKC(skinny_launch(c->temb, 256, cs + 2, 1, D, c->h1, D, B, 0, s));
-    CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
-    CKC(skinny_launch(c->xprep, D, cs + 3, 1, D, c->vec, D, B, 1, s));
+    CKC(temb_launch(c->p_guid, S, c->temb, s));
+    CKC(skinny_launch(c->temb, 256, cs + 2, 1, D, c->h1, D, S, 0, s));
+    CKC(prep_x_launch(c->h1, S, D, 1, c->xprep, s));
+    CKC(skinny_launch(c->xprep, D, cs + 3, 1, D, c->vec, D, S, 1, s));
   }
   cudaMemsetAsync(c->xprep, 0, (size_t)8 * c->Cp * 2, s);
-  cudaMemcpyAsync(c->xprep, b->pooled, (size_t)B * c->Cp * 2, cudaMemcpyDeviceToDevice, s);
-  CKC(skinny_launch(c->xprep, c->Cp, cs + 4, 1, D, c->h1, D, B, 0, s));
-  CKC(prep_x_launch(c->h1, B, D, 1, c->xprep, s));
-  CKC(skinny_launch(c->xprep, D, cs + 5, 1, D, c->vec, D, B, 1, s));
-  CKC(prep_x_launch(c->vec, B, D, 1, c->xprep, s));
-  CKK(skinny_launch(c->xprep, D, c->segs, c->nsegs, c->seg_rows, c->mod, c->mod_total, B, 0, s), 3,
-      2.0 * B * (double)c->seg_rows * D);
+  cudaMemcpyAsync(c->xprep, b->pooled, (size_t)S * c->Cp * 2, cudaMemcpyDeviceToDevice, s);
+  CKC(skinny_launch(c->xprep, c->Cp, cs + 4, 1, D, c->h1, D, S, 0, s));
+  CKC(prep_x_launch(c->h1, S, D, 1, c->xprep, s));
+  CKC(skinny_launch(c->xprep, D, cs + 5, 1, D, c->vec, D, S, 1, s));
+  CKC(prep_x_launch(c->vec, S, D, 1, c->xprep, s));
+  CKK(skinny_launch(c->xprep, D, c->segs, c->nsegs, c->seg_rows, c->mod, c->mod_total, S, 0, s), 3,
+      2.0 * S * (double)c->seg_rows * D);
 
-  // ---- embeddings into the fp32 residual stream h [B][N][D] (txt rows first)
-  CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)Mi * C, s));
+  // ---- embeddings into the fp32 residual stream h [S][N][D] (txt rows first)
+  CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)B * ni * C, s));
+  if (S > B)   // CFG on one GPU: both branches denoise the same latents
+    cudaMemcpyAsync(c->xb + (size_t)B * ni * C, c->xb, (size_t)B * ni * C * 2, cudaMemcpyDeviceToDevice, s);
   {
     EpiParams ei;
     memset(&ei, 0, sizeof(ei));
@@ -1263,11 +1380,14 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     c->gemm_label = 10;
     CK(run_gemm(c, p, 2, s));
   }
+  if (c->cfg.arch == DIT_ARCH_SD3)   // SD3 position table on the image rows (reading C21)
+    CKC(pos_embed_add_launch(c->h, S, N, nt, ni, c->rank * ni, b->img_h, b->img_w, D, c->cfg.pos_embed_max,
+                             c->cfg.pos_embed_base, s));
 
   const float scale_log2 = 1.4426950408889634f / std::sqrt((float)d);
   // ---- attention with the Ulysses exchange around it (P > 1): QKV epilogue wrote
-  // [P][3][B][H/P][N_loc][d] -> a2a -> global order -> attention on H/P heads over the
-  // full sequence -> O in [P][B][N_loc][H/P*d] -> a2a -> scatter into the local rows.
+  // [P][3][S][H/P][N_loc][d] -> a2a -> global order -> attention on H/P heads over the
+  // full sequence -> O in [P][S][N_loc][H/P*d] -> a2a -> scatter into the local rows.
   const int Hl = H / P, Nglob = P * N;
   const bool sp = P > 1 || c->force_sp;   // Ulysses exchange active
   auto a2a = [&](const void* snd, void* rcv, size_t count) -> int {
@@ -1283,22 +1403,22 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     return DIT_OK;
   };
   auto attention_stage = [&](void* out, int ld_out, int split) -> int {
-    const size_t pp1 = (size_t)3 * B * Hl * N * d, pp2 = (size_t)B * N * Hl * d;
+    const size_t pp1 = (size_t)3 * S * Hl * N * d, pp2 = (size_t)S * N * Hl * d;
     bf16_t* send1 = c->sp;
     bf16_t* recv1 = send1 + (size_t)P * pp1;
     bf16_t* send2 = recv1 + (size_t)P * pp1;
     bf16_t* recv2 = send2 + (size_t)P * pp2;
     if (sp) {
       CK(a2a(send1, recv1, pp1));
-      CKK(sp_gather_qkv_launch(recv1, c->qkv, P, B, Hl, nt, ni, d, s), 6, 0.0);
+      CKK(sp_gather_qkv_launch(recv1, c->qkv, P, S, Hl, nt, ni, d, s), 6, 0.0);
     }
     AttnParams ap;
     memset(&ap, 0, sizeof(ap));
-    const size_t sec = (size_t)B * Hl * Nglob * d;
+    const size_t sec = (size_t)S * Hl * Nglob * d;
     ap.q = c->qkv;
     ap.k = c->qkv + sec;
     ap.v = c->qkv + 2 * sec;
-    ap.B = B;
+    ap.B = S;
     ap.H = Hl;
     ap.N = Nglob;
     ap.d = d;
@@ -1315,14 +1435,16 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       ap.ld_out = Hl * d;
       ap.split = 2;
     }
-    CKK(attention_launch(ap, s), 1, 4.0 * B * (double)Nglob * Nglob * Hl * d);
+    CKK(attention_launch(ap, s), 1, 4.0 * S * (double)Nglob * Nglob * Hl * d);
     if (sp) {
       CK(a2a(send2, recv2, pp2));
-      CKK(sp_scatter_o_launch(recv2, out, ld_out, split, P, B, Hl, nt, ni, d, s), 6, 0.0);
+      CKK(sp_scatter_o_launch(recv2, out, ld_out, split, P, S, Hl, nt, ni, d, s), 6, 0.0);
     }
     return DIT_OK;
   };
-  auto lnmod2 = [&](int modT, int modI, int sh, int sc) -> int {
+  // LN-modulate of the txt and/or img stream; shift / scale given as absolute mod columns
+  // (txt_on = false: image stream only -- after SD3's context_pre_only attention)
+  auto lnmod_st = [&](bool txt_on, int shT, int scT, int shI, int scI) -> int {
     LnModParams lp;
     memset(&lp, 0, sizeof(lp));
     lp.h = c->h;
@@ -1337,24 +1459,37 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     lp.seg_rows_per_req[1] = ni;
     lp.seg_joint_off[0] = 0;
     lp.seg_joint_off[1] = nt;
-    lp.seg_shift_off[0] = modT + sh;
-    lp.seg_scale_off[0] = modT + sc;
-    lp.seg_shift_off[1] = modI + sh;
-    lp.seg_scale_off[1] = modI + sc;
+    lp.seg_shift_off[0] = shT;
+    lp.seg_scale_off[0] = scT;
+    lp.seg_shift_off[1] = shI;
+    lp.seg_scale_off[1] = scI;
     lp.seg_mod[0] = lp.seg_mod[1] = c->mod;
+    if (!txt_on) {   // the image segment alone, written at its usual place (after the txt rows)
+      lp.u = c->u + (size_t)Mt * D;
+      lp.nseg = 1;
+      lp.seg_rows[0] = Mi;
+      lp.seg_rows_per_req[0] = ni;
+      lp.seg_joint_off[0] = nt;
+      lp.seg_shift_off[0] = shI;
+      lp.seg_scale_off[0] = scI;
+    }
     prof_begin(c, s);
     cudaError_t e = lnmod_launch(lp, s);
     prof_end(c, s, 2, 0.0);
     c->launches++;
     return e == cudaSuccess ? DIT_OK : c->fail(DIT_ECUDA, "lnmod: %s", cudaGetErrorString(e));
   };
-  auto shrink2 = [&](const void* At, const void* Ai, int K, int lda, int modT, int modI) -> int {
+  auto lnmod2 = [&](int modT, int modI, int sh, int sc) -> int {
+    return lnmod_st(true, modT + sh, modT + sc, modI + sh, modI + sc);
+  };
+  auto shrink2 = [&](const void* At, const void* Ai, int K, int lda, int modT, int modI, bool txt_on = true) -> int {
     if (!any_lora) return DIT_OK;
     const void* A[2] = {At, Ai};
     const int M[2] = {Mt, Mi}, Ks[2] = {K, K}, ld[2] = {lda, lda};
     const RowSpace* R[2] = {&c->rs[0], &c->rs[1]};
     const int mods[2] = {modT, modI};
     const int base[2] = {0, Mt};
+    if (!txt_on) return run_shrink(c, 1, A + 1, M + 1, Ks + 1, ld + 1, R + 1, mods + 1, base + 1, s);
     return run_shrink(c, 2, A, M, Ks, ld, R, mods, base, s);
   };
 
@@ -1378,7 +1513,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     const int mI = (i * 2 + 0) * 6 * D, mT = (i * 2 + 1) * 6 * D;
     bf16_t* uT = c->u;
     bf16_t* uI = c->u + (size_t)Mt * D;
-    CK(lnmod2(mT, mI, 0, D));
+    // SD3 last block: the text stream is context_pre_only -- (scale, shift) modulation, then it
+    // only feeds attention (reading C21)
+    const bool po = pre_only(c->cfg, i, 1);
+    if (po) CK(lnmod_st(true, mT + D, mT, mI, mI + D));
+    else CK(lnmod2(mT, mI, 0, D));
     CK(shrink2(uT, uI, D, D, T.lora[0], I.lora[0]));
     {
       EpiParams e;
@@ -1387,7 +1526,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.joint_n = N;
       e.D = D;
       e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
-      e.batch = B;
+      e.batch = S;
       e.sp_world = P;
       e.rope = c->rope;
       e.qkv_cols = 3 * D;
@@ -1450,12 +1589,13 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         add_lora_ext(c, p[1], c->rs[1], modI_l, sext_of(c, Mt));
       }
       c->gemm_label = goff == 2 * D ? 12 : 14;
+      if (po) return run_gemm(c, p + 1, 1, s);   // context_pre_only: image stream only
       return run_gemm(c, p, 2, s);
     };
-    CK(shrink2(oT, oI, D, D, T.lora[1], I.lora[1]));
+    CK(shrink2(oT, oI, D, D, T.lora[1], I.lora[1], !po));
     CK(resid_pair(T.proj, I.proj, oT, oI, D, D, 2 * D, T.lora[1], I.lora[1], nullptr));
-    CK(lnmod2(mT, mI, 3 * D, 4 * D));
-    CK(shrink2(uT, uI, D, D, T.lora[2], I.lora[2]));
+    CK(lnmod_st(!po, mT + 3 * D, mT + 4 * D, mI + 3 * D, mI + 4 * D));
+    CK(shrink2(uT, uI, D, D, T.lora[2], I.lora[2], !po));
     bf16_t* aT = c->cat;
     bf16_t* aI = c->cat + (size_t)Mt * F;
     {
@@ -1478,18 +1618,19 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         add_lora_ext(c, p[1], c->rs[1], I.lora[2], sext_of(c, Mt));
       }
       c->gemm_label = 13;
-      CK(run_gemm(c, p, 2, s));
+      if (po) CK(run_gemm(c, p + 1, 1, s));
+      else CK(run_gemm(c, p, 2, s));
     }
     // deferred ControlNet input of block i: wait right before its consumer
     const bool has_cn = cn_wait(i);
-    CK(shrink2(aT, aI, F, F, T.lora[3], I.lora[3]));
+    CK(shrink2(aT, aI, F, F, T.lora[3], I.lora[3], !po));
     CK(resid_pair(T.fc2, I.fc2, aT, aI, F, F, 5 * D, T.lora[3], I.lora[3],
                   has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * CN_FANIN * 8) : nullptr));
   }
 
   // ---- single-stream blocks on the joint sequence
   for (int j = 0; j < c->Ls; ++j) {
-    const SingleBlk& S = c->sgl[j];
+    const SingleBlk& SB = c->sgl[j];
     const int mj = mod_off_single + j * 3 * D;
     {
       LnModParams lp;
@@ -1512,7 +1653,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       const void* A[1] = {c->u};
       const int M[1] = {Mj}, K[1] = {D}, ld[1] = {D};
       const RowSpace* R[1] = {&c->rs[2]};
-      const int mods[1] = {S.lora[0]};
+      const int mods[1] = {SB.lora[0]};
       const int base[1] = {0};
       CK(run_shrink(c, 1, A, M, K, ld, R, mods, base, s));
     }
@@ -1520,16 +1661,16 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       EpiParams e;
       memset(&e, 0, sizeof(e));
       e.kind = EPI_QKV;
-      e.bias = S.l1.b;
+      e.bias = SB.l1.b;
       e.rows_per_req = N;
       e.joint_off = 0;
       e.joint_n = N;
       e.D = D;
       e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
-      e.batch = B;
+      e.batch = S;
       e.sp_world = P;
-      e.q_gamma = S.qn;
-      e.k_gamma = S.kn;
+      e.q_gamma = SB.qn;
+      e.k_gamma = SB.kn;
       e.rope = c->rope;
       e.qkv_cols = 3 * D;
       e.heads = H;
@@ -1538,8 +1679,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.out = c->cat;
       e.ld_out = D + F;
       e.out_col0 = D;
-      GemmProblem p = base_problem(c, c->u, Mj, D, D, S.l1, e);
-      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[0], sext_of(c, 0));
+      GemmProblem p = base_problem(c, c->u, Mj, D, D, SB.l1, e);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], SB.lora[0], sext_of(c, 0));
       c->gemm_label = 15;
       CK(run_gemm(c, &p, 1, s));
     }
@@ -1548,7 +1689,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       const void* A[1] = {c->cat};
       const int M[1] = {Mj}, K[1] = {D + F}, ld[1] = {D + F};
       const RowSpace* R[1] = {&c->rs[2]};
-      const int mods[1] = {S.lora[1]};
+      const int mods[1] = {SB.lora[1]};
       const int base[1] = {0};
       CK(run_shrink(c, 1, A, M, K, ld, R, mods, base, s));
     }
@@ -1556,7 +1697,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       EpiParams e;
       memset(&e, 0, sizeof(e));
       e.kind = EPI_RESID;
-      e.bias = S.l2.b;
+      e.bias = SB.l2.b;
       e.rows_per_req = N;
       e.joint_off = 0;
       e.joint_n = N;
@@ -1574,8 +1715,8 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
           e.cn_expect = c->p_cn_expect + (size_t)(c->Ld + j) * CN_FANIN * 8;
         }
       }
-      GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, S.l2, e);
-      if (any_lora) add_lora_ext(c, p, c->rs[2], S.lora[1], sext_of(c, 0));
+      GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, SB.l2, e);
+      if (any_lora) add_lora_ext(c, p, c->rs[2], SB.lora[1], sext_of(c, 0));
       c->gemm_label = 16;
       CK(run_gemm(c, &p, 1, s));
     }
@@ -1594,8 +1735,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     lp.seg_rows[0] = Mi;
     lp.seg_rows_per_req[0] = ni;
     lp.seg_joint_off[0] = nt;
-    lp.seg_shift_off[0] = mod_off_final;
-    lp.seg_scale_off[0] = mod_off_final + D;
+    // Flux LastLayer (shift, scale); SD3 AdaLayerNormContinuous (scale, shift) [ext]
+    const bool sd3 = c->cfg.arch == DIT_ARCH_SD3;
+    lp.seg_shift_off[0] = mod_off_final + (sd3 ? D : 0);
+    lp.seg_scale_off[0] = mod_off_final + (sd3 ? 0 : D);
     lp.seg_mod[0] = c->mod;
     CKK(lnmod_launch(lp, s), 2, 0.0);
     EpiParams e;
@@ -1608,12 +1751,33 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     e.lat_out = b->latents_out;
     e.v_out = b->v_out;
     e.dsig = c->p_dsig;
+    const size_t vcount = (size_t)B * ni * C;   // one branch's v
+    if (cfgon) {   // v of every sequence into vcfg [cond B | uncond B]; Euler after the combine
+      e.lat_in = nullptr;
+      e.lat_out = nullptr;
+      e.v_out = c->vcfg + (lpar ? (size_t)c->lp_rank * vcount : 0);
+    }
     GemmProblem p = base_problem(c, c->u, Mi, D, D, c->fin_lin, e);
     c->gemm_label = 17;
     CK(run_gemm(c, &p, 1, s));
+    if (lpar) {   // latent parallelism: per-step gather of the two branches' v
+      prof_begin(c, s);
+      if (c->lp_comm) {
+        ncclResult_t r = ncclAllGather(c->vcfg + (size_t)c->lp_rank * vcount, c->vcfg, vcount, ncclFloat32,
+                                       c->lp_comm, s);
+        if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+      } else {
+        c->lp_group->allgather(c->lp_rank, c->vcfg, vcount * 4, s);
+      }
+      prof_end(c, s, 5, 0.0);
+      c->launches++;
+    }
+    if (cfgon)   // v = v_u + g (v_c - v_u); latents_out = latents_in + dsig v (reading C22)
+      CKC(cfg_euler_launch(c->vcfg, c->vcfg + vcount, c->p_cfg, c->p_dsig, b->latents_in, b->latents_out, b->v_out,
+                           B, ni * C, s));
   }
 
-  for (int i = 0; i < B; ++i)
+  for (int i = 0; i < S; ++i)
     if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
   c->cn.clear();
   c->last_launches = c->launches;

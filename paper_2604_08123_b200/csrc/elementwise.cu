@@ -569,4 +569,74 @@ cudaError_t fill_synthetic_launch(void* dst, int64_t n, uint64_t seed, uint64_t 
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ SD3 position table (reading C21)
+// h[q][nt + i][c] += table[n][c] for every sequence q < S, n = ni_off + i the global image token.
+// One thread per (token, frequency k < D/4, axis): sincos in fp64 (the argument reaches 64 rad),
+// added to the S sequences' rows (the table is sequence-independent).  Channels [0, D/2) take the
+// column coordinate, [D/2, D) the row; within a half [sin(p w_k) | cos(p w_k)], w_k = 1e4^(-k/(D/4)).
+__global__ void pos_embed_add_kernel(float* __restrict__ h, int S, int N, int nt, int ni, int ni_off, int img_h,
+                                     int img_w, int D, int pe_max, int base) {
+  const int q4 = D / 4;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)ni * 2 * q4) return;
+  const int k = (int)(t % q4);
+  const int axis = (int)((t / q4) % 2);
+  const int i = (int)(t / (2 * q4));
+  const int n = ni_off + i;
+  const int top = (pe_max - img_h) / 2, left = (pe_max - img_w) / 2;
+  const double p = (double)(axis == 0 ? left + n % img_w : top + n / img_w) * (double)base / (double)pe_max;
+  const double ang = p * pow(10000.0, -(double)k / (double)q4);
+  double sv, cv;
+  sincos(ang, &sv, &cv);
+  const float sf = (float)sv, cf = (float)cv;
+  for (int q = 0; q < S; ++q) {
+    float* row = h + ((size_t)q * N + nt + i) * D + axis * (D / 2);
+    row[k] += sf;
+    row[q4 + k] += cf;
+  }
+}
+cudaError_t pos_embed_add_launch(float* h, int S, int N, int nt, int ni, int ni_off, int img_h, int img_w, int D,
+                                 int pe_max, int base, cudaStream_t s) {
+  const long long n = (long long)ni * (D / 2);
+  if (n <= 0) return cudaSuccess;
+  pos_embed_add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h, S, N, nt, ni, ni_off, img_h, img_w, D, pe_max,
+                                                                    base);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ CFG combine + Euler (reading C22)
+// v = vu + g_b (vc - vu); lat_out = lat_in + dsig_b v; v_out = v (optional).  Per request b:
+// count = Ni_loc * C contiguous fp32 (count % 4 == 0), float4 granules.
+__global__ void cfg_euler_kernel(const float4* __restrict__ vc, const float4* __restrict__ vu,
+                                 const float* __restrict__ g, const float* __restrict__ dsig,
+                                 const float4* __restrict__ lat_in, float4* __restrict__ lat_out,
+                                 float4* __restrict__ v_out, int B, int count4) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)B * count4) return;
+  const int b = (int)(t / count4);
+  const float gb = g[b], ds = dsig[b];
+  const float4 c = vc[t], u = vu[t], x = lat_in[t];
+  float4 v, o;
+  v.x = u.x + gb * (c.x - u.x);
+  v.y = u.y + gb * (c.y - u.y);
+  v.z = u.z + gb * (c.z - u.z);
+  v.w = u.w + gb * (c.w - u.w);
+  o.x = x.x + ds * v.x;
+  o.y = x.y + ds * v.y;
+  o.z = x.z + ds * v.z;
+  o.w = x.w + ds * v.w;
+  lat_out[t] = o;
+  if (v_out != nullptr) v_out[t] = v;
+}
+cudaError_t cfg_euler_launch(const float* vc, const float* vu, const float* g, const float* dsig, const float* lat_in,
+                             float* lat_out, float* v_out, int B, int count, cudaStream_t s) {
+  const long long n = (long long)B * (count / 4);
+  if (n <= 0) return cudaSuccess;
+  cfg_euler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const float4*>(vc), reinterpret_cast<const float4*>(vu), g, dsig,
+      reinterpret_cast<const float4*>(lat_in), reinterpret_cast<float4*>(lat_out), reinterpret_cast<float4*>(v_out), B,
+      count / 4);
+  return cudaGetLastError();
+}
 }  // namespace dit

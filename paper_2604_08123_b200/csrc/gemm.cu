@@ -221,11 +221,12 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         const int dest = head / hl_n, hl = head - dest * hl_n;
         bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
                     (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
+        const bool nrm = sec < 2 && E.q_gamma != nullptr;   // SD3-medium: no QK-norm (RoPE table = identity)
         if (d == 128) {
           // head in two 64-column halves: half 0 read for the RMS statistic, half 1 read and
           // kept, processed, then half 0 re-read and processed (3 TMEM reads instead of 8)
           float ss = 0.f;
-          if (sec < 2) {
+          if (nrm) {
             float y[64];
             load_head_half(tbase + c0, bias + col0, y);
 #pragma unroll
@@ -234,20 +235,20 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           float y[64];
           load_head_half(tbase + c0 + 64, bias + col0 + 64, y);   // (tcgen05.ld: all lanes)
           float rs = 1.f;
-          if (sec < 2) {
+          if (nrm) {
 #pragma unroll
             for (int e = 0; e < 64; ++e) ss = fmaf(y[e], y[e], ss);
             rs = rsqrtf(ss / (float)d + 1e-6f);
           }
           const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
           const float4* cs = reinterpret_cast<const float4*>(E.rope + (size_t)(E.joint_off + nloc) * (d / 2));
-          if (sec < 2) norm_rope_half(y, rs, g + 64, cs + 16);
+          if (nrm) norm_rope_half(y, rs, g + 64, cs + 16);
           if (row_ok) {
 #pragma unroll
             for (int j = 0; j < 64; j += 32) store_bf16_32(dst + 64 + j, *reinterpret_cast<const float(*)[32]>(&y[j]), 32);
           }
           load_head_half(tbase + c0, bias + col0, y);
-          if (sec < 2) norm_rope_half(y, rs, g, cs);
+          if (nrm) norm_rope_half(y, rs, g, cs);
           if (row_ok) {
 #pragma unroll
             for (int j = 0; j < 64; j += 32) store_bf16_32(dst + j, *reinterpret_cast<const float(*)[32]>(&y[j]), 32);
@@ -257,7 +258,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         // generic head size (d = 32 / 64 test configurations): two passes of 32 columns
         // pass 1: sum of squares over the head (q, k only)
         float rs = 1.f;
-        if (sec < 2) {
+        if (nrm) {
           float ss = 0.f;
 #pragma unroll 1
           for (int j = 0; j < d; j += 32) {
@@ -286,7 +287,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           load_bias32(bias, col0 + j, P.N, bv);
 #pragma unroll
           for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr[e]) + bv[e];
-          if (sec < 2 && row_ok) {
+          if (nrm && row_ok) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const float x0 = y[2 * e] * rs * __bfloat162float(g[j + 2 * e]);
@@ -422,7 +423,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
       for (int e = 0; e < 32; ++e) {
         if (e < valid) {
           const size_t off = (size_t)r * P.N + col + e;
-          E.lat_out[off] = E.lat_in[off] + ds * y[e];
+          if (E.lat_out != nullptr) E.lat_out[off] = E.lat_in[off] + ds * y[e];   // (CFG: Euler after the combine)
           if (E.v_out != nullptr) E.v_out[off] = y[e];
         }
       }

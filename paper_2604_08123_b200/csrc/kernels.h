@@ -217,6 +217,13 @@ cudaError_t temb_launch(const float* vals, int B, void* out, cudaStream_t s);
 // rope table [n_rows][d/2] float2 from (Nt, img_w, first global joint row ...).
 cudaError_t rope_table_launch(float2* tab, int nt_loc, int ni_loc, int nt_off, int ni_off, int img_w,
                               int a0, int a1, int a2, float theta, cudaStream_t s);
+// SD3 2-D sincos position table added to the image rows of h [S][N][D] (reading C21).
+cudaError_t pos_embed_add_launch(float* h, int S, int N, int nt, int ni, int ni_off, int img_h, int img_w, int D,
+                                 int pe_max, int base, cudaStream_t s);
+// CFG combine + Euler: v = vu + g_b (vc - vu), lat_out = lat_in + dsig_b v, v_out = v (nullable);
+// per request b < B, count = Ni_loc * C fp32 (multiple of 4).
+cudaError_t cfg_euler_launch(const float* vc, const float* vu, const float* g, const float* dsig, const float* lat_in,
+                             float* lat_out, float* v_out, int B, int count, cudaStream_t s);
 // x fp32 [n] -> bf16
 cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t s);
 cudaError_t fill_synthetic_launch(void* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset,

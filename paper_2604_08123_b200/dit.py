@@ -27,7 +27,11 @@ class dit_config(C.Structure):
                 ("pooled_dim", C.c_int32), ("mlp_ratio", C.c_int32), ("rope_axes", C.c_int32 * 3),
                 ("rope_theta", C.c_float), ("guidance_embed", C.c_int32), ("max_batch", C.c_int32),
                 ("max_img_tokens", C.c_int32), ("max_txt_tokens", C.c_int32), ("max_rank", C.c_int32),
-                ("max_adapters", C.c_int32)]
+                ("max_adapters", C.c_int32), ("arch", C.c_int32), ("qk_norm", C.c_int32),
+                ("pos_embed_max", C.c_int32), ("pos_embed_base", C.c_int32)]
+
+
+ARCH = {"flux": 0, "sd3": 1}
 
 
 class dit_tensor(C.Structure):
@@ -40,7 +44,8 @@ class dit_batch(C.Structure):
                 ("adapter_id", C.POINTER(C.c_int32)), ("sigma", C.POINTER(C.c_float)),
                 ("sigma_next", C.POINTER(C.c_float)), ("guidance", C.POINTER(C.c_float)),
                 ("cn_scale", C.POINTER(C.c_float)), ("latents_in", C.c_void_p), ("latents_out", C.c_void_p),
-                ("txt", C.c_void_p), ("pooled", C.c_void_p), ("v_out", C.c_void_p)]
+                ("txt", C.c_void_p), ("pooled", C.c_void_p), ("v_out", C.c_void_p),
+                ("cfg_scale", C.POINTER(C.c_float))]
 
 
 EXPORTS = {
@@ -61,6 +66,8 @@ EXPORTS = {
     "dit_debug_delayed_publish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_uint64,
                                             C.c_void_p]),
     "sp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "lp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "lp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
     "dit_last_launch_count": (C.c_int, [C.c_void_p]),
@@ -125,6 +132,10 @@ def make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_
     c.guidance_embed = int(cfg.guidance_embed)
     c.max_batch, c.max_img_tokens, c.max_txt_tokens = max_batch, max_img_tokens, max_txt_tokens
     c.max_rank, c.max_adapters = max_rank, max_adapters
+    c.arch = ARCH[getattr(cfg, "arch", "flux")]
+    c.qk_norm = int(getattr(cfg, "qk_norm", True))
+    c.pos_embed_max = getattr(cfg, "pos_embed_max", 192)
+    c.pos_embed_base = getattr(cfg, "pos_embed_base", 64)
     return c
 
 
@@ -226,8 +237,15 @@ class DiT:
     def sp_init_local(self, group, rank: int):
         _check(self.lib.sp_init_local(self.ctx, group, rank), self.ctx)
 
+    def lp_init(self, world: int, rank: int, nccl_uid: bytes):
+        buf = C.create_string_buffer(nccl_uid, 128)
+        _check(self.lib.lp_init(self.ctx, world, rank, buf), self.ctx)
+
+    def lp_init_local(self, group, rank: int):
+        _check(self.lib.lp_init_local(self.ctx, group, rank), self.ctx)
+
     def make_batch(self, batch_size, img_h, img_w, txt_tokens, adapter_id, sigma, sigma_next, guidance,
-                   latents_in, latents_out, txt, pooled, v_out=None, cn_scale=None) -> dit_batch:
+                   latents_in, latents_out, txt, pooled, v_out=None, cn_scale=None, cfg_scale=None) -> dit_batch:
         b = dit_batch()
         b.batch, b.img_h, b.img_w, b.txt_tokens = batch_size, img_h, img_w, txt_tokens
         keep = [_arr(C.c_int32, [int(x) for x in adapter_id]), _arr(C.c_float, [float(x) for x in sigma]),
@@ -237,6 +255,10 @@ class DiT:
             cs = _arr(C.c_float, [float(x) for x in cn_scale])
             keep.append(cs)
             b.cn_scale = cs
+        if cfg_scale is not None:
+            gs = _arr(C.c_float, [float(x) for x in cfg_scale])
+            keep.append(gs)
+            b.cfg_scale = gs
         b.latents_in, b.latents_out = latents_in.data_ptr(), latents_out.data_ptr()
         b.txt, b.pooled = txt.data_ptr(), pooled.data_ptr()
         b.v_out = v_out.data_ptr() if v_out is not None else None

@@ -46,18 +46,27 @@ class SyntheticDiT(DiT):
         self.lora_register(adapter_id, rank, scale, tens)
         torch.cuda.current_stream().synchronize()
 
-    def device_inputs(self, batch):
+    def device_inputs(self, batch, lp_rank: Optional[int] = None):
+        """Device copies of a synth.Batch.  CFG (batch.cfg_scale set): txt / pooled hold the
+        conditional rows then the unconditional rows ([2B]); under latent parallelism
+        (lp_rank given) only this rank's branch ([B]: rank 0 conditional, 1 unconditional)."""
         import torch
-        B = batch.batch
         lat = torch.from_numpy(np.ascontiguousarray(batch.latents, dtype=np.float32)).to(self.dev)
-        txt = _bits_to_bf16_tensor(batch.txt, self.dev)
-        pooled = _bits_to_bf16_tensor(batch.pooled, self.dev)
+        txt_bits, pooled_bits = batch.txt, batch.pooled
+        if batch.cfg_scale is not None:
+            if lp_rank is None:
+                txt_bits = np.concatenate([batch.txt, batch.txt_neg])
+                pooled_bits = np.concatenate([batch.pooled, batch.pooled_neg])
+            elif lp_rank == 1:
+                txt_bits, pooled_bits = batch.txt_neg, batch.pooled_neg
+        txt = _bits_to_bf16_tensor(txt_bits, self.dev)
+        pooled = _bits_to_bf16_tensor(pooled_bits, self.dev)
         out = torch.empty_like(lat)
         v = torch.empty_like(lat)
         return lat, txt, pooled, out, v
 
     def step(self, batch, controlnet: Optional[Dict[int, Dict[int, np.ndarray]]] = None, n_res: int = 0,
-             injections=None):
+             injections=None, lp_rank: Optional[int] = None, sync: bool = True):
         """Run one dit_step on a synth.Batch; returns (latents_out, v) as numpy fp32.
 
         controlnet: request b -> {double block i -> residual bf16 bits [Ni, D]} (one
@@ -66,7 +75,7 @@ class SyntheticDiT(DiT):
         counts double blocks then single blocks (controlnet_inject's numbering).
         """
         import torch
-        lat, txt, pooled, out, v = self.device_inputs(batch)
+        lat, txt, pooled, out, v = self.device_inputs(batch, lp_rank)
         if controlnet:
             for b, d in controlnet.items():
                 for blk, bits in d.items():
@@ -75,8 +84,10 @@ class SyntheticDiT(DiT):
             self.controlnet_inject(b, blk, _bits_to_bf16_tensor(bits, self.dev), sc)
         cb = self.make_batch(batch.batch, batch.img_h, batch.img_w, batch.txt_tokens, batch.adapter_id,
                              batch.sigma, batch.sigma_next, batch.guidance, lat, out, txt, pooled, v_out=v,
-                             cn_scale=batch.cn_scale)
+                             cn_scale=batch.cn_scale, cfg_scale=batch.cfg_scale)
         self.dit_step(cb)
+        if not sync:   # (latent-parallel tests: the peer rank's thread must also have enqueued)
+            return out, v
         torch.cuda.current_stream().synchronize()
         self._keep.clear()
         return out.cpu().numpy(), v.cpu().numpy()
