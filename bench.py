@@ -41,6 +41,15 @@ WORKLOADS = {
                               "re-registered every step)"),
     "cfg5": dict(B=1, h=128, w=128, nt=512, adapters=0, cn=False,
                  desc=_FLUX + "2048^2 (16384 img + 512 txt tokens), B=1"),
+    # SD3 family (the paper's settings S1/S2 serve SD3 and SD3.5-Large,
+    # PAPER.md:1330-1331): classifier-free guidance doubles every request; at --gpus 2 the two
+    # CFG branches run on separate GPUs (latent parallelism)
+    "sd3m": dict(B=4, h=64, w=64, nt=333, adapters=0, cn=False, model="SD3_MEDIUM", cfg=7.0,
+                 desc="SD3-medium-shaped 24 joint blocks, D=1536, 24x64 heads, 1024^2 (4096 img + 333 txt tokens), "
+                      "B=4 requests x CFG 7.0 (8 sequences)"),
+    "sd35l": dict(B=4, h=64, w=64, nt=333, adapters=0, cn=False, model="SD35_LARGE", cfg=3.5,
+                  desc="SD3.5-Large-shaped 38 joint blocks, D=2432, 38x64 heads, QK-RMSNorm, 1024^2 (4096 img + "
+                       "333 txt tokens), B=4 requests x CFG 3.5 (8 sequences)"),
 }
 WORKLOAD = WORKLOADS["cfg3"]["desc"]
 
@@ -239,28 +248,39 @@ def run_gpu(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = f"cuda:{local}"
-    cfg = synth.FLUX
     wl = WORKLOADS[args.workload]
+    cfg = getattr(synth, wl.get("model", "FLUX"))
     B, H_, W_, NT = wl["B"], wl["h"], wl["w"], wl["nt"]
     n_ad, rank_lora = wl["adapters"], 64
-    model = SyntheticDiT(cfg, max_batch=B, max_img_tokens=H_ * W_, max_txt_tokens=NT,
+    lp = wl.get("cfg") is not None and world > 1      # latent (CFG) parallelism: one branch per GPU
+    if lp and world != 2:
+        raise SystemExit(f"{args.workload}: latent parallelism runs on exactly 2 GPUs (got {world})")
+    seqs = 2 * B if (wl.get("cfg") is not None and not lp) else B
+    model = SyntheticDiT(cfg, max_batch=seqs, max_img_tokens=H_ * W_, max_txt_tokens=NT,
                          max_rank=rank_lora if n_ad else 0, max_adapters=n_ad, device=local)
     for a in range(n_ad):
         model.register_synthetic_lora(a, rank=rank_lora, index=a, scale=1.0)
-    if world > 1:
+    if lp:
+        import torch.distributed as dist
+        from paper_2604_08123_b200.dit import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        model.lp_init(world, rank, obj[0])
+    elif world > 1:
         # Ulysses SP (strong scaling): the SAME batch, tokens sharded over the ranks
         import torch.distributed as dist
         from paper_2604_08123_b200.dit import nccl_unique_id
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         model.sp_init(world, rank, obj[0])
-    batch = synth.make_batch(cfg, B, H_, W_, NT, n_adapters=n_ad)
-    nil, ntl = H_ * W_ // world, NT // world
-    batch.latents = np.ascontiguousarray(batch.latents[:, rank * nil:(rank + 1) * nil])
-    batch.txt = np.ascontiguousarray(batch.txt[:, rank * ntl:(rank + 1) * ntl])
-    lat, txt, pooled, out, v = model.device_inputs(batch)
+    batch = synth.make_batch(cfg, B, H_, W_, NT, n_adapters=n_ad, cfg_scale=wl.get("cfg"))
+    sp_world = 1 if lp else world
+    nil, ntl = H_ * W_ // sp_world, NT // sp_world
+    batch.latents = np.ascontiguousarray(batch.latents[:, rank * nil:(rank + 1) * nil]) if sp_world > 1 else batch.latents
+    batch.txt = np.ascontiguousarray(batch.txt[:, rank * ntl:(rank + 1) * ntl]) if sp_world > 1 else batch.txt
+    lat, txt, pooled, out, v = model.device_inputs(batch, lp_rank=rank if lp else None)
     cb = model.make_batch(B, H_, W_, NT, batch.adapter_id, batch.sigma, batch.sigma_next, batch.guidance,
-                          lat, out, txt, pooled, v_out=None, cn_scale=batch.cn_scale)
+                          lat, out, txt, pooled, v_out=None, cn_scale=batch.cn_scale, cfg_scale=batch.cfg_scale)
     residuals = None
     if wl["cn"]:
         from paper_2604_08123_b200.dit import fill_synthetic
@@ -276,6 +296,8 @@ def run_gpu(args):
 
     stream = torch.cuda.current_stream()
     flops = model.step_flops(cb)
+    if lp:   # step_flops counts this rank's branch; the job is both branches
+        flops *= world
 
     def barrier():
         if world > 1:
@@ -314,9 +336,9 @@ def run_gpu(args):
     value = args.steps / (ms / 1e3)          # whole job: every rank works on the same batch
 
     # ---- end-to-end through the public API with host buffers (pinned), H2D + D2H in the timed region
-    h_lat = torch.from_numpy(np.ascontiguousarray(batch.latents)).pin_memory()
-    h_txt = torch.from_numpy(np.ascontiguousarray(batch.txt).view(np.int16)).view(torch.bfloat16).pin_memory()
-    h_pool = torch.from_numpy(np.ascontiguousarray(batch.pooled).view(np.int16)).view(torch.bfloat16).pin_memory()
+    h_lat = lat.cpu().pin_memory()       # exactly the step's device inputs (CFG: both prompts' rows)
+    h_txt = txt.cpu().pin_memory()
+    h_pool = pooled.cpu().pin_memory()
     h_out = torch.empty_like(h_lat).pin_memory()
     e_steps = max(1, min(args.steps, 5))
     barrier()
@@ -362,7 +384,8 @@ def run_gpu(args):
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": wl["desc"], "name": args.workload, "global_batch": B, "seq_len": H_ * W_ + NT,
-                   "parallelism": f"ulysses-sp{world}" if world > 1 else "single-gpu",
+                   "parallelism": (f"latent-cfg{world}" if lp else f"ulysses-sp{world}") if world > 1 else "single-gpu",
+                   "cfg_scale": wl.get("cfg"),
                    "l2": "inputs larger than L2 (26 GB weights+adapters streamed per step vs 126 MB L2)"},
         "tflops_per_step": flops / 1e12,
         "achieved_tflops": flops / (ms_step / 1e3) / 1e12,

@@ -8,6 +8,8 @@
 // O rows go to `out` either joint (row b*N+n) or stream-split (txt rows first,
 // then img rows) so the projection GEMM can read them as one A operand.
 #include "common.cuh"
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace dit {
@@ -220,12 +222,17 @@ static cudaError_t launch_hd(const AttnParams& p, cudaStream_t s) {
 
 cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s);
 
-// d = 128 (Flux) runs on the tcgen05 kernel (attention_tc.cu); the mma.sync
-// kernel serves the small head dims of the tiny parity configs.
+// d = 128 (Flux) and d = 64 (SD3 / SD3.5) run on the tcgen05 kernel (attention_tc.cu);
+// the mma.sync kernel serves d = 32 (tiny parity configs) and, with DIT_ATTN_MMA_SYNC=1,
+// d = 64 (the pre-tcgen05 baseline, for comparison only).
 cudaError_t attention_launch(const AttnParams& p, cudaStream_t s) {
+  static const bool legacy64 = [] {
+    const char* e = getenv("DIT_ATTN_MMA_SYNC");
+    return e && e[0] == '1';
+  }();
   switch (p.d) {
     case 32: return launch_hd<32>(p, s);
-    case 64: return launch_hd<64>(p, s);
+    case 64: return legacy64 ? launch_hd<64>(p, s) : attention_tc_launch(p, s);
     case 128: return attention_tc_launch(p, s);
     default: return cudaErrorInvalidValue;
   }

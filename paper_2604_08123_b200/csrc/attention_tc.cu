@@ -1,4 +1,6 @@
-// attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (d = 128).
+// attention_tc.cu -- joint (txt+img) attention on the 5th-gen tensor cores (head dim
+// HD = 128: Flux; HD = 64: SD3 / SD3.5, one 64-column swizzle panel per tile and O
+// in 64 TMEM columns per query tile -- the schedule below is the same).
 //
 // One CTA = TWO 128-row query tiles (256 queries) of one (request, head); KV
 // tiles of 128 keys shared by both query tiles.  TMEM (512 columns):
@@ -39,11 +41,12 @@ namespace dit {
 
 namespace attn_tc {
 
-constexpr int BQ = 128, NQ = 2, BKV = 128, HD = 128;
-constexpr int TILE_BYTES = 128 * HD * 2;         // 32 KB: 128 rows x 128 bf16 (two 64-col swizzle panels)
-constexpr int PANEL = 128 * 64 * 2;              // 16 KB
+constexpr int BQ = 128, NQ = 2, BKV = 128;
+constexpr int PANEL = 128 * 64 * 2;              // 16 KB: 128 rows x 64 bf16 (one 128-byte swizzle span)
 constexpr int KST = 2, VST = 2;
-constexpr int SMEM = TILE_BYTES * (NQ + KST + VST) + 1024 + 256;   // + alignment slack + barriers
+// per head dim: 128 rows x HD bf16 per tile (HD / 64 swizzle panels)
+template <int HD> __host__ __device__ constexpr int tile_bytes() { return 128 * HD * 2; }
+template <int HD> __host__ __device__ constexpr int smem_bytes() { return tile_bytes<HD>() * (NQ + KST + VST) + 1024 + 256; }
 constexpr int SM_WARPS_PER_TILE = 4;
 // 12 warps = 3 warpgroups: softmax WG0/WG1, WG2 = 2 idle + producer + MMA (highest ids).
 // setmaxnreg moves registers from WG2 to the softmax warpgroups (S row in registers).
@@ -165,10 +168,31 @@ __device__ long long* g_attn_trace = nullptr;
   } while (0)
 
 struct Maps {
-  CUtensorMap q, k, v;   // 3D {128 (d), N, B*H}, box {64, 128, 1}
+  CUtensorMap q, k, v;   // 3D {HD, N, B*H}, box {64, 128, 1}
 };
 
+// S = Q K^T over a K = 64 head (4 MMAs of K = 16 inside one swizzle panel), warp-converged.
+DEVI void tc_mma_ss_k64_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred L, p;\n\t.reg .b32 alo, ahi, blo, bhi, x, y;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|L, -1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 {alo, ahi}, %1;\n\tmov.b64 {blo, bhi}, %2;\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s32 x, alo, 2;\n\tadd.s32 y, blo, 2;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 4;\n\tadd.s32 y, blo, 4;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s32 x, alo, 6;\n\tadd.s32 y, blo, 6;\n\tmov.b64 a, {x, ahi};\n\tmov.b64 b, {y, bhi};\n\t"
+      "@L tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+template <int HD>
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
+  constexpr int TILE_BYTES = tile_bytes<HD>();
+  constexpr int NPANEL = HD / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                              // [NQ] tiles
@@ -229,23 +253,22 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
         mbar_expect_tx(q_full, NQ * TILE_BYTES);
-        for (int t = 0; t < NQ; ++t) {
-          tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES, 0, q0 + t * BQ, bh);
-          tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + PANEL, 64, q0 + t * BQ, bh);
-        }
+        for (int t = 0; t < NQ; ++t)
+          for (int pn = 0; pn < NPANEL; ++pn)
+            tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + pn * PANEL, pn * 64, q0 + t * BQ, bh);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
           if (it == 0) TRACE(0, j);
           mbar_expect_tx(&k_full[st], TILE_BYTES);
-          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES, 0, j * BKV, bh);
-          tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+          for (int pn = 0; pn < NPANEL; ++pn)
+            tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
           mbar_wait(&v_empty[st], ph ^ 1);
           if (it == 0) TRACE(1, j);
           mbar_expect_tx(&v_full[st], TILE_BYTES);
-          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES, 0, j * BKV, bh);
-          tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + PANEL, 64, j * BKV, bh);
+          for (int pn = 0; pn < NPANEL; ++pn)
+            tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
         }
       }
     }
@@ -263,8 +286,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       if (t == 0) mbar_wait(&k_full[st], (g >> 1) & 1);
       if (t == 0 && lane == 0 && tr) TRACE(2, j);
       tc_fence_after();
-      tc_mma_ss_k128_warp<PANEL>(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
-                                 smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
+      if constexpr (HD == 128)
+        tc_mma_ss_k128_warp<PANEL>(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
+                                   smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
+      else
+        tc_mma_ss_k64_warp(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
+                           smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
       tc_commit_warp(&s_full[t]);
       if (t == NQ - 1) tc_commit_warp(&k_empty[st]);
     };
@@ -280,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       {
         // P columns of kv [0, 96) are released first (split arrive), the last 32 after
         const uint64_t vdesc = desc_mn_sw128(smem_u32(sV + st * TILE_BYTES), PANEL);
-        const uint32_t od = tm + COL_O + t * 128, pa = tm + COL_S + t * 128;
+        const uint32_t od = tm + COL_O + t * HD, pa = tm + COL_S + t * 128;
 #pragma unroll
         for (int kk = 0; kk < 6; ++kk)
           tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, (j | kk) != 0);
@@ -320,7 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const int row = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t colS = tmem + lane_base + COL_S + t * 128;
-    const uint32_t colO = tmem + lane_base + COL_O + t * 128;
+    const uint32_t colO = tmem + lane_base + COL_O + t * HD;
     const float sl2 = p.scale_log2;
     int g = 0, it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
@@ -384,7 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           mbar_wait(&o_done[t], (g - 1) & 1);
           tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < HD / 16; ++c) {
             uint32_t r[16];
             tmem_ld16(colO + c * 16, r);
             tmem_ld_wait();
@@ -447,9 +474,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       // (one 256-byte output row per thread)
       mbar_wait(&o_done[t], (g - 1) & 1);
       tc_fence_after();
-      uint32_t o[128];
+      uint32_t o[HD];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(colO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32 * c]));
+      for (int c = 0; c < HD / 32; ++c) tmem_ld32(colO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32 * c]));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
@@ -460,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         bf16* out = reinterpret_cast<bf16*>(p.out);
         uint4* dst = reinterpret_cast<uint4*>(out + (size_t)attn_out_row(p, b, n) * p.ld_out + (size_t)h * HD);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < HD / 8; ++q) {
           uint4 u;
           u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
           u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
@@ -485,11 +512,13 @@ cudaError_t attention_set_trace(long long* buf) {
   return cudaMemcpyToSymbol(attn_tc::g_attn_trace, &buf, sizeof(buf));
 }
 
-cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
+template <int HD>
+static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   using namespace attn_tc;
+  constexpr int SMEM = smem_bytes<HD>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -509,8 +538,13 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
   // persistent: one CTA per SM walks work items (query block fastest, so the CTAs running at
   // the same time share each head's K/V in L2)
   const int total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
-  attn_tc_kernel<<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
+  attn_tc_kernel<HD><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
+}
+
+cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
+  if (p.d == 64) return attention_tc_launch_hd<64>(p, s);
+  return attention_tc_launch_hd<128>(p, s);
 }
 
 }  // namespace dit

@@ -210,15 +210,15 @@ def test_sequence_parallel_local_group(torch_cuda, P, hidden, heads):
     D.load_library().dit_local_group_destroy(group)
 
 
+@pytest.mark.parametrize("d", [128, 64])
 @pytest.mark.parametrize("B,H,N", [(3, 70, 333), (1, 3, 129), (2, 150, 1000)])
-def test_attention_kernel_vs_torch_fp32(torch_cuda, B, H, N):
-    """tcgen05 attention alone (d = 128) against a plain PyTorch fp32 reference: more work items
-    than SMs (persistent CTAs walk several), ragged query blocks and ragged KV tails."""
+def test_attention_kernel_vs_torch_fp32(torch_cuda, B, H, N, d):
+    """tcgen05 attention alone (d = 128 Flux, d = 64 SD3) against a plain PyTorch fp32 reference:
+    more work items than SMs (persistent CTAs walk several), ragged query blocks and KV tails."""
     import ctypes as C
     import torch
     from paper_2604_08123_b200 import dit
     lib = dit.load_library()
-    d = 128
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + H * 10 + N)
     q, k, v = (torch.randn(B, H, N, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
     out = torch.zeros(B * N, H * d, device="cuda", dtype=torch.bfloat16)
