@@ -70,6 +70,14 @@ static_assert(2 * 128 * ATTN_REG_SOFTMAX + 128 * ATTN_REG_OTHER <= THREADS * 168
 #define ATTN_POLY_RES 1
 #endif
 constexpr int POLY_MOD = ATTN_POLY_MOD, POLY_RES = ATTN_POLY_RES;   // every POLY_MOD-th exp2 pair on the FMA-pipe polynomial
+// d = 64 (half the MMA work per score): 3/8 of the pairs on the polynomial measured best
+// (1/2: 723, 1/4: 744, 3/8: 758, 5/8: 664 TFLOP/s at B=8 H=24 N=4429 alone)
+#ifndef ATTN_POLY_MOD64
+#define ATTN_POLY_MOD64 8
+#endif
+#ifndef ATTN_POLY_RES64
+#define ATTN_POLY_RES64 3
+#endif
 constexpr uint32_t COL_S = 0, COL_O = 256;
 constexpr float RESCALE_THRESH = 8.0f;
 
@@ -433,7 +441,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           for (int e = 0; e < 16; ++e) {
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[32 * c + 2 * e]), __uint_as_float(sr[32 * c + 2 * e + 1])), sl2v, nm);
             float2 pp;
-            if ((e % POLY_MOD) >= POLY_MOD - POLY_RES) {
+            constexpr int PM = HD == 64 ? ATTN_POLY_MOD64 : POLY_MOD, PR = HD == 64 ? ATTN_POLY_RES64 : POLY_RES;
+            if ((e % PM) >= PM - PR) {
               pp = poly_exp2x2(x);                   // POLY_RES/POLY_MOD of the pairs on the FMA pipe
             } else {
               pp.x = mufu_exp2(x.x);
