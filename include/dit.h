@@ -253,6 +253,15 @@ typedef struct dit_batch {
    * conditional, rank 1 unconditional) and slots are request indices.  v_out, when
    * given, receives the guided v. */
   const float* cfg_scale;
+  /* Ragged batch (mixed resolutions, reading C24).  NULL =
+   * every request uses img_h x img_w.  Non-NULL: host [B][2], request b's own packed
+   * grid (h_b, w_b) with h_b * w_b <= img_h * img_w; img_h x img_w is then the PADDED
+   * slot size: latents_in / latents_out / v_out stay [B][img_h*img_w][C] and request b's
+   * tokens are its first h_b * w_b rows (rows beyond are ignored on input and
+   * unspecified on output); ControlNet residuals of request b are [h_b*w_b][D].  Each
+   * request's result equals running it alone at its own grid (keys of the padding are
+   * masked out of attention).  Sequence parallelism must be off (DIT_EPARALLEL). */
+  const int32_t* img_hw;
 } dit_batch;
 
 /* execute() + denoise(): one flow-matching Euler step

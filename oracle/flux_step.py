@@ -334,14 +334,22 @@ def dit_step(cfg, W, batch, adapters: Optional[Mapping[int, OracleLoRA]] = None,
     for b in reqs:
         aid = int(batch.adapter_id[b])
         ad = adapters[aid] if (adapters is not None and aid >= 0) else None
-        x = batch.latents[b].astype(F64)
+        h, w = batch.grid(b)          # a ragged batch: each request at its own grid (reading C24)
+        x = batch.latents[b][:h * w].astype(F64)
         v = velocity(cfg, W, x, bf16_to_f64(batch.txt[b]), bf16_to_f64(batch.pooled[b]),
-                     float(batch.sigma[b]), float(batch.guidance[b]), batch.img_h, batch.img_w,
+                     float(batch.sigma[b]), float(batch.guidance[b]), h, w,
                      adapter=ad, residuals=(controlnet or {}).get(b), cn_scale=float(batch.cn_scale[b]),
                      n_res=n_res, controlnets=(controlnets or {}).get(b))
-        vs.append(v)
-        xs.append(euler(x, v, batch.sigma[b], batch.sigma_next[b]))
+        vs.append(_pad_rows(v, batch.img_tokens))
+        xs.append(_pad_rows(euler(x, v, batch.sigma[b], batch.sigma_next[b]), batch.img_tokens))
     return np.stack(xs), np.stack(vs)
+
+
+def _pad_rows(a: np.ndarray, n: int) -> np.ndarray:
+    """Zero rows up to the batch's padded slot (rows beyond a request's grid carry no value)."""
+    if a.shape[0] == n:
+        return a
+    return np.concatenate([a, np.zeros((n - a.shape[0],) + a.shape[1:], dtype=a.dtype)])
 
 
 def merged_weights(W, adapter: OracleLoRA) -> Dict[str, np.ndarray]:

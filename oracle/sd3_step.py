@@ -31,7 +31,7 @@ from typing import Mapping, Optional
 
 import numpy as np
 
-from .flux_step import (F64, ControlNetInput, OracleLoRA, _cn_sum, _heads, _lora, _unheads, attention,
+from .flux_step import (F64, ControlNetInput, OracleLoRA, _cn_sum, _heads, _lora, _pad_rows, _unheads, attention,
                         bf16_to_f64, conditioning_vec, euler, gelu_tanh, layer_norm, linear, rms_norm, silu)
 
 
@@ -150,8 +150,10 @@ def dit_step(cfg, W, batch, adapters: Optional[Mapping[int, OracleLoRA]] = None,
         vc = _branch(cfg, W, batch, b, False, adapters, controlnets)
         v = vc if batch.cfg_scale is None else cfg_combine(
             vc, _branch(cfg, W, batch, b, True, adapters, controlnets), batch.cfg_scale[b])
-        vs.append(v)
-        xs.append(euler(batch.latents[b].astype(F64), v, batch.sigma[b], batch.sigma_next[b]))
+        h, w = batch.grid(b)
+        vs.append(_pad_rows(v, batch.img_tokens))
+        xs.append(_pad_rows(euler(batch.latents[b][:h * w].astype(F64), v, batch.sigma[b], batch.sigma_next[b]),
+                            batch.img_tokens))
     return np.stack(xs), np.stack(vs)
 
 
@@ -165,8 +167,9 @@ def _branch(cfg, W, batch, b, uncond, adapters, controlnets):
     pooled = batch.pooled_neg[b] if uncond else batch.pooled[b]
     slot = batch.batch + b if uncond else b
     vel = _sd3_velocity_kw if cfg.arch == "sd3" else _flux_velocity
-    return vel(cfg, W, batch.latents[b].astype(F64), bf16_to_f64(txt), bf16_to_f64(pooled),
-               float(batch.sigma[b]), batch.img_h, batch.img_w, adapter=ad,
+    h, w = batch.grid(b)   # ragged batch: the request's own grid (reading C24)
+    return vel(cfg, W, batch.latents[b][:h * w].astype(F64), bf16_to_f64(txt), bf16_to_f64(pooled),
+               float(batch.sigma[b]), h, w, adapter=ad,
                controlnets=(controlnets or {}).get(slot), cn_scale=float(batch.cn_scale[b]),
                guidance=float(batch.guidance[b]))
 

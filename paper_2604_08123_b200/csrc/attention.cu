@@ -59,11 +59,12 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
   const bf16* K = reinterpret_cast<const bf16*>(p.k) + head_off;
   const bf16* V = reinterpret_cast<const bf16*>(p.v) + head_off;
   const int q0 = qt * C::BQ;
-  const int nkv = (N + C::BKV - 1) / C::BKV;
+  const int Nv = p.seq_valid ? p.seq_valid[b] : N;   // ragged batch: keys [Nv, N) are padding
+  const int nkv = (Nv + C::BKV - 1) / C::BKV;
 
   load_tile_async<HD>(sQ, Q, q0, N, C::BQ, tid, 256);
-  load_tile_async<HD>(sK0, K, 0, N, C::BKV, tid, 256);
-  load_tile_async<HD>(sV0, V, 0, N, C::BKV, tid, 256);
+  load_tile_async<HD>(sK0, K, 0, Nv, C::BKV, tid, 256);
+  load_tile_async<HD>(sV0, V, 0, Nv, C::BKV, tid, 256);
   cp_async_commit();
 
   // Q fragments (16 rows of this warp, all HD)
@@ -78,8 +79,8 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
     const int buf = j & 1;
     if (j + 1 < nkv) {
       const int nb = buf ^ 1;
-      load_tile_async<HD>(sK0 + nb * C::KV_BYTES, K, (j + 1) * C::BKV, N, C::BKV, tid, 256);
-      load_tile_async<HD>(sV0 + nb * C::KV_BYTES, V, (j + 1) * C::BKV, N, C::BKV, tid, 256);
+      load_tile_async<HD>(sK0 + nb * C::KV_BYTES, K, (j + 1) * C::BKV, Nv, C::BKV, tid, 256);
+      load_tile_async<HD>(sV0 + nb * C::KV_BYTES, V, (j + 1) * C::BKV, Nv, C::BKV, tid, 256);
     }
     cp_async_commit();
     cp_async_wait<1>();
@@ -114,14 +115,14 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
         mma_bf16_16816(s[2 * np + 1], qf[ks], b1);
       }
     }
-    // mask keys beyond N
+    // mask keys beyond Nv
     const int kbase = j * C::BKV;
-    if (kbase + C::BKV > N) {
+    if (kbase + C::BKV > Nv) {
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         const int key = kbase + nt * 8 + 2 * tig;
-        if (key >= N) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
-        if (key + 1 >= N) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+        if (key >= Nv) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
+        if (key + 1 >= Nv) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
       }
     }
     // online softmax (rows gid and gid+8)

@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int N = p.N;
-  const int nkv = (N + BKV - 1) / BKV;
+  // ragged batch: request b's keys [seq_valid[b], N) are padding (masked; their K/V rows are
+  // finite, so P = 0 contributes exactly nothing); query rows beyond are computed and ignored
+  auto nkv_of = [&](int b) { return ((p.seq_valid ? p.seq_valid[b] : N) + BKV - 1) / BKV; };
   const int nqb = (N + NQ * BQ - 1) / (NQ * BQ);
   const int total = nqb * p.H * p.B;               // work items: (query block, head, request), block fastest
 
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       int g = 0, it = 0;                           // kv-tile counter (ring position), item counter
       for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
         const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
+        const int nkv = nkv_of(bh / p.H);
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
         mbar_expect_tx(q_full, NQ * TILE_BYTES);
         for (int t = 0; t < NQ; ++t)
@@ -328,7 +331,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       if (t == NQ - 1) tc_commit_warp(&v_empty[st]);
     };
     int g = 0, it = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it, g += nkv) {
+    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      const int nkv = nkv_of((w / nqb) / p.H);
       tr = trace != nullptr && it == 0;
       mbar_wait(q_full, it & 1);
       issue_qk(0, g, 0);
@@ -343,6 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           if (j + 2 == nkv) tc_commit_warp(q_empty);   // last QK of this item issued
         }
       }
+      g += nkv;
     }
    }
   } else {
@@ -362,6 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       const bool tr = trace != nullptr && it == 0 && lane == 0 && wq == 0;
       const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
       const int b = bh / p.H, h = bh - b * p.H;
+      const int Nv = p.seq_valid ? p.seq_valid[b] : N, nkv = nkv_of(b);
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j, ++g) {
         mbar_wait(&s_full[t], g & 1);
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
         tmem_ld_wait();
         if (tr) TRACE(10 + t, j);
-        const int kv_valid = N - j * BKV;
+        const int kv_valid = Nv - j * BKV;
         if (kv_valid < BKV) {
 #pragma unroll
           for (int e = 0; e < 128; ++e)

@@ -202,6 +202,9 @@ struct dit_ctx {
   float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][8] cn_scale_b * inject scale
   const uint32_t** p_cn_flag = nullptr;   // [Ld + Ls][CN_FANIN][8] device ready flags (controlnet_inject_flag)
   uint32_t* p_cn_expect = nullptr;        // [Ld + Ls][CN_FANIN][8]
+  int* p_img_valid = nullptr;             // [8] ragged batch: image rows of each sequence
+  int* p_seq_valid = nullptr;             // [8] ragged batch: joint rows of each sequence
+  std::vector<int> plan_hw;               // ragged grids the rope tables were built for
   bool cn_flags = false;                  // any flag registration in the current step
   RowSpace rs[3];                    // 0 txt stream, 1 img stream, 2 joint
   int slot_cap = 1;
@@ -307,7 +310,7 @@ Layout layout_of(const dit_config& c) {
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
   L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
   L.vcfg = cv.take(2 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);   // CFG: v of both branches
-  L.rope = cv.take(N * (d / 2) * 8);
+  L.rope = cv.take((size_t)c.max_batch * N * (d / 2) * 8);   // one table per sequence for ragged batches
   L.mod = cv.take(8 * mod_total * 4);
   L.vec = cv.take(8 * D * 4);
   L.h1 = cv.take(8 * D * 4);
@@ -401,6 +404,8 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take(ncn * 4));
     c->p_cn_flag = reinterpret_cast<const uint32_t**>(p + cv.take(ncn * sizeof(void*)));
     c->p_cn_expect = reinterpret_cast<uint32_t*>(p + cv.take(ncn * 4));
+    c->p_img_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
+    c->p_seq_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
   }
   {
     const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
@@ -1122,31 +1127,32 @@ int run_shrink(dit_ctx* c, int np, const void* const* A, const int* M, const int
 
 // ------------------------------------------------------------------ step
 extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
-  if (!c || !b) return 0.0;
-  // sequences computed on this GPU: CFG doubles the batch unless latent parallelism splits it
-  const double seq = (b->cfg_scale && c->lp_world == 1) ? 2.0 * b->batch : (double)b->batch;
-  const double B = seq, Ni = (double)b->img_h * b->img_w, Nt = b->txt_tokens, N = Ni + Nt;
-  const double D = c->D, F = c->F, C = c->C, Ct = c->Ct;
+  if (!c || !b || b->batch < 1) return 0.0;
+  // sequences computed on this GPU: CFG doubles the batch unless latent parallelism splits it;
+  // a ragged batch counts each request at its own grid (padding is not algorithmic work)
+  const int seq = (b->cfg_scale && c->lp_world == 1) ? 2 * b->batch : b->batch;
+  const double Nt = b->txt_tokens, D = c->D, F = c->F, C = c->C, Ct = c->Ct;
   const bool sd3 = c->cfg.arch == DIT_ARCH_SD3;
   double f = 0;
-  // embedders (the conditioning MLPs are included as 2MNK with M = B)
-  f += 2 * B * Ni * D * C + 2 * B * Nt * D * Ct;
-  // double blocks: qkv, proj, fc1, fc2 per stream + attention
-  f += c->Ld * (2 * B * N * D * (3 * D) + 2 * B * N * D * D + 2 * 2 * B * N * D * F + 4 * B * N * N * D);
-  // SD3: the context_pre_only last block has no text proj / MLP
-  if (sd3) f -= 2 * B * Nt * D * D + 2 * 2 * B * Nt * D * F;
-  // single blocks
-  f += c->Ls * (2 * B * N * D * (3 * D + F) + 2 * B * N * (D + F) * D + 4 * B * N * N * D);
-  // final
-  f += 2 * B * Ni * D * C;
-  // LoRA: 2 r (in + out) per row per adapted linear, rows of adapted requests only
-  for (int q = 0; q < (int)seq; ++q) {
-    int aid = b->adapter_id ? b->adapter_id[q % b->batch] : -1;
+  for (int q = 0; q < seq; ++q) {
+    const int r = q % b->batch;
+    const double Ni = b->img_hw ? (double)b->img_hw[2 * r] * b->img_hw[2 * r + 1] : (double)b->img_h * b->img_w;
+    const double N = Ni + Nt;
+    // embedders, final
+    f += 2 * Ni * D * C + 2 * Nt * D * Ct + 2 * Ni * D * C;
+    // double blocks: qkv, proj, fc1, fc2 per stream + attention; SD3's context_pre_only last
+    // block has no text proj / MLP
+    f += c->Ld * (2 * N * D * (3 * D) + 2 * N * D * D + 2 * 2 * N * D * F + 4 * N * N * D);
+    if (sd3) f -= 2 * Nt * D * D + 2 * 2 * Nt * D * F;
+    // single blocks
+    f += c->Ls * (2 * N * D * (3 * D + F) + 2 * N * (D + F) * D + 4 * N * N * D);
+    // LoRA: 2 r (in + out) per row per adapted linear
+    const int aid = b->adapter_id ? b->adapter_id[r] : -1;
     if (aid < 0 || c->merged_adapter >= 0) continue;   // merged: the delta is inside the base GEMMs
-    double r = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
-    f += c->Ld * 2 * r * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
-    if (sd3) f -= 2 * r * Nt * ((D + D) + (D + F) + (F + D));
-    f += c->Ls * 2 * r * N * ((D + 3 * D + F) + (D + F + D));
+    const double rk = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
+    f += c->Ld * 2 * rk * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
+    if (sd3) f -= 2 * rk * Nt * ((D + D) + (D + F) + (F + D));
+    f += c->Ls * 2 * rk * N * ((D + 3 * D + F) + (D + F + D));
   }
   return f;
 }
@@ -1189,7 +1195,25 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   const int Ni = b->img_h * b->img_w, Nt = b->txt_tokens;
   if (Ni > c->cfg.max_img_tokens || Nt > c->cfg.max_txt_tokens)
     return c->fail(DIT_ESHAPE, "tokens (%d img, %d txt) exceed the configured maxima", Ni, Nt);
-  if (c->cfg.arch == DIT_ARCH_SD3 && (b->img_h > c->cfg.pos_embed_max || b->img_w > c->cfg.pos_embed_max))
+  // ragged batch (reading C24): per-request grids inside the padded img_h x img_w slot
+  const bool ragged = b->img_hw != nullptr;
+  std::vector<int> seq_hw(2 * S), img_valid(S), seq_valid(S);
+  for (int q = 0; q < S; ++q) {
+    const int r = q % B;
+    seq_hw[2 * q] = ragged ? b->img_hw[2 * r] : b->img_h;
+    seq_hw[2 * q + 1] = ragged ? b->img_hw[2 * r + 1] : b->img_w;
+    const int hq = seq_hw[2 * q], wq = seq_hw[2 * q + 1];
+    if (hq < 1 || wq < 1 || (long long)hq * wq > (long long)b->img_h * b->img_w)
+      return c->fail(DIT_ESHAPE, "request %d grid %dx%d does not fit the %dx%d slot", r, hq, wq, b->img_h, b->img_w);
+    if (c->cfg.arch == DIT_ARCH_SD3 && (hq > c->cfg.pos_embed_max || wq > c->cfg.pos_embed_max))
+      return c->fail(DIT_ESHAPE, "request %d grid %dx%d exceeds the %d^2 position table", r, hq, wq,
+                     c->cfg.pos_embed_max);
+    img_valid[q] = hq * wq;
+    seq_valid[q] = b->txt_tokens + hq * wq;
+  }
+  if (ragged && (c->world > 1 || c->force_sp))
+    return c->fail(DIT_EPARALLEL, "ragged batches (img_hw) run without sequence parallelism");
+  if (c->cfg.arch == DIT_ARCH_SD3 && (b->img_h > c->cfg.pos_embed_max || b->img_w > c->cfg.pos_embed_max) && !ragged)
     return c->fail(DIT_ESHAPE, "token grid %dx%d exceeds the %d^2 position table", b->img_h, b->img_w,
                    c->cfg.pos_embed_max);
   const int P = c->world;
@@ -1255,15 +1279,33 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     c->plan_nt = Nt;
     c->plan_slots = req_slot;
   }
-  if (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w) {
+  // RoPE tables: one shared by every sequence, or one per sequence of a ragged Flux batch
+  const bool rope_per_seq = ragged && c->cfg.arch == DIT_ARCH_FLUX;
+  const int rope_stride = rope_per_seq ? N * (d / 2) : 0;
+  const std::vector<int> hw_key = rope_per_seq ? seq_hw : std::vector<int>();
+  if (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w || c->plan_hw != hw_key) {
     if (c->cfg.arch == DIT_ARCH_SD3)   // no RoPE: the QKV epilogue rotates by angle 0 (exact identity)
       CKC(rope_table_launch(c->rope, nt, ni, 0, 0, 1, 0, 0, d, 1.f, s));   // theta 1, width 1: angle 0
+    else if (rope_per_seq)
+      for (int q = 0; q < S; ++q)   // (P = 1) positions from request q's own grid width
+        CKC(rope_table_launch(c->rope + (size_t)q * rope_stride, nt, ni, 0, 0, seq_hw[2 * q + 1],
+                              c->cfg.rope_axes[0], c->cfg.rope_axes[1], c->cfg.rope_axes[2], c->cfg.rope_theta, s));
     else
       CKC(rope_table_launch(c->rope, nt, ni, c->rank * nt, c->rank * ni, b->img_w, c->cfg.rope_axes[0],
                             c->cfg.rope_axes[1], c->cfg.rope_axes[2], c->cfg.rope_theta, s));
     c->rope_key[0] = nt;
     c->rope_key[1] = ni;
     c->rope_key[2] = b->img_w;
+    c->plan_hw = hw_key;
+  }
+  if (ragged) {
+    std::vector<int> iv(16, 0);
+    for (int q = 0; q < S; ++q) {
+      iv[q] = img_valid[q];
+      iv[8 + q] = seq_valid[q];
+    }
+    cudaMemcpyAsync(c->p_img_valid, iv.data(), 8 * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->p_seq_valid, iv.data() + 8, 8 * 4, cudaMemcpyHostToDevice, s);
   }
   // ---- per-step parameter block (pageable source: safe to reuse after return)
   {
@@ -1358,7 +1400,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       2.0 * S * (double)c->seg_rows * D);
 
   // ---- embeddings into the fp32 residual stream h [S][N][D] (txt rows first)
-  CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)B * ni * C, s));
+  if (ragged)   // padding rows of the latents become exact zeros (every padded row stays finite)
+    CKC(cast_latents_ragged_launch(b->latents_in, c->xb, B, ni, C, c->p_img_valid, s));
+  else
+    CKC(cast_bf16_launch(b->latents_in, c->xb, (int64_t)B * ni * C, s));
   if (S > B)   // CFG on one GPU: both branches denoise the same latents
     cudaMemcpyAsync(c->xb + (size_t)B * ni * C, c->xb, (size_t)B * ni * C * 2, cudaMemcpyDeviceToDevice, s);
   {
@@ -1380,9 +1425,15 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     c->gemm_label = 10;
     CK(run_gemm(c, p, 2, s));
   }
-  if (c->cfg.arch == DIT_ARCH_SD3)   // SD3 position table on the image rows (reading C21)
-    CKC(pos_embed_add_launch(c->h, S, N, nt, ni, c->rank * ni, b->img_h, b->img_w, D, c->cfg.pos_embed_max,
-                             c->cfg.pos_embed_base, s));
+  if (c->cfg.arch == DIT_ARCH_SD3) {   // SD3 position table on the image rows (reading C21)
+    if (ragged)
+      for (int q = 0; q < S; ++q)
+        CKC(pos_embed_add_launch(c->h + (size_t)q * N * D, 1, N, nt, img_valid[q], 0, seq_hw[2 * q],
+                                 seq_hw[2 * q + 1], D, c->cfg.pos_embed_max, c->cfg.pos_embed_base, s));
+    else
+      CKC(pos_embed_add_launch(c->h, S, N, nt, ni, c->rank * ni, b->img_h, b->img_w, D, c->cfg.pos_embed_max,
+                               c->cfg.pos_embed_base, s));
+  }
 
   const float scale_log2 = 1.4426950408889634f / std::sqrt((float)d);
   // ---- attention with the Ulysses exchange around it (P > 1): QKV epilogue wrote
@@ -1426,6 +1477,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     ap.nt = nt;
     ap.ni = ni;
     ap.Nt = Nt;
+    ap.seq_valid = ragged ? c->p_seq_valid : nullptr;
     if (!sp) {
       ap.out = out;
       ap.ld_out = ld_out;
@@ -1529,6 +1581,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.batch = S;
       e.sp_world = P;
       e.rope = c->rope;
+      e.rope_stride = rope_stride;
       e.qkv_cols = 3 * D;
       e.heads = H;
       e.head_dim = d;
@@ -1578,6 +1631,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         eI.cn_ptr = cn_ptr;
         eI.cn_scale = c->p_cn_kappa + (size_t)i * CN_FANIN * 8;
         eI.cn_row0 = 0;   // the img-stream problem's rows are exactly the residual's rows
+        eI.img_valid = ragged ? c->p_img_valid : nullptr;
         if (c->cn_flags) {
           eI.cn_flag = c->p_cn_flag + (size_t)i * CN_FANIN * 8;
           eI.cn_expect = c->p_cn_expect + (size_t)i * CN_FANIN * 8;
@@ -1672,6 +1726,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.q_gamma = SB.qn;
       e.k_gamma = SB.kn;
       e.rope = c->rope;
+      e.rope_stride = rope_stride;
       e.qkv_cols = 3 * D;
       e.heads = H;
       e.head_dim = d;
@@ -1710,6 +1765,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
         e.cn_ptr = (const void* const*)(c->p_cn_ptr + (size_t)(c->Ld + j) * CN_FANIN * 8);
         e.cn_scale = c->p_cn_kappa + (size_t)(c->Ld + j) * CN_FANIN * 8;
         e.cn_row0 = nt;           // joint rows are [txt; img] per request
+        e.img_valid = ragged ? c->p_img_valid : nullptr;
         if (c->cn_flags) {
           e.cn_flag = c->p_cn_flag + (size_t)(c->Ld + j) * CN_FANIN * 8;
           e.cn_expect = c->p_cn_expect + (size_t)(c->Ld + j) * CN_FANIN * 8;

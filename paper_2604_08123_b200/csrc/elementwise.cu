@@ -483,6 +483,22 @@ __global__ void cast_bf16_kernel(const float* x, bf16* out, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(x[i]);
 }
+__global__ void cast_latents_ragged_kernel(const float* x, bf16* out, int ni_pad, int C, const int* valid,
+                                           int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t row = i / C;
+  const int b = (int)(row / ni_pad), r = (int)(row - (int64_t)b * ni_pad);
+  out[i] = __float2bfloat16_rn(r < valid[b] ? x[i] : 0.f);
+}
+cudaError_t cast_latents_ragged_launch(const float* x, void* out, int B, int ni_pad, int C, const int* valid,
+                                       cudaStream_t s) {
+  const int64_t n = (int64_t)B * ni_pad * C;
+  if (n <= 0) return cudaSuccess;
+  cast_latents_ragged_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, reinterpret_cast<bf16*>(out), ni_pad, C,
+                                                                          valid, n);
+  return cudaGetLastError();
+}
 cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   cast_bf16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, reinterpret_cast<bf16*>(out), n);

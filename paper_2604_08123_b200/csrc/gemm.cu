@@ -241,7 +241,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
             rs = rsqrtf(ss / (float)d + 1e-6f);
           }
           const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
-          const float4* cs = reinterpret_cast<const float4*>(E.rope + (size_t)(E.joint_off + nloc) * (d / 2));
+          const float4* cs = reinterpret_cast<const float4*>(E.rope + (size_t)b * E.rope_stride +
+                                                             (size_t)(E.joint_off + nloc) * (d / 2));
           if (nrm) norm_rope_half(y, rs, g + 64, cs + 16);
           if (row_ok) {
 #pragma unroll
@@ -276,7 +277,7 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           rs = rsqrtf(ss / (float)d + 1e-6f);
         }
         const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
-        const float2* cs = E.rope + (size_t)(E.joint_off + nloc) * (d / 2);
+        const float2* cs = E.rope + (size_t)b * E.rope_stride + (size_t)(E.joint_off + nloc) * (d / 2);
         // pass 2: normalise, rotate interleaved pairs, store
 #pragma unroll 1
         for (int j = 0; j < d; j += 32) {
@@ -379,7 +380,8 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
       const bf16* cn0 = nullptr;
       const bf16* cn1 = nullptr;
       float kap0 = 0.f, kap1 = 0.f;
-      if (E.cn_ptr != nullptr && nloc >= E.cn_row0) {
+      if (E.cn_ptr != nullptr && nloc >= E.cn_row0 &&
+          (E.img_valid == nullptr || nloc - E.cn_row0 < E.img_valid[b])) {   // (ragged: residual has Ni_b rows)
         const size_t roff = (size_t)(nloc - E.cn_row0) * E.D + col;
         cn0 = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
         cn1 = reinterpret_cast<const bf16*>(E.cn_ptr[8 + b]);
@@ -447,7 +449,7 @@ DEVI void prefetch_epilogue_rows(const GemmProblem& P, const TileInfo& ti, int r
   const float* hp = E.h + (size_t)jrow * E.D + col;
 #pragma unroll
   for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(hp + q * 32));
-  if (E.cn_ptr != nullptr && nloc >= E.cn_row0) {
+  if (E.cn_ptr != nullptr && nloc >= E.cn_row0 && (E.img_valid == nullptr || nloc - E.cn_row0 < E.img_valid[b])) {
 #pragma unroll
     for (int k = 0; k < CN_FANIN; ++k) {
       const bf16* cn = reinterpret_cast<const bf16*>(E.cn_ptr[8 * k + b]);

@@ -47,6 +47,7 @@ struct EpiParams {
   int cn_row0;               // request-local row of residual row 0 (0: img-stream GEMM; Nt_loc: joint rows)
   const uint32_t* const* cn_flag;  // device [CN_FANIN][8] ready flags (nullptr = resident / event-ordered)
   const uint32_t* cn_expect;       // device [CN_FANIN][8] value the flag must reach
+  const int* img_valid;            // device [8] valid image rows per sequence (ragged batch; nullptr = all)
   // bf16 outputs
   void* out;
   int ld_out;
@@ -58,7 +59,8 @@ struct EpiParams {
   int sp_world;              // P
   const void* q_gamma;       // bf16 [d]
   const void* k_gamma;
-  const float2* rope;        // [joint_n][d/2] (cos, sin)
+  const float2* rope;        // [joint_n][d/2] (cos, sin) (+ b * rope_stride for a ragged batch)
+  int rope_stride;           // float2 entries per sequence (0: one table shared by all sequences)
   int qkv_cols;              // 3D (columns beyond go to the GELU branch)
   int heads, head_dim;
   int seq_len;               // rows per (b, h) of q/k/v (= joint_n)
@@ -122,6 +124,8 @@ struct AttnParams {
   int nt;              // txt rows per request (split: global Nt; SP: local nt)
   int ni;              // img rows per request (split: global Ni; SP: local ni)
   int Nt;              // global txt rows (SP mode)
+  const int* seq_valid;  // device [B] valid joint rows per sequence (ragged batch; nullptr = N):
+                         // keys beyond are masked, query rows beyond are written as zeros
 };
 // Output row of query token n (global joint order) of request b; SP mode also
 // returns the destination rank in *dest (rows are then [dest][B][N_loc]).
@@ -226,6 +230,9 @@ cudaError_t cfg_euler_launch(const float* vc, const float* vu, const float* g, c
                              float* lat_out, float* v_out, int B, int count, cudaStream_t s);
 // x fp32 [n] -> bf16
 cudaError_t cast_bf16_launch(const float* x, void* out, int64_t n, cudaStream_t s);
+// ragged batch: latents [B][ni_pad][C] fp32 -> bf16, rows >= valid[b] (device) set to zero
+cudaError_t cast_latents_ragged_launch(const float* x, void* out, int B, int ni_pad, int C, const int* valid,
+                                       cudaStream_t s);
 cudaError_t fill_synthetic_launch(void* dst, int64_t n, uint64_t seed, uint64_t tid, float scale, float offset,
                                   cudaStream_t s);
 

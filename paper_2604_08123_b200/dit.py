@@ -45,7 +45,7 @@ class dit_batch(C.Structure):
                 ("sigma_next", C.POINTER(C.c_float)), ("guidance", C.POINTER(C.c_float)),
                 ("cn_scale", C.POINTER(C.c_float)), ("latents_in", C.c_void_p), ("latents_out", C.c_void_p),
                 ("txt", C.c_void_p), ("pooled", C.c_void_p), ("v_out", C.c_void_p),
-                ("cfg_scale", C.POINTER(C.c_float))]
+                ("cfg_scale", C.POINTER(C.c_float)), ("img_hw", C.POINTER(C.c_int32))]
 
 
 EXPORTS = {
@@ -245,7 +245,8 @@ class DiT:
         _check(self.lib.lp_init_local(self.ctx, group, rank), self.ctx)
 
     def make_batch(self, batch_size, img_h, img_w, txt_tokens, adapter_id, sigma, sigma_next, guidance,
-                   latents_in, latents_out, txt, pooled, v_out=None, cn_scale=None, cfg_scale=None) -> dit_batch:
+                   latents_in, latents_out, txt, pooled, v_out=None, cn_scale=None, cfg_scale=None,
+                   img_hw=None) -> dit_batch:
         b = dit_batch()
         b.batch, b.img_h, b.img_w, b.txt_tokens = batch_size, img_h, img_w, txt_tokens
         keep = [_arr(C.c_int32, [int(x) for x in adapter_id]), _arr(C.c_float, [float(x) for x in sigma]),
@@ -259,6 +260,10 @@ class DiT:
             gs = _arr(C.c_float, [float(x) for x in cfg_scale])
             keep.append(gs)
             b.cfg_scale = gs
+        if img_hw is not None:
+            hw = _arr(C.c_int32, [int(x) for pair in img_hw for x in pair])
+            keep.append(hw)
+            b.img_hw = hw
         b.latents_in, b.latents_out = latents_in.data_ptr(), latents_out.data_ptr()
         b.txt, b.pooled = txt.data_ptr(), pooled.data_ptr()
         b.v_out = v_out.data_ptr() if v_out is not None else None

@@ -84,7 +84,7 @@ class SyntheticDiT(DiT):
             self.controlnet_inject(b, blk, _bits_to_bf16_tensor(bits, self.dev), sc)
         cb = self.make_batch(batch.batch, batch.img_h, batch.img_w, batch.txt_tokens, batch.adapter_id,
                              batch.sigma, batch.sigma_next, batch.guidance, lat, out, txt, pooled, v_out=v,
-                             cn_scale=batch.cn_scale, cfg_scale=batch.cfg_scale)
+                             cn_scale=batch.cn_scale, cfg_scale=batch.cfg_scale, img_hw=batch.img_hw)
         self.dit_step(cb)
         if not sync:   # (latent-parallel tests: the peer rank's thread must also have enqueued)
             return out, v

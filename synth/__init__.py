@@ -362,6 +362,10 @@ class Batch:
     cfg_scale: Optional[np.ndarray] = None   # fp32 [B]
     txt_neg: Optional[np.ndarray] = None     # uint16 bf16 bits [B, Nt, Ct] (unconditional branch)
     pooled_neg: Optional[np.ndarray] = None  # uint16 bf16 bits [B, Cp]
+    # ragged batch (mixed resolutions; reading C24): None = every request img_h x img_w;
+    # else int32 [B, 2] per-request grids, img_h x img_w is the padded slot and request b's
+    # latents are its first h_b * w_b rows
+    img_hw: Optional[np.ndarray] = None
 
     @property
     def batch(self) -> int:
@@ -370,6 +374,12 @@ class Batch:
     @property
     def img_tokens(self) -> int:
         return self.img_h * self.img_w
+
+    def grid(self, b: int) -> Tuple[int, int]:
+        """Request b's own (h, w) token grid."""
+        if self.img_hw is None:
+            return self.img_h, self.img_w
+        return int(self.img_hw[b][0]), int(self.img_hw[b][1])
 
 
 def negative_txt_bf16(b_seed_index: int, nt: int, ct: int) -> np.ndarray:
