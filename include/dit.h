@@ -199,6 +199,30 @@ int controlnet_inject(dit_ctx* ctx, int32_t slot, int32_t block, const void* res
 int controlnet_inject_flag(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
                            float scale, const uint32_t* flag, uint32_t expect);
 
+/* --------------------------------------------- ControlNet producer side (f2) */
+/* The data engine's push half: a
+ * ControlNet executor on another GPU or in another process writes each residual
+ * straight into the DiT's registered buffer and releases a ready flag, which the DiT's
+ * consuming GEMM epilogue acquires (controlnet_inject_flag) -- deferred fetch with no
+ * host round trip.  controlnet_push copies `bytes` (multiple of 16, 16-byte aligned)
+ * from `src` to `dst` with a grid of CTAs (dst may be a peer GPU's memory mapped by
+ * cudaDeviceEnablePeerAccess / dit_ipc_open: the stores travel over NVLink), then a
+ * second kernel stores *flag = value with a system-scope release after the copy
+ * (stream order + fence.sys).  Enqueued on `stream`; nothing is read back.
+ * Errors: DIT_EINVAL (NULL / misaligned / bytes % 16), DIT_ECUDA. */
+int controlnet_push(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value, void* stream);
+
+/* Inter-process export / import of a device buffer (residuals and flags of another
+ * executor).  A handle is DIT_IPC_HANDLE_BYTES opaque bytes: the CUDA IPC handle of the
+ * allocation containing dev_ptr plus dev_ptr's offset inside it, so interior pointers of
+ * a caching allocator work.  dit_ipc_open maps it into this process (*out = the same
+ * byte the exporter named); dit_ipc_close unmaps.  The exporter must keep the
+ * allocation alive while it is open elsewhere.  Errors: DIT_EINVAL, DIT_ECUDA. */
+#define DIT_IPC_HANDLE_BYTES 72
+int dit_ipc_export(const void* dev_ptr, void* handle_out);
+int dit_ipc_open(const void* handle, void** out);
+int dit_ipc_close(void* dev_ptr);
+
 /* ------------------------------------------------------ sequence parallel */
 /* Parallelism descriptor: this context is rank `rank` of
  * `world` GPUs running one dit_step together with Ulysses sequence

@@ -917,6 +917,74 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   return DIT_OK;
 }
 
+// ------------------------------------------------------------------ ControlNet producer side (f2)
+extern "C" int controlnet_push(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                               void* stream) {
+  if (!dst || !src || !flag || bytes % 16 || (reinterpret_cast<uintptr_t>(dst) & 15) ||
+      (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(flag) & 3))
+    return DIT_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return controlnet_push_launch(dst, src, bytes, flag, value, sms, reinterpret_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? DIT_OK
+             : DIT_ECUDA;
+}
+
+namespace {
+struct IpcHandle {
+  cudaIpcMemHandle_t h;   // 64 bytes
+  uint64_t offset;        // dev_ptr - allocation base
+};
+static_assert(sizeof(IpcHandle) == DIT_IPC_HANDLE_BYTES, "ipc handle layout");
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link)
+CUresult mem_range(CUdeviceptr* base, size_t* size, CUdeviceptr p) {
+  typedef CUresult (*Fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return CUDA_ERROR_NOT_FOUND;
+    fn = reinterpret_cast<Fn>(f);
+  }
+  return fn(base, size, p);
+}
+}  // namespace
+
+extern "C" int dit_ipc_export(const void* dev_ptr, void* out) {
+  if (!dev_ptr || !out) return DIT_EINVAL;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (mem_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) return DIT_EINVAL;
+  IpcHandle ih;
+  memset(&ih, 0, sizeof(ih));
+  if (cudaIpcGetMemHandle(&ih.h, reinterpret_cast<void*>(base)) != cudaSuccess) return DIT_ECUDA;
+  ih.offset = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
+  memcpy(out, &ih, sizeof(ih));
+  return DIT_OK;
+}
+
+extern "C" int dit_ipc_open(const void* handle, void** out) {
+  if (!handle || !out) return DIT_EINVAL;
+  IpcHandle ih;
+  memcpy(&ih, handle, sizeof(ih));
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, ih.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return DIT_ECUDA;
+  *out = static_cast<uint8_t*>(base) + ih.offset;
+  return DIT_OK;
+}
+
+extern "C" int dit_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return DIT_EINVAL;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (mem_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) return DIT_EINVAL;
+  return cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
 // ------------------------------------------------------------------ latent parallelism
 extern "C" int lp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
   if (!c) return DIT_EINVAL;

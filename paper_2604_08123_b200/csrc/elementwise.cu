@@ -225,6 +225,42 @@ cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uin
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ ControlNet push (f2)
+__global__ void __launch_bounds__(256) push_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                        size_t n16) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  // 4 independent 16-byte loads in flight per thread before the (possibly remote) stores
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldg(src + i), b = __ldg(src + i + stride), c = __ldg(src + i + 2 * stride),
+                d = __ldg(src + i + 3 * stride);
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = __ldg(src + i);
+}
+__global__ void push_release_kernel(uint32_t* flag, uint32_t value) {
+  // every store of the copy kernel happens-before this kernel (same stream); the system-scope
+  // fence + release make them visible to a consumer that acquires the flag (any GPU / process)
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                                   int num_sms, cudaStream_t s) {
+  if (bytes % 16 || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
+    return cudaErrorInvalidValue;
+  const size_t n16 = bytes / 16;
+  if (n16 > 0) {
+    const size_t want = (n16 + 1023) / 1024;
+    const unsigned grid = (unsigned)std::min<size_t>(want, (size_t)num_sms * 4);
+    push_copy_kernel<<<grid, 256, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+  }
+  push_release_kernel<<<1, 1, 0, s>>>(flag, value);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ merged LoRA
 // Weight patching: W' = bf16(W + s * B A) for one adapted linear.
 // A 128 x 128 output tile per CTA, 8 warps x 16 rows; the rank-r product runs on

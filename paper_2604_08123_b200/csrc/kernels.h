@@ -200,6 +200,10 @@ cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s);
 // release (so a consumer that acquires the flag sees the data).  One CTA.
 cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
                                    uint64_t delay_ns, cudaStream_t s);
+// ControlNet push (producer side, §8(f) f2): grid copy dst <- src (16-byte granules), then a
+// one-thread kernel: fence.sys + st.release.sys *flag = value.
+cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
+                                   int num_sms, cudaStream_t s);
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 

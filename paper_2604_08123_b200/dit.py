@@ -65,6 +65,10 @@ EXPORTS = {
                                          C.c_uint32]),
     "dit_debug_delayed_publish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_uint64,
                                             C.c_void_p]),
+    "controlnet_push": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_void_p]),
+    "dit_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dit_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dit_ipc_close": (C.c_int, [C.c_void_p]),
     "sp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "lp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "lp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
@@ -309,6 +313,35 @@ class DiT:
         import torch
         s = stream if stream is not None else torch.cuda.current_stream()
         return C.c_void_p(s.cuda_stream)
+
+
+IPC_HANDLE_BYTES = 72
+
+
+def ipc_export(t) -> bytes:
+    """Inter-process handle of a device tensor's first byte (dit_ipc_export)."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(load_library().dit_ipc_export(t.data_ptr(), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = C.c_void_p()
+    _check(load_library().dit_ipc_open(C.create_string_buffer(handle, IPC_HANDLE_BYTES), C.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int):
+    _check(load_library().dit_ipc_close(C.c_void_p(ptr)))
+
+
+def controlnet_push(dst: int, src, flag: int, value: int, stream=None):
+    """Producer side of the deferred ControlNet input: copy `src` (a device tensor) to the
+    consumer's buffer `dst` (a device pointer, e.g. from ipc_open) and release *flag = value."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(load_library().controlnet_push(C.c_void_p(dst), C.c_void_p(src.data_ptr()), src.numel() * src.element_size(),
+                                          C.c_void_p(flag), value, C.c_void_p(s.cuda_stream)))
 
 
 def nccl_unique_id() -> bytes:
