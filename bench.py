@@ -386,6 +386,8 @@ def run_gpu(args):
         "config": {"workload": wl["desc"], "name": args.workload, "global_batch": B, "seq_len": H_ * W_ + NT,
                    "parallelism": (f"latent-cfg{world}" if lp else f"ulysses-sp{world}") if world > 1 else "single-gpu",
                    "cfg_scale": wl.get("cfg"),
+                   "sp_exchange": {0: None, 1: "nccl-all-to-all", 2: "fused-epilogue-peer-stores"}[
+                       int(model.lib.dit_sp_exchange(model.ctx))],
                    "l2": "inputs larger than L2 (26 GB weights+adapters streamed per step vs 126 MB L2)"},
         "tflops_per_step": flops / 1e12,
         "achieved_tflops": flops / (ms_step / 1e3) / 1e12,

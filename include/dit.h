@@ -226,7 +226,9 @@ int dit_ipc_close(void* dev_ptr);
 /* ------------------------------------------------------ sequence parallel */
 /* Parallelism descriptor: this context is rank `rank` of
  * `world` GPUs running one dit_step together with Ulysses sequence
- * parallelism.  nccl_unique_id: 128-byte ncclUniqueId (host), identical on all
+ * parallelism.  At world > 1 it also maps every peer's workspace (CUDA IPC handles
+ * all-gathered over the new communicator) so the exchange is fused into the
+ * epilogues (dit_sp_exchange); if any rank cannot map, all ranks use NCCL all-to-alls.  nccl_unique_id: 128-byte ncclUniqueId (host), identical on all
  * ranks (broadcast by the caller).  Collective: every rank must call it.
  * world == 1 disables communication.  Shard layout (bit-exact):
  * rank r owns, of every request, txt rows [r*Nt/P, (r+1)*Nt/P) and img rows
@@ -303,6 +305,12 @@ double dit_step_flops(const dit_ctx* ctx, const dit_batch* batch);
 /* Number of kernels the last dit_step launched (for bench.py gpu_launches). */
 int dit_last_launch_count(const dit_ctx* ctx);
 
+/* Sequence-parallel exchange in use: 0 none (world 1), 1 NCCL all-to-all + gather/scatter
+ * kernels, 2 fused -- the QKV and attention epilogues store straight into the owning rank's
+ * buffers (peer-mapped over NVLink through CUDA IPC) behind device flag barriers (the
+ * default when every rank can map every peer; DIT_SP_NCCL=1 forces 1). */
+int dit_sp_exchange(const dit_ctx* ctx);
+
 /* ------------------------------------------------------ profiling exports */
 /* Per-launch device timing for bench.py's roofline (CUDA events recorded on
  * the launch stream around every kernel while enabled).  kind: 0 tcgen05
@@ -354,7 +362,9 @@ int dit_nccl_unique_id(void* out128);
 /* Host copy of the sequence-parallel index maps the kernels use (bit-exact
  * layout tests, no GPU needed).  which: 0 shard map (local row -> global joint
  * row b*N+n), 1 QKV send layout, 2 gather (recv -> attention layout), 3 O send
- * rows, 4 O scatter rows (stream-split).  Writes up to cap int64 entries to
+ * rows, 4 O scatter rows (stream-split); fused exchange: 5 QKV peer stores
+ * (dest * 3BHlN + attention-buffer index), 6 O peer stores (dest * 2^40 +
+ * row * H + global head of the stream-split O buffer).  Writes up to cap int64 entries to
  * out; returns the number of entries, or -status. */
 int64_t dit_sp_layout(int32_t which, int32_t world, int32_t rank, int32_t B, int32_t H, int32_t Nt, int32_t Ni,
                       int64_t* out, int64_t cap);

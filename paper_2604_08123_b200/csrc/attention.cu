@@ -44,7 +44,7 @@ DEVI void load_tile_async(uint32_t s_base, const bf16* g, int row0, int rows_tot
 }
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   using C = AttnCfg<HD>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sQ = smem_u32(smem);
@@ -201,9 +201,8 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const AttnParams p) {
     const int r = i / C::CHUNKS, c = i % C::CHUNKS;
     const int n = q0 + r;
     if (n >= N) continue;
-    const size_t orow = (size_t)attn_out_row(p, b, n);
     const uint4 val = *reinterpret_cast<const uint4*>(sq + swz_off<HD>(r, c));
-    *reinterpret_cast<uint4*>(out + orow * p.ld_out + (size_t)h * HD + c * 8) = val;
+    *reinterpret_cast<uint4*>(attn_out_addr(p, b, n, h, HD) + c * 8) = val;
   }
 }
 

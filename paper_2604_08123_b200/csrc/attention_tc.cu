@@ -197,8 +197,15 @@ DEVI void tc_mma_ss_k64_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, 
       : "memory");
 }
 
-template <int HD>
-__global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const AttnParams p) {
+// kv tiles of request b's (possibly ragged) joint sequence
+// (RAGGED = false: the uniform-batch instantiation carries no per-request length at all)
+template <bool RAGGED>
+DEVI int seq_len_of(const AttnParams& p, int b) { return RAGGED ? p.seq_valid[b] : p.N; }
+template <bool RAGGED>
+DEVI int kv_tiles(const AttnParams& p, int b) { return (seq_len_of<RAGGED>(p, b) + BKV - 1) / BKV; }
+
+template <int HD, bool RAGGED>
+__global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ AttnParams p) {
   constexpr int TILE_BYTES = tile_bytes<HD>();
   constexpr int NPANEL = HD / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   const int N = p.N;
   // ragged batch: request b's keys [seq_valid[b], N) are padding (masked; their K/V rows are
   // finite, so P = 0 contributes exactly nothing); query rows beyond are computed and ignored
-  auto nkv_of = [&](int b) { return ((p.seq_valid ? p.seq_valid[b] : N) + BKV - 1) / BKV; };
+
   const int nqb = (N + NQ * BQ - 1) / (NQ * BQ);
   const int total = nqb * p.H * p.B;               // work items: (query block, head, request), block fastest
 
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       int g = 0, it = 0;                           // kv-tile counter (ring position), item counter
       for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
         const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
-        const int nkv = nkv_of(bh / p.H);
+        const int nkv = kv_tiles<RAGGED>(p, bh / p.H);
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
         mbar_expect_tx(q_full, NQ * TILE_BYTES);
         for (int t = 0; t < NQ; ++t)
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     };
     int g = 0, it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-      const int nkv = nkv_of((w / nqb) / p.H);
+      const int nkv = kv_tiles<RAGGED>(p, (w / nqb) / p.H);
       tr = trace != nullptr && it == 0;
       mbar_wait(q_full, it & 1);
       issue_qk(0, g, 0);
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       const bool tr = trace != nullptr && it == 0 && lane == 0 && wq == 0;
       const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
       const int b = bh / p.H, h = bh - b * p.H;
-      const int Nv = p.seq_valid ? p.seq_valid[b] : N, nkv = nkv_of(b);
+      const int Nv = seq_len_of<RAGGED>(p, b), nkv = kv_tiles<RAGGED>(p, b);
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j, ++g) {
         mbar_wait(&s_full[t], g & 1);
@@ -487,6 +494,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       }
       // epilogue: read O out of TMEM, release it to the next work item, then O / l -> bf16
       // (one 256-byte output row per thread)
+      // (the output address first: its temporaries die before the 128 O registers go live)
+      const int n = q0 + t * BQ + row;
+      uint4* dst = n < N ? reinterpret_cast<uint4*>(attn_out_addr(p, b, n, h, HD)) : nullptr;
       mbar_wait(&o_done[t], (g - 1) & 1);
       tc_fence_after();
       uint32_t o[HD];
@@ -496,11 +506,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
-      const int n = q0 + t * BQ + row;
-      if (n < N) {
+      if (dst != nullptr) {
         const float inv = 1.0f / l;
-        bf16* out = reinterpret_cast<bf16*>(p.out);
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)attn_out_row(p, b, n) * p.ld_out + (size_t)h * HD);
 #pragma unroll
         for (int q = 0; q < HD / 8; ++q) {
           uint4 u;
@@ -527,13 +534,13 @@ cudaError_t attention_set_trace(long long* buf) {
   return cudaMemcpyToSymbol(attn_tc::g_attn_trace, &buf, sizeof(buf));
 }
 
-template <int HD>
+template <int HD, bool RAGGED>
 static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   using namespace attn_tc;
   constexpr int SMEM = smem_bytes<HD>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -553,13 +560,14 @@ static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   // persistent: one CTA per SM walks work items (query block fastest, so the CTAs running at
   // the same time share each head's K/V in L2)
   const int total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
-  attn_tc_kernel<HD><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
+  attn_tc_kernel<HD, RAGGED><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
 
 cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
-  if (p.d == 64) return attention_tc_launch_hd<64>(p, s);
-  return attention_tc_launch_hd<128>(p, s);
+  if (p.seq_valid != nullptr)
+    return p.d == 64 ? attention_tc_launch_hd<64, true>(p, s) : attention_tc_launch_hd<128, true>(p, s);
+  return p.d == 64 ? attention_tc_launch_hd<64, false>(p, s) : attention_tc_launch_hd<128, false>(p, s);
 }
 
 }  // namespace dit

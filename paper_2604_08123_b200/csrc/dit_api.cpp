@@ -94,6 +94,9 @@ struct LocalGroup {
   long gen = 0;
   std::vector<const void*> send;
   std::vector<cudaEvent_t> ready, done;
+  // fused exchange: every rank's peer-visible buffers (same process: plain device pointers)
+  std::vector<void*> qkv, o, cat;
+  std::vector<uint32_t*> flags;
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const long g = gen;
@@ -168,6 +171,18 @@ struct dit_ctx {
   ncclComm_t comm = nullptr;
   LocalGroup* local_group = nullptr;
   bool force_sp = false;             // test-only: SP data path at world == 1 (DIT_FORCE_SP)
+  // fused Ulysses exchange (default at P > 1; DIT_SP_NCCL=1 selects the NCCL all-to-all path):
+  // the QKV epilogue and the attention epilogue store straight into the owning rank's buffers
+  // (peer-mapped through CUDA IPC), with device flag barriers instead of all-to-alls
+  bool sp_fused = false;
+  bool peers_ready = false;
+  void* peer_qkv[8] = {};
+  void* peer_o[8] = {};
+  void* peer_cat[8] = {};
+  PeerFlags peer_flags = {};
+  uint32_t* flags = nullptr;         // [8] arrival epochs, written by the peers
+  uint32_t sp_epoch = 0;
+  std::vector<void*> ipc_opened;
   // latent (CFG) parallelism: rank 0 conditional, rank 1 unconditional branch
   int lp_world = 1, lp_rank = 0;
   ncclComm_t lp_comm = nullptr;
@@ -406,6 +421,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     c->p_cn_expect = reinterpret_cast<uint32_t*>(p + cv.take(ncn * 4));
     c->p_img_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
     c->p_seq_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
+    c->flags = reinterpret_cast<uint32_t*>(p + cv.take(8 * 4));
   }
   {
     const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
@@ -473,6 +489,7 @@ extern "C" void dit_destroy(dit_ctx* c) {
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
   for (auto& e : c->slot_last_use)
     if (e) cudaEventDestroy(e);
+  for (void* ptr : c->ipc_opened) dit_ipc_close(ptr);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->lp_comm) ncclCommDestroy(c->lp_comm);
   delete c;
@@ -853,6 +870,10 @@ extern "C" void* dit_local_group_create(int32_t world) {
   LocalGroup* g = new LocalGroup();
   g->world = world;
   g->send.assign(world, nullptr);
+  g->qkv.assign(world, nullptr);
+  g->o.assign(world, nullptr);
+  g->cat.assign(world, nullptr);
+  g->flags.assign(world, nullptr);
   g->ready.assign(world, nullptr);
   g->done.assign(world, nullptr);
   for (int r = 0; r < world; ++r) {
@@ -876,12 +897,89 @@ extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   if (!g || rank < 0 || rank >= g->world) return c->fail(DIT_EINVAL, "bad local group / rank");
   if (c->H % g->world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", g->world, c->H);
   if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
+  const char* nccl_path = getenv("DIT_SP_NCCL");
+  c->sp_fused = g->world > 1 && !(nccl_path && nccl_path[0] == '1');
+  if (c->sp_fused) {   // peers resolve at the first dit_step, once every rank has registered
+    cudaMemset(c->flags, 0, 8 * 4);
+    cudaDeviceSynchronize();
+    g->qkv[rank] = c->qkv;
+    g->o[rank] = c->o;
+    g->cat[rank] = c->cat;
+    g->flags[rank] = c->flags;
+    c->peers_ready = false;
+    c->sp_epoch = 0;
+  }
   c->local_group = g;
   c->world = g->world;
   c->rank = rank;
   c->plan_B = -1;
   c->rope_key[0] = -1;
   return DIT_OK;
+}
+
+// Fused exchange setup over NCCL: zero my arrival flags, all-gather every rank's IPC handles of
+// (qkv, o, cat, flags) through the new communicator, map the peers' buffers.  Any failure leaves
+// sp_fused off (the NCCL all-to-all path then runs) -- a capability check, not an error.
+static void setup_fused_peers(dit_ctx* c) {
+  // one handle per rank: the workspace, whose carve-out layout is identical on every rank
+  // (same dit_config), so a peer's qkv / o / cat / flags sit at my offsets from its base
+  const int P = c->world, me = c->rank;
+  constexpr int H = DIT_IPC_HANDLE_BYTES;
+  std::vector<uint8_t> mine(H + 8), all((size_t)P * (H + 8));
+  bool ok = dit_ipc_export(c->ws, mine.data()) == DIT_OK;
+  const uint64_t wsb = c->ws_bytes;
+  memcpy(mine.data() + H, &wsb, 8);
+  cudaMemset(c->flags, 0, 8 * 4);    // before the all-gather: no peer can signal before it completes
+  // the exchange runs even when the export failed (a zeroed handle marks it), so no rank hangs
+  if (!ok) std::fill(mine.begin(), mine.end(), 0);
+  uint8_t* dev = reinterpret_cast<uint8_t*>(c->sp);
+  cudaMemcpy(dev, mine.data(), mine.size(), cudaMemcpyHostToDevice);
+  if (ncclAllGather(dev, dev + 4096, H + 8, ncclUint8, c->comm, 0) != ncclSuccess) return;
+  if (cudaStreamSynchronize(0) != cudaSuccess) return;
+  cudaMemcpy(all.data(), dev + 4096, all.size(), cudaMemcpyDeviceToHost);
+  for (int r = 0; r < P; ++r) {
+    uint64_t b = 0;
+    memcpy(&b, all.data() + (size_t)r * (H + 8) + H, 8);
+    if (b != wsb) return;              // an export failed (zeroed) or layouts differ: every rank falls back alike
+  }
+  std::vector<void*> opened;
+  uint8_t* base[8] = {};
+  int ok_open = 1;
+  for (int r = 0; r < P && ok_open; ++r) {
+    if (r == me) { base[r] = c->ws; continue; }
+    void* ptr = nullptr;
+    if (dit_ipc_open(all.data() + (size_t)r * (H + 8), &ptr) == DIT_OK) {
+      opened.push_back(ptr);
+      base[r] = static_cast<uint8_t*>(ptr);
+    } else {
+      ok_open = 0;
+    }
+  }
+  // consensus: every rank must have mapped every peer, else all fall back together
+  int* dflag = reinterpret_cast<int*>(dev + 8192);
+  cudaMemcpy(dflag, &ok_open, 4, cudaMemcpyHostToDevice);
+  if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, 0) != ncclSuccess) ok_open = 0;
+  cudaStreamSynchronize(0);
+  int all_ok = 0;
+  cudaMemcpy(&all_ok, dflag, 4, cudaMemcpyDeviceToHost);
+  if (!ok_open || !all_ok) {
+    for (void* x : opened) dit_ipc_close(x);
+    cudaGetLastError();
+    return;
+  }
+  auto at = [&](int r, const void* mine_ptr) {
+    return static_cast<void*>(base[r] + (static_cast<const uint8_t*>(mine_ptr) - c->ws));
+  };
+  for (int r = 0; r < P; ++r) {
+    c->peer_qkv[r] = at(r, c->qkv);
+    c->peer_o[r] = at(r, c->o);
+    c->peer_cat[r] = at(r, c->cat);
+    c->peer_flags.f[r] = static_cast<uint32_t*>(at(r, c->flags));
+  }
+  c->ipc_opened = opened;
+  c->sp_fused = true;
+  c->peers_ready = true;
+  c->sp_epoch = 0;
 }
 
 extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
@@ -914,6 +1012,9 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   c->rank = rank;
   c->plan_B = -1;
   c->rope_key[0] = -1;
+  c->sp_fused = false;
+  const char* nccl_path = getenv("DIT_SP_NCCL");
+  if (world > 1 && world <= 8 && !(nccl_path && nccl_path[0] == '1')) setup_fused_peers(c);
   return DIT_OK;
 }
 
@@ -1227,6 +1328,11 @@ extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
 
 extern "C" int dit_last_launch_count(const dit_ctx* c) { return c ? c->last_launches : 0; }
 
+extern "C" int dit_sp_exchange(const dit_ctx* c) {
+  if (!c || (c->world == 1 && !c->force_sp)) return 0;
+  return c->sp_fused ? 2 : 1;
+}
+
 #define CK(x)                                                                        \
   do {                                                                               \
     int _r = (x);                                                                    \
@@ -1509,6 +1615,29 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   // full sequence -> O in [P][S][N_loc][H/P*d] -> a2a -> scatter into the local rows.
   const int Hl = H / P, Nglob = P * N;
   const bool sp = P > 1 || c->force_sp;   // Ulysses exchange active
+  const bool fused = P > 1 && c->sp_fused;  // ... done by the epilogues over peer memory
+  if (fused && !c->peers_ready) {          // in-process group: every rank has registered by now
+    LocalGroup* g = c->local_group;
+    for (int r = 0; r < P; ++r) {
+      if (!g || !g->qkv[r]) return c->fail(DIT_EPARALLEL, "rank %d of the local group has not called sp_init_local", r);
+      c->peer_qkv[r] = g->qkv[r];
+      c->peer_o[r] = g->o[r];
+      c->peer_cat[r] = g->cat[r];
+      c->peer_flags.f[r] = g->flags[r];
+    }
+    c->peers_ready = true;
+  }
+  // fused exchange barrier: my stores into the peers are done -> tell them; wait for theirs
+  auto exchange_barrier = [&]() -> int {
+    ++c->sp_epoch;
+    prof_begin(c, s);
+    cudaError_t e1 = sp_signal_launch(c->peer_flags, c->rank, P, c->sp_epoch, s);
+    cudaError_t e2 = sp_wait_launch(c->flags, c->rank, P, c->sp_epoch, s);
+    prof_end(c, s, 5, 0.0);
+    c->launches += 2;
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return c->fail(DIT_ECUDA, "sp barrier launch failed");
+    return DIT_OK;
+  };
   auto a2a = [&](const void* snd, void* rcv, size_t count) -> int {
     prof_begin(c, s);
     if (c->comm) {
@@ -1527,7 +1656,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     bf16_t* recv1 = send1 + (size_t)P * pp1;
     bf16_t* send2 = recv1 + (size_t)P * pp1;
     bf16_t* recv2 = send2 + (size_t)P * pp2;
-    if (sp) {
+    if (fused) {
+      CK(exchange_barrier());   // every rank's q/k/v rows are in my attention buffer
+    } else if (sp) {
       CK(a2a(send1, recv1, pp1));
       CKK(sp_gather_qkv_launch(recv1, c->qkv, P, S, Hl, nt, ni, d, s), 6, 0.0);
     }
@@ -1546,7 +1677,13 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     ap.ni = ni;
     ap.Nt = Nt;
     ap.seq_valid = ragged ? c->p_seq_valid : nullptr;
-    if (!sp) {
+    if (fused) {   // O rows straight to their owners' buffers
+      ap.split = 3;
+      ap.out_split = split;
+      ap.ld_out = ld_out;
+      ap.head_off = c->rank * Hl;
+      for (int r = 0; r < P; ++r) ap.out_peer[r] = (out == (void*)c->o) ? c->peer_o[r] : c->peer_cat[r];
+    } else if (!sp) {
       ap.out = out;
       ap.ld_out = ld_out;
       ap.split = split;
@@ -1556,7 +1693,9 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       ap.split = 2;
     }
     CKK(attention_launch(ap, s), 1, 4.0 * S * (double)Nglob * Nglob * Hl * d);
-    if (sp) {
+    if (fused) {
+      CK(exchange_barrier());   // every rank's O rows of my tokens are in my buffer
+    } else if (sp) {
       CK(a2a(send2, recv2, pp2));
       CKK(sp_scatter_o_launch(recv2, out, ld_out, split, P, S, Hl, nt, ni, d, s), 6, 0.0);
     }
@@ -1646,6 +1785,12 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.joint_n = N;
       e.D = D;
       e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
+      if (fused) {
+        for (int r = 0; r < P; ++r) e.qkv_peer[r] = c->peer_qkv[r];
+        e.sp_rank = c->rank;
+        e.sp_nt = nt;
+        e.sp_ni = ni;
+      }
       e.batch = S;
       e.sp_world = P;
       e.rope = c->rope;
@@ -1789,6 +1934,12 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       e.joint_n = N;
       e.D = D;
       e.qkv = (P == 1 && !c->force_sp) ? c->qkv : c->sp;
+      if (fused) {
+        for (int r = 0; r < P; ++r) e.qkv_peer[r] = c->peer_qkv[r];
+        e.sp_rank = c->rank;
+        e.sp_nt = nt;
+        e.sp_ni = ni;
+      }
       e.batch = S;
       e.sp_world = P;
       e.q_gamma = SB.qn;
@@ -2061,6 +2212,29 @@ extern "C" int64_t dit_sp_layout(int32_t which, int32_t world, int32_t rank, int
     for (int rs = 0; rs < P; ++rs)
       for (int b = 0; b < B; ++b)
         for (int i = 0; i < nloc; ++i) put(sp_local_row(1, B, nt, ni, b, i));
+  } else if (which == 5) {
+    // fused exchange, QKV epilogue: (sec, b, head, local row i) -> dest * 3*B*Hl*N + index in
+    // dest's attention buffer (the expression of the EPI_QKV peer store)
+    const int64_t span = (int64_t)3 * B * Hl * N;
+    for (int sec = 0; sec < 3; ++sec)
+      for (int b = 0; b < B; ++b)
+        for (int h = 0; h < H; ++h)
+          for (int i = 0; i < nloc; ++i)
+            put((h / Hl) * span + sp_attn_vec(B, Hl, N, sec, b, h % Hl, sp_global_row(P, nt, ni, rank, i)));
+  } else if (which == 6) {
+    // fused exchange, attention epilogue: (b, global query n, local head hl) -> dest * 2^40 +
+    // element index (row * H + global head) in dest's stream-split O buffer (attn_out_addr itself)
+    AttnParams p;
+    memset(&p, 0, sizeof(p));
+    p.B = B; p.H = Hl; p.N = N; p.split = 3; p.out_split = 1; p.nt = nt; p.ni = ni; p.Nt = Nt;
+    p.ld_out = H; p.head_off = rank * Hl;
+    for (int r = 0; r < P; ++r) p.out_peer[r] = reinterpret_cast<void*>((uintptr_t)r << 41);
+    for (int b = 0; b < B; ++b)
+      for (int n = 0; n < N; ++n)
+        for (int hl = 0; hl < Hl; ++hl) {
+          const uintptr_t a = reinterpret_cast<uintptr_t>(attn_out_addr(p, b, n, hl, 1));
+          put((int64_t)(a >> 41) * ((int64_t)1 << 40) + (int64_t)((a & (((uintptr_t)1 << 41) - 1)) >> 1));
+        }
   } else {
     return -DIT_EINVAL;
   }

@@ -225,6 +225,37 @@ cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uin
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ fused Ulysses exchange barrier
+__global__ void sp_signal_kernel(PeerFlags peers, int me, int P, uint32_t epoch) {
+  const int t = threadIdx.x;
+  if (t < P && t != me) {
+    __threadfence_system();   // the producing kernel's peer stores (earlier on this stream) first
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peers.f[t] + me), "r"(epoch) : "memory");
+  }
+}
+__global__ void sp_wait_kernel(const uint32_t* flags, int me, int P, uint32_t epoch) {
+  const int t = threadIdx.x;
+  if (t < P && t != me) {
+    uint32_t v, spins = 0;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + t) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      __nanosleep(128);
+      if (++spins > (1u << 26)) __trap();   // a peer that never arrives: fail loudly, do not hang
+    }
+  }
+  // the next kernels read the peers' stores, also through TMA (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+cudaError_t sp_signal_launch(const PeerFlags& peers, int me, int P, uint32_t epoch, cudaStream_t s) {
+  sp_signal_kernel<<<1, 32, 0, s>>>(peers, me, P, epoch);
+  return cudaGetLastError();
+}
+cudaError_t sp_wait_launch(const uint32_t* flags, int me, int P, uint32_t epoch, cudaStream_t s) {
+  sp_wait_kernel<<<1, 32, 0, s>>>(flags, me, P, epoch);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ ControlNet push (f2)
 __global__ void __launch_bounds__(256) push_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                                         size_t n16) {

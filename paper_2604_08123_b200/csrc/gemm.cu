@@ -219,8 +219,13 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         const int head = (col0 - sec * D) / d;
         const int hl_n = E.heads / E.sp_world;
         const int dest = head / hl_n, hl = head - dest * hl_n;
-        bf16* dst = reinterpret_cast<bf16*>(E.qkv) +
-                    (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
+        bf16* dst =
+            E.qkv_peer[0] != nullptr
+                ? reinterpret_cast<bf16*>(E.qkv_peer[dest]) +   // fused exchange: the owner's attention buffer
+                      (size_t)sp_attn_vec(E.batch, hl_n, E.sp_world * E.seq_len, sec, b, hl,
+                                          sp_global_row(E.sp_world, E.sp_nt, E.sp_ni, E.sp_rank, E.joint_off + nloc)) * d
+                : reinterpret_cast<bf16*>(E.qkv) +
+                      (size_t)sp_qkv_send_vec(E.batch, hl_n, E.seq_len, dest, sec, b, hl, E.joint_off + nloc) * d;
         const bool nrm = sec < 2 && E.q_gamma != nullptr;   // SD3-medium: no QK-norm (RoPE table = identity)
         if (d == 128) {
           // head in two 64-column halves: half 0 read for the RMS statistic, half 1 read and

@@ -64,6 +64,11 @@ struct EpiParams {
   int qkv_cols;              // 3D (columns beyond go to the GELU branch)
   int heads, head_dim;
   int seq_len;               // rows per (b, h) of q/k/v (= joint_n)
+  // fused Ulysses exchange (qkv_peer[0] != nullptr): every q/k/v row is stored straight into
+  // the attention buffer [3][B][H/P][P*seq_len][d] of the rank that owns its head
+  // (qkv_peer[dest], peer-mapped), at its global joint position; no send buffer, no all-to-all
+  void* qkv_peer[8];
+  int sp_rank, sp_nt, sp_ni;  // this rank, local txt / img rows per request
   // final layer
   const float* lat_in;
   float* lat_out;
@@ -126,6 +131,12 @@ struct AttnParams {
   int Nt;              // global txt rows (SP mode)
   const int* seq_valid;  // device [B] valid joint rows per sequence (ragged batch; nullptr = N):
                          // keys beyond are masked, query rows beyond are written as zeros
+  // split 3 = fused Ulysses exchange: O rows go straight to the owner rank's buffer
+  // out_peer[dest] (peer-mapped) at its local row (out_split: 1 stream-split, 0 joint) and
+  // columns (head_off + h) * d
+  void* out_peer[8];
+  int out_split;
+  int head_off;
 };
 // Output row of query token n (global joint order) of request b; SP mode also
 // returns the destination rank in *dest (rows are then [dest][B][N_loc]).
@@ -163,6 +174,25 @@ __host__ __device__ inline long long sp_local_row(int split, int B, int nt, int 
   if (split) return (i < nt) ? (long long)b * nt + i : (long long)B * nt + (long long)b * ni + (i - nt);
   return (long long)b * (nt + ni) + i;
 }
+
+// Output address of (request b, global query n, local head h) for every split mode.
+__host__ __device__ inline uint16_t* attn_out_addr(const AttnParams& p, int b, int n, int h, int hd) {
+  if (p.split == 3) {
+    int dest, i;
+    if (n < p.Nt) { dest = n / p.nt; i = n - dest * p.nt; }
+    else { dest = (n - p.Nt) / p.ni; i = p.nt + (n - p.Nt) - dest * p.ni; }
+    const long long row = sp_local_row(p.out_split, p.B, p.nt, p.ni, b, i);
+    return static_cast<uint16_t*>(p.out_peer[dest]) + row * p.ld_out + (long long)(p.head_off + h) * hd;
+  }
+  return static_cast<uint16_t*>(p.out) + attn_out_row(p, b, n) * p.ld_out + (long long)h * hd;
+}
+
+// Fused Ulysses exchange barrier over peer-mapped flags: signal stores epoch into every peer's
+// flags[me] (fence.sys + st.release.sys, after the producing kernel on the same stream); wait
+// spins (ld.acquire.sys, bounded -> trap) until flags[src] >= epoch for every peer src.
+struct PeerFlags { uint32_t* f[8]; };
+cudaError_t sp_signal_launch(const PeerFlags& peers, int me, int P, uint32_t epoch, cudaStream_t s);
+cudaError_t sp_wait_launch(const uint32_t* flags, int me, int P, uint32_t epoch, cudaStream_t s);
 
 // ------------------------------------------------------------------ Ulysses SP layout kernels
 // recv [P][3][B][Hl][nloc][d] (chunk r_s = rank r_s's tokens, my heads) ->

@@ -75,6 +75,7 @@ EXPORTS = {
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
     "dit_last_launch_count": (C.c_int, [C.c_void_p]),
+    "dit_sp_exchange": (C.c_int, [C.c_void_p]),
     "dit_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "dit_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_int)]),
@@ -104,6 +105,8 @@ def load_library():
                            "(run `python __graft_entry__.py`); there is no CPU fallback")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in EXPORTS.items():
+        if os.environ.get("DIT_LIB_OVERRIDE") and not hasattr(lib, name):
+            continue   # an older experimental build (perf comparisons only)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

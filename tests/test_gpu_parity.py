@@ -176,13 +176,18 @@ def _shard_step(models, batch, P):
     return lat, v
 
 
+@pytest.mark.parametrize("exchange", ["fused", "a2a"])
 @pytest.mark.parametrize("P,hidden,heads", [(2, 512, 4), (4, 512, 4), (2, 128, 4), (4, 128, 4)])
-def test_sequence_parallel_local_group(torch_cuda, P, hidden, heads):
+def test_sequence_parallel_local_group(torch_cuda, P, hidden, heads, exchange, monkeypatch):
     """Ulysses SP at P ranks (in-process group, one GPU): bitwise equal to P = 1 (pin P10) and oracle parity.
 
     hidden 512 / 4 heads -> d = 128 (tcgen05 attention); hidden 128 / 4 heads -> d = 32 (mma.sync kernel).
+    exchange "fused": the QKV / attention epilogues store straight into the owning rank's buffers with
+    device flag barriers (the default); "a2a": send buffers + all-to-all + gather/scatter kernels
+    (DIT_SP_NCCL=1, the NCCL path's data layout).
     """
     from paper_2604_08123_b200 import dit as D
+    monkeypatch.setenv("DIT_SP_NCCL", "1" if exchange == "a2a" else "0")
     d = hidden // heads
     cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=hidden, heads=heads, depth_single=1,
                               rope_axes=(16, 56, 56) if d == 128 else (4, 14, 14))

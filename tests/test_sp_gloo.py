@@ -88,6 +88,34 @@ def _worker(rank, world, port, B, H, Nt, Ni, errq):
                 lr = b * nt + i if i < nt else B * nt + b * ni + (i - nt)
                 exp_out[lr] = [_code(0, b, h, grow(rank, i), B, H, N) for h in range(H)]
         np.testing.assert_array_equal(out, exp_out)
+
+        # fused exchange (the default at P > 1): the same codes stored one-sidedly at the
+        # peer addresses the QKV / attention epilogues compute (dit_sp_layout 5 / 6); every
+        # rank's puts are all-gathered and each rank keeps those addressed to it
+        span = 3 * B * Hl * N
+        dst = dit.sp_layout(5, world, rank, B, H, Nt, Ni)
+        puts = [torch.empty(2 * codes.size, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(puts, torch.from_numpy(np.concatenate([dst, codes])))
+        attn_f = np.full(span, -1, dtype=np.int64)
+        for pr in puts:
+            d_, c_ = pr.numpy()[:codes.size], pr.numpy()[codes.size:]
+            mine = d_ // span == rank
+            assert (attn_f[d_[mine] % span] == -1).all()           # every slot written once
+            attn_f[d_[mine] % span] = c_[mine]
+        np.testing.assert_array_equal(attn_f, exp_attn)
+        odst = dit.sp_layout(6, world, rank, B, H, Nt, Ni)
+        ocodes = np.array([_code(0, b, rank * Hl + hl, n, B, H, N)
+                           for b in range(B) for n in range(N) for hl in range(Hl)])
+        puts = [torch.empty(2 * ocodes.size, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(puts, torch.from_numpy(np.concatenate([odst, ocodes])))
+        out_f = np.full(B * nloc * H, -1, dtype=np.int64)
+        for pr in puts:
+            d_, c_ = pr.numpy()[:ocodes.size], pr.numpy()[ocodes.size:]
+            mine = d_ >> 40 == rank
+            idx = d_[mine] & ((1 << 40) - 1)
+            assert (out_f[idx] == -1).all()
+            out_f[idx] = c_[mine]
+        np.testing.assert_array_equal(out_f.reshape(B * nloc, H), exp_out)
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent
