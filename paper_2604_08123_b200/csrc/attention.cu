@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant_
     const uint4 val = *reinterpret_cast<const uint4*>(sq + swz_off<HD>(r, c));
     *reinterpret_cast<uint4*>(attn_out_addr(p, b, n, h, HD) + c * 8) = val;
   }
+  if (p.split == 3) __threadfence_system();   // fused exchange: peer stores, system scope
 }
 
 template <int HD>

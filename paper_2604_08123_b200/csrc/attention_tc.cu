@@ -517,6 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
           dst[q] = u;
         }
+        if (p.split == 3) __threadfence_system();   // fused exchange: peer stores, system scope
       }
     }
   }

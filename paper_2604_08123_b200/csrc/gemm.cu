@@ -323,6 +323,9 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
         }
       }
     }
+    // fused exchange: this thread's peer stores reach system scope before the kernel ends
+    // (the barrier kernel's release then covers them on the peer)
+    if (E.qkv_peer[0] != nullptr) __threadfence_system();
     return;
   }
 
