@@ -241,7 +241,7 @@ __global__ void sp_wait_kernel(const uint32_t* flags, int me, int P, uint32_t ep
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + t) : "memory");
       if ((int32_t)(v - epoch) >= 0) break;
       __nanosleep(128);
-      if (++spins > (1u << 26)) __trap();   // a peer that never arrives: fail loudly, do not hang
+      if (++spins > (1u << 28)) __trap();   // a peer that never arrives (~30 s): fail loudly, do not hang
     }
   }
   // the next kernels read the peers' stores, also through TMA (async proxy)

@@ -147,7 +147,7 @@ def test_head_dim_128_tcgen05_attention(torch_cuda, grid, nt):
     check(lat, x_o, "latents")
 
 
-def _shard_step(models, batch, P):
+def _shard_step(models, batch, P, cfg_scale=None):
     """Run one dit_step on P in-process ranks (one host thread + stream each); gather v, latents."""
     import concurrent.futures as cf
     import torch
@@ -165,7 +165,8 @@ def _shard_step(models, batch, P):
         outs.append(out)
         vs.append(v)
         cbs.append(m.make_batch(B, batch.img_h, batch.img_w, nt, batch.adapter_id, batch.sigma, batch.sigma_next,
-                                batch.guidance, lat, out, txt, pooled, v_out=v, cn_scale=batch.cn_scale))
+                                batch.guidance, lat, out, txt, pooled, v_out=v, cn_scale=batch.cn_scale,
+                                cfg_scale=cfg_scale))
         streams.append(torch.cuda.Stream())
     torch.cuda.synchronize()
     with cf.ThreadPoolExecutor(P) as ex:

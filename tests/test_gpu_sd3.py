@@ -179,3 +179,32 @@ def test_sd3_and_cfg_error_paths(torch_cuda):
     bad = dataclasses.replace(cfg, depth_single=1)
     with pytest.raises(D.DitError):
         _model(bad, 1, 16, 8)
+
+
+@pytest.mark.parametrize("exchange", ["fused", "a2a"])
+def test_sd3_cfg_with_sequence_parallel_bitwise(torch_cuda, exchange, monkeypatch):
+    """CFG (2B sequences) under Ulysses SP at P = 2 (in-process group): bitwise = P = 1."""
+    from tests.test_gpu_parity import _shard_step
+    from paper_2604_08123_b200 import dit as D
+    monkeypatch.setenv("DIT_SP_NCCL", "1" if exchange == "a2a" else "0")
+    cfg = CFGS["d128"]
+    B, hh, ww, nt, P = 2, 8, 8, 16, 2
+    batch = synth.make_batch(cfg, B, hh, ww, nt, cfg_scale=4.0)
+    ref = _model(cfg, 2 * B, hh * ww, nt)
+    lat1, v1 = ref.step(batch)
+    ref.close()
+    group = D.load_library().dit_local_group_create(P)
+    ms = []
+    for r in range(P):
+        m = _model(cfg, 2 * B, hh * ww, nt)
+        m.sp_init_local(group, r)
+        ms.append(m)
+    # _shard_step shards latents / txt per rank; CFG needs both prompts' rows per rank
+    both = dataclasses.replace(batch, txt=np.concatenate([batch.txt, batch.txt_neg]),
+                               pooled=np.concatenate([batch.pooled, batch.pooled_neg]))
+    latP, vP = _shard_step(ms, both, P, cfg_scale=batch.cfg_scale)
+    np.testing.assert_array_equal(vP, v1)
+    np.testing.assert_array_equal(latP, lat1)
+    for m in ms:
+        m.close()
+    D.load_library().dit_local_group_destroy(group)
