@@ -345,6 +345,11 @@ int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N, int32_t d,
                         void* out, void* stream);
 
+/* Bench/test-only: out = bf16(A W^T + bias) through the step's tcgen05 GEMM (A [M][K],
+ * W [N][K], bias [N], out [M][N], all device bf16; K % 64 == 0).  Asynchronous on stream. */
+int dit_debug_gemm(const void* A, const void* W, const void* bias, void* out, int32_t M, int32_t N, int32_t K,
+                   void* stream);
+
 /* Debug-only: record a clock64 timeline of CTA 0's first work item of the
  * tcgen05 attention kernel into buf (device int64 [20 events][64 kv tiles]);
  * NULL disables (the default). */

@@ -366,9 +366,11 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
     load_bias32(bias, col, P.N, bv);
 #pragma unroll
     for (int e = 0; e < 32; ++e) y[e] = __uint_as_float(rr2[hh * 32 + e]) + bv[e];
-    if (E.kind == EPI_GELU) {
+    if (E.kind == EPI_GELU || E.kind == EPI_BIAS) {
+      if (E.kind == EPI_GELU) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) y[e] = gelu_tanh_f(y[e]);
+        for (int e = 0; e < 32; ++e) y[e] = gelu_tanh_f(y[e]);
+      }
       store_bf16_32(reinterpret_cast<bf16*>(E.out) + (size_t)r * E.ld_out + E.out_col0 + col, y, valid);
     } else if (E.kind == EPI_STORE_H) {
       float* hp = E.h + (size_t)jrow * E.D + col;

@@ -26,6 +26,7 @@ enum EpiKind : int {
   EPI_RESID = 3,    // h[jrow][c] += gate_b[c] * (acc + bias) (+ cn_scale_b * R_b[n][c])
   EPI_FINAL = 4,    // v = acc + bias; lat_out = lat_in + dsig_b * v
   EPI_SHRINK = 5,   // S[r][slot*r_alloc + c] = row_slot(r)==slot ? bf16(scale_slot*acc) : 0
+  EPI_BIAS = 6,     // out[r][out_col0 + c] = bf16(acc + bias)  (plain projection; library-bar runs)
 };
 
 struct EpiParams {

@@ -87,6 +87,8 @@ EXPORTS = {
     "sp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "dit_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "dit_debug_attention_trace": (C.c_int, [C.c_void_p]),
+    "dit_debug_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                 C.c_void_p]),
     "dit_debug_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_void_p, C.c_void_p]),
     "dit_sp_layout": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

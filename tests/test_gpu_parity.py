@@ -323,3 +323,24 @@ def test_controlnet_device_flag_deferred_fetch(torch_cuda):
         lat, v = m.step(batch)
         np.testing.assert_array_equal(v, ref_v)
         np.testing.assert_array_equal(lat, ref_lat)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 520, 192), (4096, 3072, 3072), (1000, 21504, 64)])
+def test_debug_gemm_vs_torch_fp32(torch_cuda, M, N, K):
+    """The step's tcgen05 GEMM alone (dit_debug_gemm, EPI_BIAS) against a PyTorch fp32 matmul:
+    ragged M / N tails, a single K block, a Flux-size projection."""
+    import ctypes as C
+    import torch
+    from paper_2604_08123_b200 import dit
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * K ** -0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16)
+    y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream()
+    assert dit.load_library().dit_debug_gemm(x.data_ptr(), w.data_ptr(), bias.data_ptr(), y.data_ptr(), M, N, K,
+                                             C.c_void_p(s.cuda_stream)) == 0
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().T + bias.float()
+    err = ((y.float() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 8e-3, err
