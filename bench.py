@@ -317,13 +317,17 @@ def run_gpu(args):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         one_step()
+        marks[i].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
+    per_step = sorted([e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, args.steps)])
+    pct = lambda q: per_step[min(len(per_step) - 1, int(round(q * (len(per_step) - 1))))]
     clk = clocks.stop()
     model.profile(False)
     prof = {k: model.profile_read(k) for k in list(range(7)) + list(range(10, 19))}
@@ -381,6 +385,7 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "step_ms_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": wl["desc"], "name": args.workload, "global_batch": B, "seq_len": H_ * W_ + NT,
