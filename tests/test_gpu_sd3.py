@@ -208,3 +208,20 @@ def test_sd3_cfg_with_sequence_parallel_bitwise(torch_cuda, exchange, monkeypatc
     for m in ms:
         m.close()
     D.load_library().dit_local_group_destroy(group)
+
+
+def test_sd35_large_width_parity(torch_cuda):
+    """SD3.5-Large width (D = 2432 = 9.5 GEMM tiles, 38 x 64 heads, QK-RMSNorm), 2 joint blocks,
+    32 x 32 latent grid + 333 text tokens, B = 1 with CFG 3.5, a rank-16 LoRA."""
+    cfg = dataclasses.replace(synth.SD35_LARGE, depth_double=2)
+    hh = ww = 32
+    nt = synth.SD3_TXT_TOKENS
+    m = _model(cfg, 2, hh * ww, nt, rank=16, adapters=1)
+    m.register_synthetic_lora(3, rank=16, index=0, scale=0.5)
+    batch = synth.make_batch(cfg, 1, hh, ww, nt, cfg_scale=3.5)
+    batch.adapter_id = np.array([3], dtype=np.int32)
+    lat, v = m.step(batch)
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    x_o, v_o = S.dit_step(cfg, W, batch, {3: oracle_adapter(cfg, 16, 0, scale=0.5)[0]})
+    check(v, v_o, "v")
+    check(lat, x_o, "latents_out")
