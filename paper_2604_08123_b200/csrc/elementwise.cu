@@ -298,7 +298,10 @@ cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uin
 // mma.sync m16n8k16 (r <= 128: 8 K-steps at most) with the B rows (A operand) and the
 // A columns (B operand, ldmatrix .trans from its [k][n] storage) staged in shared memory.
 // Bandwidth-bound: 2 bytes read + 2 written per weight (+ the tiny factors).
-constexpr int LM_TILE = 128, LM_ROWS = 64, LM_PAD = 8, LM_MAXR = 128;   // tile: LM_ROWS x LM_TILE
+#ifndef LORA_MERGE_ROWS
+#define LORA_MERGE_ROWS 128
+#endif
+constexpr int LM_TILE = 128, LM_ROWS = LORA_MERGE_ROWS, LM_PAD = 8, LM_MAXR = 128;   // tile: LM_ROWS x LM_TILE
 
 DEVI void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -309,7 +312,7 @@ DEVI void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uin
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
 }
 
-__global__ void __launch_bounds__(LM_ROWS * 2, 6) lora_merge_kernel(const bf16* __restrict__ W, const bf16* __restrict__ A,
+__global__ void __launch_bounds__(LM_ROWS * 2, LM_ROWS == 64 ? 6 : 3) lora_merge_kernel(const bf16* __restrict__ W, const bf16* __restrict__ A,
                                                          const bf16* __restrict__ Bm, bf16* __restrict__ out, int rows,
                                                          int cols, int ra, float scale) {
   // smem: W tile [LM_ROWS][128 + PAD] (staged in and out with 16-byte coalesced copies), B rows of
