@@ -196,7 +196,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant_
     *reinterpret_cast<uint32_t*>(sq + swz_off<HD>(r1, col / 8) + (col % 8) * 2) = pack_bf16(o[i][2] * inv1, o[i][3] * inv1);
   }
   __syncthreads();
-  bf16* out = reinterpret_cast<bf16*>(p.out);
   for (int i = tid; i < C::BQ * C::CHUNKS; i += 256) {
     const int r = i / C::CHUNKS, c = i % C::CHUNKS;
     const int n = q0 + r;
