@@ -802,12 +802,17 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
       return c->fail(DIT_EINVAL, "tensor map for the merged copy failed");
     off = align_up(off + (size_t)L.out * L.in * 2, 256);
   }
+  // tensor-core merge (merge_tc.cu); DIT_MERGE_MMA_SYNC=1 selects the mma.sync kernel (comparison)
+  const char* legacy = getenv("DIT_MERGE_MMA_SYNC");
+  const bool use_tc = !(legacy && legacy[0] == '1') && (ra == 64 || ra == 128);
   for (size_t k = 0; k < lins.size(); ++k) {
     Lin& L = *lins[k].first;
     const LoraPool& P = c->pools[lins[k].second];
-    cudaError_t e = lora_merge_launch(L.w, static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
-                                      static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2,
-                                      static_cast<uint8_t*>(merged) + offs[k], L.out, L.in, ra, scale, s);
+    const uint8_t* Aslot = static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2;
+    const uint8_t* Bslot = static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2;
+    cudaError_t e = use_tc ? lora_merge_tc_launch(L.tm, maps[k], Aslot, Bslot, L.out, L.in, ra, scale, s)
+                           : lora_merge_launch(L.w, Aslot, Bslot, static_cast<uint8_t*>(merged) + offs[k], L.out,
+                                               L.in, ra, scale, s);
     if (e != cudaSuccess) return c->fail(DIT_ECUDA, "lora_merge kernel: %s", cudaGetErrorString(e));
   }
   for (size_t k = 0; k < lins.size(); ++k) {

@@ -235,6 +235,10 @@ cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uin
 // one-thread kernel: fence.sys + st.release.sys *flag = value.
 cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
                                    int num_sms, cudaStream_t s);
+// Merged LoRA on the tensor cores (merge_tc.cu): same result as lora_merge_launch; w_map / out_map
+// are the [rows][cols] box {64, 128} maps of W and of the output; ra in {64, 128}.
+cudaError_t lora_merge_tc_launch(const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
+                                 int rows, int cols, int ra, float scale, cudaStream_t s);
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 

@@ -37,9 +37,14 @@ def _merged_modules(m, cfg):
     return out
 
 
-def test_merged_weights_match_numpy(torch_cuda):
-    cfg = synth.TINY_SINGLE
-    rank, scale = 8, 0.75
+@pytest.mark.parametrize("wide,rank", [(False, 8), (True, 100)])
+def test_merged_weights_match_numpy(torch_cuda, wide, rank):
+    """rank 8 (r_alloc 64) on 64-wide tiles; rank 100 (r_alloc 128, two K panels) on a 256-wide model
+    (ragged 128 x 128 merge tiles at the F + D = 1280 / 768 edges)."""
+    import dataclasses
+    cfg = (dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, rope_axes=(16, 56, 56)) if wide
+           else synth.TINY_SINGLE)
+    scale = 0.75
     m = _model(cfg, 2, 16, 8, rank=rank, adapters=2)
     m.register_synthetic_lora(5, rank=rank, index=1, scale=scale)
     m.lora_merge(5)
@@ -51,9 +56,13 @@ def test_merged_weights_match_numpy(torch_cuda):
         ref = bf16_to_f64(W[mod + ".w"]) + scale * bf16_to_f64(L[mod + ".lora_B"]) @ bf16_to_f64(L[mod + ".lora_A"])
         want = _bf16_rne(ref)
         g = got[mod]
-        # same value up to one bf16 ulp (fp32 accumulation order), and almost always exact
+        # same value up to one bf16 ulp (fp32 accumulation order), and almost always exact; more
+        # than one ulp only where W and s B A cancel (absolute error far below the tensor's scale)
         ulp = np.abs(g.astype(np.int64) - want.astype(np.int64))
-        assert ulp.max() <= 1, (mod, int(ulp.max()))
+        far = ulp > 1
+        if far.any():
+            err = np.abs(bf16_to_f64(g) - ref)[far]
+            assert err.max() <= 1e-5 * np.abs(ref).max(), (mod, int(ulp.max()), float(err.max()))
         assert (ulp == 0).mean() > 0.99, (mod, float((ulp == 0).mean()))
 
 
