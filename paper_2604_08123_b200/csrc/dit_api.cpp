@@ -197,6 +197,7 @@ struct dit_ctx {
   bf16_t* sext = nullptr;
   bf16_t* xb = nullptr;
   float* vcfg = nullptr;             // CFG: v of every sequence [2][B][ni][C] (cond block, uncond block)
+  uint8_t* mjobs = nullptr;          // lora_merge: device job table (one per adapted linear)
   float2* rope = nullptr;
   float* mod = nullptr;
   float* vec = nullptr;
@@ -302,7 +303,8 @@ bool cfg_valid(const dit_config* c, std::string* why) {
 }
 
 struct Layout {
-  size_t h, u, qkv, sp, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, vcfg, total;
+  size_t h, u, qkv, sp, o, cat, sext, xb, rope, mod, vec, h1, xprep, temb, segs, params, rowspace, pools, vcfg, mjobs,
+      total;
   size_t pool_bytes_per_slot;
 };
 
@@ -325,6 +327,7 @@ Layout layout_of(const dit_config& c) {
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
   L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
   L.vcfg = cv.take(2 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);   // CFG: v of both branches
+  L.mjobs = cv.take((size_t)n_lora_modules(c) * merge_job_bytes());   // lora_merge job table
   L.rope = cv.take((size_t)c.max_batch * N * (d / 2) * 8);   // one table per sequence for ragged batches
   L.mod = cv.take(8 * mod_total * 4);
   L.vec = cv.take(8 * D * 4);
@@ -398,6 +401,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   c->sext = reinterpret_cast<bf16_t*>(w + L.sext);
   c->xb = reinterpret_cast<bf16_t*>(w + L.xb);
   c->vcfg = reinterpret_cast<float*>(w + L.vcfg);
+  c->mjobs = w + L.mjobs;
   c->rope = reinterpret_cast<float2*>(w + L.rope);
   c->mod = reinterpret_cast<float*>(w + L.mod);
   c->vec = reinterpret_cast<float*>(w + L.vec);
@@ -805,15 +809,35 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
   // tensor-core merge (merge_tc.cu); DIT_MERGE_MMA_SYNC=1 selects the mma.sync kernel (comparison)
   const char* legacy = getenv("DIT_MERGE_MMA_SYNC");
   const bool use_tc = !(legacy && legacy[0] == '1') && (ra == 64 || ra == 128);
-  for (size_t k = 0; k < lins.size(); ++k) {
-    Lin& L = *lins[k].first;
-    const LoraPool& P = c->pools[lins[k].second];
-    const uint8_t* Aslot = static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2;
-    const uint8_t* Bslot = static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2;
-    cudaError_t e = use_tc ? lora_merge_tc_launch(L.tm, maps[k], Aslot, Bslot, L.out, L.in, ra, scale, s)
-                           : lora_merge_launch(L.w, Aslot, Bslot, static_cast<uint8_t*>(merged) + offs[k], L.out,
-                                               L.in, ra, scale, s);
+  if (use_tc) {   // one job per adapted linear, one persistent launch
+    const size_t jb = merge_job_bytes();
+    uint8_t* host = static_cast<uint8_t*>(aligned_alloc(64, align_up(lins.size() * jb, 64)));
+    if (!host) return c->fail(DIT_ENOMEM, "host job table");
+    int tiles = 0;
+    for (size_t k = 0; k < lins.size(); ++k) {
+      Lin& L = *lins[k].first;
+      const LoraPool& P = c->pools[lins[k].second];
+      if (!merge_job_fill(host + k * jb, L.tm, maps[k], static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
+                          static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, L.out, L.in, ra, scale,
+                          tiles)) {
+        free(host);
+        return c->fail(DIT_EINVAL, "tensor map for the merge operands failed");
+      }
+      tiles += merge_job_tiles(host + k * jb);
+    }
+    cudaMemcpyAsync(c->mjobs, host, lins.size() * jb, cudaMemcpyHostToDevice, s);   // (staged: host reusable)
+    free(host);
+    cudaError_t e = lora_merge_tc_launch(c->mjobs, (int)lins.size(), tiles, ra, c->num_sms, s);
     if (e != cudaSuccess) return c->fail(DIT_ECUDA, "lora_merge kernel: %s", cudaGetErrorString(e));
+  } else {
+    for (size_t k = 0; k < lins.size(); ++k) {
+      Lin& L = *lins[k].first;
+      const LoraPool& P = c->pools[lins[k].second];
+      cudaError_t e = lora_merge_launch(L.w, static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
+                                        static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2,
+                                        static_cast<uint8_t*>(merged) + offs[k], L.out, L.in, ra, scale, s);
+      if (e != cudaSuccess) return c->fail(DIT_ECUDA, "lora_merge kernel: %s", cudaGetErrorString(e));
+    }
   }
   for (size_t k = 0; k < lins.size(); ++k) {
     lins[k].first->tm_m = maps[k];

@@ -235,10 +235,16 @@ cudaError_t delayed_publish_launch(void* dst, const void* src, size_t bytes, uin
 // one-thread kernel: fence.sys + st.release.sys *flag = value.
 cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
                                    int num_sms, cudaStream_t s);
-// Merged LoRA on the tensor cores (merge_tc.cu): same result as lora_merge_launch; w_map / out_map
-// are the [rows][cols] box {64, 128} maps of W and of the output; ra in {64, 128}.
-cudaError_t lora_merge_tc_launch(const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
-                                 int rows, int cols, int ra, float scale, cudaStream_t s);
+// Merged LoRA on the tensor cores (merge_tc.cu), one persistent launch over every adapted
+// linear: the host fills one job per linear (merge_job_fill: w_map / out_map = the [rows][cols]
+// box {64, 128} maps of W and of the output, tile_begin = running tile count) into device memory
+// (merge_job_bytes each, 64-byte aligned); ra in {64, 128}.  Same result as lora_merge_launch.
+size_t merge_job_bytes();
+bool merge_job_fill(void* job, const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
+                    int rows, int cols, int ra, float scale, int tile_begin);
+int merge_job_tiles(const void* job);
+cudaError_t lora_merge_tc_launch(const void* jobs_dev, int njobs, int total_tiles, int ra, int num_sms,
+                                 cudaStream_t s);
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 

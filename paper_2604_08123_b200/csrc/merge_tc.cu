@@ -6,6 +6,8 @@
 // accumulator row from TMEM, adds it into the W row in shared memory, and one thread TMA-stores
 // the patched tile.  Global traffic is the W read + W' write (the factors are L2-resident), all
 // of it as TMA bulk copies; the product costs no CUDA-core time.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -42,8 +44,19 @@ struct Maps {
 template <int RA>
 constexpr int smem_bytes() { return (RA / 64) * 16384 + 2 * RA * 128 + 32768 + 1024 + 64; }
 
+// One adapted linear of the merge: its maps live in device memory (64-byte aligned, written
+// by the host before the launch), tiles [tile_begin, tile_begin + tiles) of the global list.
+struct alignas(64) Job {
+  Maps m;
+  int tile_begin, tiles, tiles_n;
+  float scale;
+};
+
+// Persistent: each CTA walks the global tile list of ALL adapted linears (one launch per
+// merge: no per-module launch tails), one TMEM allocation and one barrier pair per CTA,
+// phases tracked per tile.
 template <int RA>
-__global__ void __launch_bounds__(THREADS) merge_tc_kernel(const __grid_constant__ Maps m, float scale) {
+__global__ void __launch_bounds__(THREADS) merge_tc_kernel(const Job* __restrict__ jobs, int njobs, int total) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int KP = RA / 64;
@@ -52,10 +65,8 @@ __global__ void __launch_bounds__(THREADS) merge_tc_kernel(const __grid_constant
   uint8_t* sW = sA + 2 * RA * 128;       // 2 x [128 rows][64 cols]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + 32768);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-  const int c0 = blockIdx.x * TILE, r0 = blockIdx.y * TILE;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&m.w);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_barrier_init();
@@ -65,75 +76,101 @@ __global__ void __launch_bounds__(THREADS) merge_tc_kernel(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bars[0], KP * 16384 + 2 * RA * 128 + 32768);
-    for (int p = 0; p < KP; ++p) tma_load_2d(&m.b, &bars[0], sB + p * 16384, p * 64, r0);
-    for (int p = 0; p < 2; ++p) tma_load_2d(&m.a, &bars[0], sA + p * RA * 128, c0 + p * 64, 0);
-    for (int p = 0; p < 2; ++p) tma_load_2d(&m.w, &bars[0], sW + p * 16384, c0 + p * 64, r0);
-    mbar_wait(&bars[0], 0);
-    tc_fence_after();
-    constexpr uint32_t idesc = idesc_bf16_f32(TILE, TILE) | (1u << 16);   // A K-major, B MN-major
-    const uint64_t bdesc = desc_mn_sw128(smem_u32(sA), RA * 128);
-#pragma unroll
-    for (int k = 0; k < RA / 16; ++k)
-      tc_mma_f16(tmem, smem_desc_k_sw128(smem_u32(sB + (k / 4) * 16384)) + 2 * (k % 4),
-                 bdesc + (uint64_t)(k * 128), idesc, k > 0);
-    tc_commit(&bars[1]);
-  }
-  __syncwarp();
-  // every thread: one tile row (TMEM lane), 4 x 32 accumulator columns into the swizzled W row
-  mbar_wait(&bars[1], 0);
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    uint32_t acc[32];
-    tmem_ld32(taddr + cc * 32, acc);
-    tmem_ld_wait();
-    uint8_t* prow = sW + (cc / 2) * 16384 + row * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = (cc % 2) * 4 + q;                                   // logical 16-byte chunk
-      uint4* pc = reinterpret_cast<uint4*>(prow + ((j ^ (row & 7)) << 4));   // SWIZZLE_128B
-      uint4 w = *pc;
-      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        ws[e] = pack_bf16(bf16_lo(ws[e]) + scale * __uint_as_float(acc[q * 8 + 2 * e]),
-                          bf16_hi(ws[e]) + scale * __uint_as_float(acc[q * 8 + 2 * e + 1]));
-      *pc = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+  int it = 0;
+  for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    int lo = 0, hi = njobs - 1;           // the job holding tile t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (jobs[mid].tile_begin <= t) lo = mid; else hi = mid - 1;
     }
-  }
-  fence_async_shared();   // the patched rows (generic proxy) -> the TMA store (async proxy)
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int p = 0; p < 2; ++p) tma_store_2d(&m.out, sW + p * 16384, c0 + p * 64, r0);
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 0) {
+    const Job& J = jobs[lo];
+    const int lt = t - J.tile_begin;
+    const int c0 = (lt % J.tiles_n) * TILE, r0 = (lt / J.tiles_n) * TILE;
+    const float scale = J.scale;
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bars[0], KP * 16384 + 2 * RA * 128 + 32768);
+      for (int p = 0; p < KP; ++p) tma_load_2d(&J.m.b, &bars[0], sB + p * 16384, p * 64, r0);
+      for (int p = 0; p < 2; ++p) tma_load_2d(&J.m.a, &bars[0], sA + p * RA * 128, c0 + p * 64, 0);
+      for (int p = 0; p < 2; ++p) tma_load_2d(&J.m.w, &bars[0], sW + p * 16384, c0 + p * 64, r0);
+      mbar_wait(&bars[0], it & 1);
+      tc_fence_after();
+      constexpr uint32_t idesc = idesc_bf16_f32(TILE, TILE) | (1u << 16);   // A K-major, B MN-major
+      const uint64_t bdesc = desc_mn_sw128(smem_u32(sA), RA * 128);
+#pragma unroll
+      for (int k = 0; k < RA / 16; ++k)
+        tc_mma_f16(tmem, smem_desc_k_sw128(smem_u32(sB + (k / 4) * 16384)) + 2 * (k % 4),
+                   bdesc + (uint64_t)(k * 128), idesc, k > 0);
+      tc_commit(&bars[1]);
+    }
+    __syncwarp();
+    // every thread: one tile row (TMEM lane), 4 x 32 accumulator columns into the swizzled W row
+    mbar_wait(&bars[1], it & 1);
     tc_fence_after();
-    tmem_dealloc<128>(tmem);
+    const int row = warp * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t acc[32];
+      tmem_ld32(taddr + cc * 32, acc);
+      tmem_ld_wait();
+      uint8_t* prow = sW + (cc / 2) * 16384 + row * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = (cc % 2) * 4 + q;                                       // logical 16-byte chunk
+        uint4* pc = reinterpret_cast<uint4*>(prow + ((j ^ (row & 7)) << 4));   // SWIZZLE_128B
+        uint4 w = *pc;
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          ws[e] = pack_bf16(bf16_lo(ws[e]) + scale * __uint_as_float(acc[q * 8 + 2 * e]),
+                            bf16_hi(ws[e]) + scale * __uint_as_float(acc[q * 8 + 2 * e + 1]));
+        *pc = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+      }
+    }
+    fence_async_shared();   // the patched rows (generic proxy) -> the TMA store (async proxy)
+    tc_fence_before();
+    __syncthreads();        // (also: every thread's TMEM reads are done before the next MMA)
+    if (threadIdx.x == 0) {
+      for (int p = 0; p < 2; ++p) tma_store_2d(&J.m.out, sW + p * 16384, c0 + p * 64, r0);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // sW reusable
+    }
+    __syncthreads();
+    tc_fence_after();
   }
+  if (warp == 0) tmem_dealloc<128>(tmem);
 }
 
 }  // namespace merge_tc
 
-cudaError_t lora_merge_tc_launch(const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
-                                 int rows, int cols, int ra, float scale, cudaStream_t s) {
+size_t merge_job_bytes() { return sizeof(merge_tc::Job); }
+
+bool merge_job_fill(void* job, const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
+                    int rows, int cols, int ra, float scale, int tile_begin) {
   using namespace merge_tc;
-  if (ra != 64 && ra != 128) return cudaErrorInvalidValue;
-  Maps m;
-  m.w = w_map;
-  m.out = out_map;
-  if (!make_tmap_2d(&m.b, Bm, ra, rows, (uint64_t)ra * 2, 64, 128) ||
-      !make_tmap_2d(&m.a, A, cols, ra, (uint64_t)cols * 2, 64, ra))
-    return cudaErrorInvalidValue;
+  Job* J = static_cast<Job*>(job);
+  J->m.w = w_map;
+  J->m.out = out_map;
+  if (!make_tmap_2d(&J->m.b, Bm, ra, rows, (uint64_t)ra * 2, 64, 128) ||
+      !make_tmap_2d(&J->m.a, A, cols, ra, (uint64_t)cols * 2, 64, ra))
+    return false;
+  J->tiles_n = (cols + TILE - 1) / TILE;
+  J->tiles = J->tiles_n * ((rows + TILE - 1) / TILE);
+  J->tile_begin = tile_begin;
+  J->scale = scale;
+  return true;
+}
+
+int merge_job_tiles(const void* job) { return static_cast<const merge_tc::Job*>(job)->tiles; }
+
+cudaError_t lora_merge_tc_launch(const void* jobs_dev, int njobs, int total_tiles, int ra, int num_sms,
+                                 cudaStream_t s) {
+  using namespace merge_tc;
+  if ((ra != 64 && ra != 128) || njobs < 1 || total_tiles < 1) return cudaErrorInvalidValue;
+  const Job* jobs = static_cast<const Job*>(jobs_dev);
   static bool attr64 = false, attr128 = false;
-  dim3 grid((cols + TILE - 1) / TILE, (rows + TILE - 1) / TILE);
+  const int per_sm = ra == 64 ? 3 : 2;
+  const int grid = std::min(total_tiles, num_sms * per_sm);
   if (ra == 64) {
     if (!attr64) {
       cudaError_t e = cudaFuncSetAttribute(merge_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -141,7 +178,7 @@ cudaError_t lora_merge_tc_launch(const CUtensorMap& w_map, const CUtensorMap& ou
       if (e != cudaSuccess) return e;
       attr64 = true;
     }
-    merge_tc_kernel<64><<<grid, THREADS, smem_bytes<64>(), s>>>(m, scale);
+    merge_tc_kernel<64><<<grid, THREADS, smem_bytes<64>(), s>>>(jobs, njobs, total_tiles);
   } else {
     if (!attr128) {
       cudaError_t e = cudaFuncSetAttribute(merge_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -149,7 +186,7 @@ cudaError_t lora_merge_tc_launch(const CUtensorMap& w_map, const CUtensorMap& ou
       if (e != cudaSuccess) return e;
       attr128 = true;
     }
-    merge_tc_kernel<128><<<grid, THREADS, smem_bytes<128>(), s>>>(m, scale);
+    merge_tc_kernel<128><<<grid, THREADS, smem_bytes<128>(), s>>>(jobs, njobs, total_tiles);
   }
   return cudaGetLastError();
 }
