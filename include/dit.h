@@ -350,6 +350,11 @@ int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, 
 int dit_debug_gemm(const void* A, const void* W, const void* bias, void* out, int32_t M, int32_t N, int32_t K,
                    void* stream);
 
+/* Bench-only: h[M][N] (device fp32) += gate[N] (device fp32) * (A W^T + bias) through the step's
+ * GEMM with its gated-residual epilogue (N % 32 == 0).  Asynchronous on stream. */
+int dit_debug_gemm_resid(const void* A, const void* W, const void* bias, float* h, const float* gate, int32_t M,
+                         int32_t N, int32_t K, void* stream);
+
 /* Debug-only: record a clock64 timeline of CTA 0's first work item of the
  * tcgen05 attention kernel into buf (device int64 [20 events][64 kv tiles]);
  * NULL disables (the default). */

@@ -2200,6 +2200,42 @@ extern "C" int dit_debug_gemm(const void* A, const void* W, const void* bias, vo
   return gemm_launch(a, sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
 }
 
+// Bench-only: the gated-residual projection of the step alone: h[M][N] (fp32) += gate[N] * (A W^T +
+// bias) through the same GEMM + EPI_RESID epilogue (profiling the epilogue's cost).
+extern "C" int dit_debug_gemm_resid(const void* A, const void* W, const void* bias, float* h, const float* gate,
+                                    int32_t M, int32_t N, int32_t K, void* stream) {
+  if (!A || !W || !bias || !h || !gate || M < 1 || N < 1 || K < 64 || K % 64 || N % 32) return DIT_EINVAL;
+  GemmProblem P;
+  memset(&P, 0, sizeof(P));
+  if (!make_tmap_2d(&P.tmA, A, K, M, (uint64_t)K * 2, 64, GEMM_BM) ||
+      !make_tmap_2d(&P.tmB, W, K, N, (uint64_t)K * 2, 64, 128))
+    return DIT_EINVAL;
+  P.M = M;
+  P.N = N;
+  P.K = K;
+  P.tiles_m = (M + GEMM_TM - 1) / GEMM_TM;
+  P.tiles_n = (N + GEMM_BN - 1) / GEMM_BN;
+  P.num_tiles = P.tiles_m * P.tiles_n;
+  P.epi.kind = EPI_RESID;
+  P.epi.bias = bias;
+  P.epi.h = h;
+  P.epi.D = N;
+  P.epi.rows_per_req = M;
+  P.epi.joint_n = M;
+  P.epi.mod = gate;
+  P.epi.mod_stride = 0;
+  P.epi.gate_off = 0;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.p[0] = P;
+  a.num_problems = 1;
+  a.total_tiles = P.num_tiles;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return gemm_launch(a, sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
 // Test/bench-only: one attention launch on head-major q/k/v [B][H][N][d] (bf16),
 // O written joint-row-major [B*N][H*d] (d = 128 -> tcgen05 kernel).
 extern "C" int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N,
