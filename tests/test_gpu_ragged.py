@@ -123,3 +123,36 @@ def test_ragged_error_paths(torch_cuda):
     assert e.value.code == D.CODES["DIT_EPARALLEL"]
     m.close()
     D.load_library().dit_local_group_destroy(group)
+
+
+def test_step_flops_accounting(torch_cuda):
+    """dit_step_flops (the bench's algorithmic FLOPs): a ragged batch counts each request at its own
+    grid (= the sum of the requests alone), CFG doubles the work, SD3's context_pre_only last block
+    drops its text proj / MLP."""
+    cfg = FLUX128
+    m = _model(cfg, 4, 80, 24)
+    batch = synth.make_batch(cfg, 3, 8, 10, 24)
+    batch.img_hw = np.array([[8, 8], [6, 10], [5, 7]], dtype=np.int32)
+
+    def flops(b):
+        lat, txt, pooled, out, v = m.device_inputs(b)
+        cb = m.make_batch(b.batch, b.img_h, b.img_w, b.txt_tokens, b.adapter_id, b.sigma, b.sigma_next, b.guidance,
+                          lat, out, txt, pooled, cfg_scale=b.cfg_scale, img_hw=b.img_hw)
+        return m.step_flops(cb)
+
+    total = flops(batch)
+    alone = sum(flops(_alone(batch, i)) for i in range(3))
+    assert abs(total - alone) <= 1e-9 * alone
+    one = _alone(batch, 0)
+    assert abs(flops(dataclasses.replace(one, cfg_scale=np.ones(1, np.float32), txt_neg=one.txt,
+                                         pooled_neg=one.pooled)) - 2 * flops(one)) <= 1e-9 * flops(one)
+    sd3 = dataclasses.replace(synth.SD3_TINY, hidden=128, heads=2, depth_double=2, pos_embed_max=12)
+    ms = _model(sd3, 1, 64, 8)
+    b3 = synth.make_batch(sd3, 1, 8, 8, 8)
+    lat, txt, pooled, out, v = ms.device_inputs(b3)
+    cb = ms.make_batch(1, 8, 8, 8, b3.adapter_id, b3.sigma, b3.sigma_next, b3.guidance, lat, out, txt, pooled)
+    D, F, N, Nt, Ni = 128, 512, 72, 8, 64
+    expect = (2 * Ni * D * 16 + 2 * Nt * D * 32 + 2 * Ni * D * 16
+              + 2 * (2 * N * D * 3 * D + 2 * N * D * D + 2 * 2 * N * D * F + 4 * N * N * D)
+              - (2 * Nt * D * D + 2 * 2 * Nt * D * F))
+    assert abs(ms.step_flops(cb) - expect) <= 1e-9 * expect
