@@ -261,7 +261,27 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           }
           continue;
         }
-        // generic head size (d = 32 / 64 test configurations): two passes of 32 columns
+        if (d == 64) {
+          // SD3 / SD3.5 heads: the whole head in one pair of TMEM reads, the RMS statistic and the
+          // normalise(+RoPE) pass from registers (2 TMEM reads per head instead of 4)
+          float y[64];
+          load_head_half(tbase + c0, bias + col0, y);   // (tcgen05.ld: all lanes)
+          if (nrm) {
+            float ss = 0.f;
+#pragma unroll
+            for (int e = 0; e < 64; ++e) ss = fmaf(y[e], y[e], ss);
+            const bf16* g = reinterpret_cast<const bf16*>(sec == 0 ? E.q_gamma : E.k_gamma);
+            const float4* cs = reinterpret_cast<const float4*>(E.rope + (size_t)b * E.rope_stride +
+                                                               (size_t)(E.joint_off + nloc) * (d / 2));
+            norm_rope_half(y, rsqrtf(ss / 64.f + 1e-6f), g, cs);
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 32) store_bf16_32(dst + j, *reinterpret_cast<const float(*)[32]>(&y[j]), 32);
+          }
+          continue;
+        }
+        // generic head size (d = 32 test configurations): two passes of 32 columns
         // pass 1: sum of squares over the head (q, k only)
         float rs = 1.f;
         if (nrm) {
