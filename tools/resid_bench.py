@@ -25,8 +25,9 @@ def timed(fn, n=30, warm=5):
     return e0.elapsed_time(e1) / n
 
 
-for name, (M, K, N) in {"proj": (36864, 3072, 3072), "fc2": (36864, 12288, 3072),
-                        "linear2": (36864, 15360, 3072)}.items():
+SHAPES = {"proj": (36864, 3072, 3072), "fc2": (36864, 12288, 3072), "linear2": (36864, 15360, 3072),
+          "sd3m_proj": (35432, 1536, 1536), "sd3m_fc2": (35432, 6144, 1536), "sd35l_proj": (35432, 2432, 2432)}
+for name, (M, K, N) in SHAPES.items():
     x = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
     w = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.02
     b = torch.randn(N, device="cuda", dtype=torch.bfloat16) * 0.02
