@@ -189,29 +189,85 @@ def blas_threads():
     return os.cpu_count()
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def block_flops(n_double, n_single, N=4608, D=3072, H=24, r=64):
+    """Algorithmic fp64 FLOPs of the oracle's sampled blocks (one request, N tokens, rank-r LoRA on
+    every adapted linear): the same 2MNK / 4N^2D / 2r(in+out) formula as dit_step_flops."""
+    F = 4 * D
+    dbl = 2 * N * D * (3 * D) + 2 * N * D * D + 2 * 2 * N * D * F + 4 * N * N * D
+    dbl += 2 * r * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D))
+    sgl = 2 * N * D * (3 * D + F) + 2 * N * (D + F) * D + 4 * N * N * D
+    sgl += 2 * r * N * ((D + 3 * D + F) + (D + F + D))
+    return n_double * dbl + n_single * sgl
+
+
+def time_t0():
+    """configs[0] (T0) in full: the oracle's whole dit_step on the tiny config (1 double block,
+    hidden 64, 2 heads, 16 img + 8 txt tokens, batch 2, one rank-4 LoRA) for 2 Euler steps."""
+    import numpy as np
+    import synth
+    from oracle import flux_step as O
+    cfg = synth.TINY
+    W = O.weights_to_f64(synth.make_weights_bf16(cfg))
+    bits = synth.make_lora_bf16(cfg, 4, 0)
+    ad = {0: O.OracleLoRA(1.0, {m: (O.bf16_to_f64(bits[m + ".lora_A"]), O.bf16_to_f64(bits[m + ".lora_B"]))
+                                 for m, _, _ in synth.lora_targets(cfg)})}
+    batch = synth.make_batch(cfg, 2, 4, 4, 8, n_adapters=1)
+    batch.adapter_id = np.array([0, 0], dtype=np.int32)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        lat, _v = O.dit_step(cfg, W, batch, ad, None)
+        batch.latents = lat
+    return (time.perf_counter() - t0) / 2
+
+
 def cpu_baseline(B=8, n_double=1, n_single=1):
     t0 = time.perf_counter()
     td, ts = oracle_sample_times(n_double, n_single)
     t_step = B * (19 * td + 38 * ts)
+    fl = block_flops(n_double, n_single)
+    t_t0 = time_t0()
     return {
         "value": 1.0 / t_step, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+        "cpu_model": cpu_model(), "extrapolated": True,
+        "fp64_gflops": fl / (n_double * td + n_single * ts) / 1e9,
+        "t0_full_step_s": t_t0,
         "sample": (f"fp64 numpy oracle, {n_double} double + {n_single} single Flux-width block(s) of one request "
                    f"(N=4608, rank-64 LoRA) timed ({td:.2f} s / {ts:.2f} s per block); steps/s extrapolated as "
                    f"1 / (B=8 x (19 t_double + 38 t_single)), embedders/final omitted (<0.1% of FLOPs); "
+                   f"T0 (configs[0], tiny) timed in full: {t_t0 * 1e3:.1f} ms per 2-request step; "
                    f"sample wall {time.perf_counter() - t0:.1f} s"),
     }
 
 
 def run_reference(args):
+    """The reference arm of this tier: the fp64 CPU oracle as it stands.  A full cfg3 step would take
+    over an hour on the host, so each timed STEP is one Flux-width block of one request (alternating
+    double / single); `steps` counts those blocks, `ms_per_step` is the measured time per block, and
+    `value` is the full-step rate extrapolated from them (flagged `extrapolated`)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     tds, tss = [], []
+    wall0 = None
     for i in range(args.warmup + args.steps):
         dbl = (i % 2 == 0)
+        if i == args.warmup:
+            wall0 = time.perf_counter()
         td, ts = oracle_sample_times(1 if dbl else 0, 0 if dbl else 1)
         if i >= args.warmup:
             (tds if dbl else tss).append(td if dbl else ts)
+    wall = time.perf_counter() - wall0
     if not tds:
         tds.append(oracle_sample_times(1, 0)[0])
     if not tss:
@@ -219,14 +275,22 @@ def run_reference(args):
     td, ts = sum(tds) / len(tds), sum(tss) / len(tss)
     t_step = 8 * (19 * td + 38 * ts)
     val = 1.0 / t_step
+    sample = (f"each timed step = one Flux-width block of one request (alternating double/single, N=4608, "
+              f"rank-64 LoRA): {len(tds)} double ({td:.2f} s) + {len(tss)} single ({ts:.2f} s); value = full "
+              f"cfg3 steps/s extrapolated as 1/(8 x (19 t_d + 38 t_s)) = {t_step:.0f} s per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / max(1, args.steps) * 1e3,
+        "step_unit": "one sampled transformer block (see extrapolated)",
+        "extrapolated": {"timed_blocks": args.steps, "timed_wall_s": wall, "full_step_s": t_step,
+                         "formula": "1 / (B=8 x (19 t_double + 38 t_single))"},
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "global_batch": 8, "seq_len": 4608, "parallelism": "cpu-oracle"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-                         "sample": f"each timed step = one Flux-width block of one request (alternating double/"
-                                   f"single, N=4608, rank-64 LoRA); steps/s = 1/(8 x (19 t_d + 38 t_s))"},
+                         "cpu_model": cpu_model(), "extrapolated": True,
+                         "fp64_gflops": block_flops(len(tds), len(tss)) / (sum(tds) + sum(tss)) / 1e9,
+                         "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -374,11 +438,16 @@ def run_gpu(args):
     g_ms, g_fl, g_n = prof[0]
     a_ms, a_fl, a_n = prof[1]
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
+    # ncu dram bytes of THIS workload's gemm_kernel launches (tools/gemm_traffic.py over an ncu capture
+    # of `tools/profile_step.py --workload <name>`); null when that workload was never captured
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", f"gemm_traffic_{args.workload}.json")
+    if os.path.exists(tp) and world == 1:
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            tj = json.load(open(tp))
+            traffic = tj.get("bytes_per_launch")
+            traffic_src = (f"ncu dram__bytes_read.sum+dram__bytes_write.sum per gemm_kernel launch, mean over one warm "
+                           f"{args.workload} step ({os.path.relpath(tp, ROOT)}, captured {tj.get('source')})")
         except Exception:
             traffic = None
     prof_total = sum(prof[k][0] for k in range(7))   # kinds 0-6 partition the step (10-18 split kind 0)
@@ -400,7 +469,7 @@ def run_gpu(args):
         "roofline": {"bound": "tensor", "kernel": "gemm_kernel (2-SM tcgen05, 256x256x64 pair tiles, fused epilogues)",
                      "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                      "frac": (achieved / peaks["bf16_sus"]) if achieved else None, "traffic": traffic,
-                     "traffic_source": "ncu dram__bytes_read.sum+dram__bytes_write.sum per gemm_kernel launch, mean over one warm step (profiles/gemm_traffic.json)" if traffic else None,
+                     "traffic_source": traffic_src,
                      "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside the long step)",
                      "launches": g_n, "share_of_step": g_ms / prof_total if prof_total else None},
         "kernels": {
@@ -430,6 +499,20 @@ def run_gpu(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a launcher: re-exec this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1, exactly as the driver launches it; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")   # NCCL init lines show every rank joined
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -442,6 +525,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

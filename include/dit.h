@@ -122,7 +122,8 @@ typedef struct dit_tensor {
  * are [out][in] row-major (K-major), biases [out]; names and shapes are those
  * of synth.weight_manifest(cfg).  BORROWED: must outlive the context and stay
  * unchanged.  May be called several times (later tensors replace earlier).
- * Errors: DIT_EINVAL (unknown name, wrong shape/dtype, duplicate in one call). */
+ * Errors: DIT_EINVAL (unknown name, wrong shape/dtype, duplicate in one call,
+ * or an adapter is merged: lora_unmerge first). */
 int dit_load_weights(dit_ctx* ctx, const dit_tensor* tensors, int n);
 
 /* ------------------------------------------------------------------- LoRA */
@@ -179,11 +180,16 @@ int lora_unmerge(dit_ctx* ctx);
  * before block `block`'s consuming kernel ("returns immediately if the data is
  * available, or blocks until the data arrives").
  * BORROWED and immutable until that dit_step completes.
- * Registrations apply to exactly one dit_step and are then cleared.
+ * Registrations apply to exactly one dit_step CALL and are cleared when it
+ * returns, whatever its status (a failed step never leaves stale pointers).
  * Errors: DIT_EINVAL (slot >= B_max, block >= L_d + L_s, NULL or misaligned
  * residual), DIT_ENOSPC (fan-in limit reached for this slot and block). */
 int controlnet_inject(dit_ctx* ctx, int32_t slot, int32_t block, const void* residual,
                       float scale, void* ready_event);
+
+/* Drop every ControlNet registration made since the last dit_step (a scheduler
+ * that cancels a request before stepping).  Errors: DIT_EINVAL (NULL ctx). */
+int controlnet_clear(dit_ctx* ctx);
 
 /* controlnet_inject with the readiness carried by a DEVICE FLAG instead of a
  * CUDA event -- the data engine's deferred fetch done in hardware
@@ -236,6 +242,21 @@ int dit_ipc_close(void* dev_ptr);
  * Errors: DIT_EPARALLEL (world does not divide H), DIT_ENCCL, DIT_EINVAL. */
 int sp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_id);
 
+/* Bring-your-own-transport variant of sp_init (no NCCL): every rank calls
+ * dit_peer_handle (which also resets this context's arrival flags, so it must
+ * precede any peer's first dit_step), the caller all-gathers the
+ * DIT_PEER_HANDLE_BYTES-byte handles by any means (a serving control plane, a
+ * gloo group, a file), and every rank then calls sp_init_peers with all of them
+ * in rank order (host, world x DIT_PEER_HANDLE_BYTES).  The fused exchange
+ * (dit_sp_exchange == 2) is then the only exchange: there is no all-to-all
+ * fallback.  Works across processes on one GPU too (the tests' cross-process
+ * check of the system-scope flag protocol).
+ * Errors: DIT_EINVAL (world not in [2, 8], bad rank, NULL), DIT_EPARALLEL,
+ * DIT_ECUDA (a peer's workspace cannot be mapped, or the configs differ). */
+#define DIT_PEER_HANDLE_BYTES 80
+int dit_peer_handle(dit_ctx* ctx, void* handle_out);
+int sp_init_peers(dit_ctx* ctx, int32_t world, int32_t rank, const void* handles);
+
 /* ------------------------------------------------------ latent parallelism */
 /* Latent (CFG) parallelism (the conditional and unconditional
  * passes of classifier-free guidance on separate GPUs, with a scatter-gather of the
@@ -249,6 +270,13 @@ int sp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_i
  * Errors: DIT_EPARALLEL (world != 2, or sp_init already active), DIT_ENCCL,
  * DIT_EINVAL. */
 int lp_init(dit_ctx* ctx, int32_t world, int32_t rank, const void* nccl_unique_id);
+/* lp_init also maps the peer's workspace through CUDA IPC (handles all-gathered
+ * over the new communicator): the final GEMM's epilogue then stores this rank's v
+ * straight into the peer's buffer as well and a device flag barrier replaces the
+ * all-gather (dit_sp_exchange == 2; 1 = ncclAllGather, forced by DIT_SP_NCCL=1).
+ * lp_init_peers is its bring-your-own-transport variant (see sp_init_peers):
+ * handles = both ranks' dit_peer_handle outputs in rank order. */
+int lp_init_peers(dit_ctx* ctx, int32_t world, int32_t rank, const void* handles);
 /* Test analogue of lp_init over an in-process group (dit_local_group_create(2)). */
 int lp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 
@@ -308,7 +336,9 @@ int dit_last_launch_count(const dit_ctx* ctx);
 /* Sequence-parallel exchange in use: 0 none (world 1), 1 NCCL all-to-all + gather/scatter
  * kernels, 2 fused -- the QKV and attention epilogues store straight into the owning rank's
  * buffers (peer-mapped over NVLink through CUDA IPC) behind device flag barriers (the
- * default when every rank can map every peer; DIT_SP_NCCL=1 forces 1). */
+ * default when every rank can map every peer; DIT_SP_NCCL=1 forces 1).  Under latent
+ * parallelism: 1 = ncclAllGather of v (or the in-process group), 2 = v stored into the
+ * peer by the final GEMM's epilogue. */
 int dit_sp_exchange(const dit_ctx* ctx);
 
 /* ------------------------------------------------------ profiling exports */
@@ -366,6 +396,11 @@ int dit_debug_attention_trace(void* buf);
 int dit_debug_delayed_publish(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
                               uint64_t delay_ns, void* stream);
 
+/* Test-only stand-in for a slow producer that occupies no SM: stalls `stream` for
+ * delay_ns on the host (cudaLaunchHostFunc + nanosleep); later work on that stream
+ * (a copy, an event record) starts after it. */
+int dit_debug_host_delay(void* stream, uint64_t delay_ns);
+
 /* ncclGetUniqueId for sp_init (rank 0 calls it, the caller broadcasts the 128 bytes). */
 int dit_nccl_unique_id(void* out128);
 
@@ -381,9 +416,19 @@ int64_t dit_sp_layout(int32_t which, int32_t world, int32_t rank, int32_t B, int
 
 /* Integer plan artefacts of `batch` (host outputs; bit-exact tests):
  * row_adapter: int32 [rows] LoRA pool slot of each local row of the
- *   txt-stream GEMM followed by the img-stream GEMM (-1 = none), rows =
- *   B*(Nt/P) + B*(Ni/P).  Returns rows written, or -status. */
+ *   txt-stream GEMM followed by the img-stream GEMM (-1 = none), computed by the
+ *   step's own planner without running a step; rows = S*(Nt/P) + S*(Ni/P), S =
+ *   sequences (2B with CFG on one GPU).  Returns rows written, or -status. */
 int dit_debug_row_adapter(dit_ctx* ctx, const dit_batch* batch, int32_t* out, int cap);
+/* The integer tables the LAST dit_step uploaded for row space `which` (0 txt
+ * stream GEMM rows, 1 img stream, 2 joint sequence of the single blocks), read
+ * back from the device -- exactly what the GEMM / shrink kernels consumed: kind
+ * 0 row -> adapter-pool slot int32 [M] (-1 none), 1 tile -> its distinct slots
+ * sorted ascending [tiles_m][B_max] (256-row tiles; unused entries 0), 2 distinct
+ * slots per tile [tiles_m], 3 the LoRA shrink work list of (tile, slot) pairs
+ * [n_shrink][2] in tile order.  Returns entries written, or -status (-DIT_ENOENT
+ * before the first dit_step).  Synchronous, test-only. */
+int dit_debug_plan(dit_ctx* ctx, int32_t which, int32_t kind, int32_t* out, int cap);
 /* shard_map: int32 [B*(Nt/P + Ni/P)]: global joint token index (txt first,
  * request-major: b*N + n) of every local row.  Returns rows, or -status. */
 int dit_debug_shard_map(dit_ctx* ctx, const dit_batch* batch, int32_t* out, int cap);

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <ctime>
 #include <vector>
 
 #include "../../include/dit.h"
@@ -95,7 +96,7 @@ struct LocalGroup {
   std::vector<const void*> send;
   std::vector<cudaEvent_t> ready, done;
   // fused exchange: every rank's peer-visible buffers (same process: plain device pointers)
-  std::vector<void*> qkv, o, cat;
+  std::vector<void*> qkv, o, cat, vcfg;
   std::vector<uint32_t*> flags;
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -185,6 +186,9 @@ struct dit_ctx {
   std::vector<void*> ipc_opened;
   // latent (CFG) parallelism: rank 0 conditional, rank 1 unconditional branch
   int lp_world = 1, lp_rank = 0;
+  bool lp_fused = false;             // the final GEMM epilogue stores v into the peer's vcfg too
+  float* peer_vcfg[2] = {};
+  uint32_t lp_steps = 0;             // step parity selects the vcfg buffer (peer-store WAR safety)
   ncclComm_t lp_comm = nullptr;
   LocalGroup* lp_group = nullptr;
   bf16_t* sp = nullptr;              // [send1 | recv1 | send2 | recv2] at P > 1
@@ -326,7 +330,8 @@ Layout layout_of(const dit_config& c) {
   L.cat = cv.take(R * (D + F) * 2);
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
   L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
-  L.vcfg = cv.take(2 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);   // CFG: v of both branches
+  // CFG: v of both branches, twice (latent parallelism over peer stores alternates buffers by step parity)
+  L.vcfg = cv.take(4 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);
   L.mjobs = cv.take((size_t)n_lora_modules(c) * merge_job_bytes());   // lora_merge job table
   L.rope = cv.take((size_t)c.max_batch * N * (d / 2) * 8);   // one table per sequence for ragged batches
   L.mod = cv.take(8 * mod_total * 4);
@@ -615,6 +620,10 @@ int bind_all(dit_ctx* c) {
 
 extern "C" int dit_load_weights(dit_ctx* c, const dit_tensor* t, int n) {
   if (!c) return DIT_EINVAL;
+  // the merged copies W' were computed from the current base weights: replacing a base tensor
+  // under them would leave the step running a stale patch
+  if (c->merged_adapter >= 0)
+    return c->fail(DIT_EINVAL, "adapter %d is merged; lora_unmerge before replacing base weights", c->merged_adapter);
   if (n < 0 || (n > 0 && !t)) return c->fail(DIT_EINVAL, "bad tensor list");
   std::vector<Expect> ex;
   expected_tensors(c, ex);
@@ -887,6 +896,27 @@ extern "C" int controlnet_inject_flag(dit_ctx* c, int32_t slot, int32_t block, c
   return DIT_OK;
 }
 
+extern "C" int controlnet_clear(dit_ctx* c) {
+  if (!c) return DIT_EINVAL;
+  c->cn.clear();
+  return DIT_OK;
+}
+
+namespace {
+void CUDART_CB host_delay_cb(void* arg) {
+  const uint64_t ns = reinterpret_cast<uint64_t>(arg);
+  struct timespec ts;
+  ts.tv_sec = (time_t)(ns / 1000000000ull);
+  ts.tv_nsec = (long)(ns % 1000000000ull);
+  nanosleep(&ts, nullptr);
+}
+}  // namespace
+
+extern "C" int dit_debug_host_delay(void* stream, uint64_t delay_ns) {
+  return cudaLaunchHostFunc(reinterpret_cast<cudaStream_t>(stream), host_delay_cb,
+                            reinterpret_cast<void*>(delay_ns)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
 extern "C" int dit_debug_delayed_publish(void* dst, const void* src, size_t bytes, uint32_t* flag, uint32_t value,
                                          uint64_t delay_ns, void* stream) {
   return delayed_publish_launch(dst, src, bytes, flag, value, delay_ns, reinterpret_cast<cudaStream_t>(stream)) ==
@@ -902,6 +932,7 @@ extern "C" void* dit_local_group_create(int32_t world) {
   g->qkv.assign(world, nullptr);
   g->o.assign(world, nullptr);
   g->cat.assign(world, nullptr);
+  g->vcfg.assign(world, nullptr);
   g->flags.assign(world, nullptr);
   g->ready.assign(world, nullptr);
   g->done.assign(world, nullptr);
@@ -927,7 +958,9 @@ extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   if (c->H % g->world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", g->world, c->H);
   if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   const char* nccl_path = getenv("DIT_SP_NCCL");
-  c->sp_fused = g->world > 1 && !(nccl_path && nccl_path[0] == '1');
+  // the fused exchange's peer tables and flag words are sized for 8 ranks (PeerFlags, qkv_peer,
+  // out_peer); larger in-process groups use the all-to-all path
+  c->sp_fused = g->world > 1 && g->world <= 8 && !(nccl_path && nccl_path[0] == '1');
   if (c->sp_fused) {   // peers resolve at the first dit_step, once every rank has registered
     cudaMemset(c->flags, 0, 8 * 4);
     cudaDeviceSynchronize();
@@ -946,69 +979,120 @@ extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   return DIT_OK;
 }
 
-// Fused exchange setup over NCCL: zero my arrival flags, all-gather every rank's IPC handles of
-// (qkv, o, cat, flags) through the new communicator, map the peers' buffers.  Any failure leaves
-// sp_fused off (the NCCL all-to-all path then runs) -- a capability check, not an error.
-static void setup_fused_peers(dit_ctx* c) {
-  // one handle per rank: the workspace, whose carve-out layout is identical on every rank
-  // (same dit_config), so a peer's qkv / o / cat / flags sit at my offsets from its base
-  const int P = c->world, me = c->rank;
-  constexpr int H = DIT_IPC_HANDLE_BYTES;
-  std::vector<uint8_t> mine(H + 8), all((size_t)P * (H + 8));
-  bool ok = dit_ipc_export(c->ws, mine.data()) == DIT_OK;
+// Peer handle of a context: the CUDA IPC handle of its workspace + the workspace size.  One
+// handle per rank suffices: the carve-out layout is identical on every rank (same dit_config),
+// so a peer's qkv / o / cat / vcfg / flags sit at my offsets from its base.
+constexpr int PEER_HANDLE = DIT_IPC_HANDLE_BYTES + 8;
+static_assert(PEER_HANDLE == DIT_PEER_HANDLE_BYTES, "peer handle layout");
+
+extern "C" int dit_peer_handle(dit_ctx* c, void* out) {
+  if (!c || !out) return DIT_EINVAL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
+  // zero my arrival flags BEFORE the handle leaves this process: no peer can signal before it has
+  // every handle, and it has mine only after this call returned
+  if (cudaMemset(c->flags, 0, 8 * 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return c->fail(DIT_ECUDA, "flag reset failed");
+  uint8_t* o = static_cast<uint8_t*>(out);
+  if (dit_ipc_export(c->ws, o) != DIT_OK) return c->fail(DIT_ECUDA, "cudaIpcGetMemHandle of the workspace failed");
   const uint64_t wsb = c->ws_bytes;
-  memcpy(mine.data() + H, &wsb, 8);
-  cudaMemset(c->flags, 0, 8 * 4);    // before the all-gather: no peer can signal before it completes
-  // the exchange runs even when the export failed (a zeroed handle marks it), so no rank hangs
-  if (!ok) std::fill(mine.begin(), mine.end(), 0);
-  uint8_t* dev = reinterpret_cast<uint8_t*>(c->sp);
-  cudaMemcpy(dev, mine.data(), mine.size(), cudaMemcpyHostToDevice);
-  if (ncclAllGather(dev, dev + 4096, H + 8, ncclUint8, c->comm, 0) != ncclSuccess) return;
-  if (cudaStreamSynchronize(0) != cudaSuccess) return;
-  cudaMemcpy(all.data(), dev + 4096, all.size(), cudaMemcpyDeviceToHost);
+  memcpy(o + DIT_IPC_HANDLE_BYTES, &wsb, 8);
+  return DIT_OK;
+}
+
+namespace {
+// Map every peer's workspace from the all-gathered handles (P x PEER_HANDLE bytes, rank order).
+// base[me] = my own workspace.  Returns false (nothing left open) if any handle is unusable.
+bool open_peer_bases(dit_ctx* c, int P, int me, const uint8_t* all, uint8_t** base, std::vector<void*>& opened) {
+  opened.clear();
   for (int r = 0; r < P; ++r) {
     uint64_t b = 0;
-    memcpy(&b, all.data() + (size_t)r * (H + 8) + H, 8);
-    if (b != wsb) return;              // an export failed (zeroed) or layouts differ: every rank falls back alike
+    memcpy(&b, all + (size_t)r * PEER_HANDLE + DIT_IPC_HANDLE_BYTES, 8);
+    if (b != c->ws_bytes) return false;   // an export failed (zeroed) or layouts differ
   }
-  std::vector<void*> opened;
-  uint8_t* base[8] = {};
-  int ok_open = 1;
-  for (int r = 0; r < P && ok_open; ++r) {
+  for (int r = 0; r < P; ++r) {
     if (r == me) { base[r] = c->ws; continue; }
     void* ptr = nullptr;
-    if (dit_ipc_open(all.data() + (size_t)r * (H + 8), &ptr) == DIT_OK) {
-      opened.push_back(ptr);
-      base[r] = static_cast<uint8_t*>(ptr);
-    } else {
-      ok_open = 0;
+    if (dit_ipc_open(all + (size_t)r * PEER_HANDLE, &ptr) != DIT_OK) {
+      for (void* x : opened) dit_ipc_close(x);
+      opened.clear();
+      cudaGetLastError();
+      return false;
     }
+    opened.push_back(ptr);
+    base[r] = static_cast<uint8_t*>(ptr);
   }
-  // consensus: every rank must have mapped every peer, else all fall back together
+  return true;
+}
+
+void* at_peer(const dit_ctx* c, uint8_t* const* base, int r, const void* mine_ptr) {
+  return static_cast<void*>(base[r] + (static_cast<const uint8_t*>(mine_ptr) - c->ws));
+}
+
+void bind_sp_peers(dit_ctx* c, uint8_t* const* base, int P) {
+  for (int r = 0; r < P; ++r) {
+    c->peer_qkv[r] = at_peer(c, base, r, c->qkv);
+    c->peer_o[r] = at_peer(c, base, r, c->o);
+    c->peer_cat[r] = at_peer(c, base, r, c->cat);
+    c->peer_flags.f[r] = static_cast<uint32_t*>(at_peer(c, base, r, c->flags));
+  }
+  c->sp_fused = true;
+  c->peers_ready = true;
+  c->sp_epoch = 0;
+}
+
+void bind_lp_peers(dit_ctx* c, uint8_t* const* base) {
+  for (int r = 0; r < 2; ++r) {
+    c->peer_vcfg[r] = static_cast<float*>(at_peer(c, base, r, c->vcfg));
+    c->peer_flags.f[r] = static_cast<uint32_t*>(at_peer(c, base, r, c->flags));
+  }
+  c->lp_fused = true;
+  c->peers_ready = true;
+  c->sp_epoch = 0;
+  c->lp_steps = 0;
+}
+
+void close_opened(dit_ctx* c) {
+  for (void* x : c->ipc_opened) dit_ipc_close(x);
+  c->ipc_opened.clear();
+}
+
+// All-gather every rank's peer handle over an NCCL communicator and map the peers, with a
+// consensus all-reduce: every rank mapped every peer, or all ranks report false together.
+bool nccl_gather_and_open(dit_ctx* c, ncclComm_t comm, int P, int me, uint8_t** base, std::vector<void*>& opened) {
+  std::vector<uint8_t> mine(PEER_HANDLE, 0), all((size_t)P * PEER_HANDLE);
+  // the exchange runs even when the export failed (a zeroed handle marks it), so no rank hangs
+  if (dit_peer_handle(c, mine.data()) != DIT_OK) std::fill(mine.begin(), mine.end(), 0);
+  uint8_t* dev = reinterpret_cast<uint8_t*>(c->sp);
+  cudaMemcpy(dev, mine.data(), mine.size(), cudaMemcpyHostToDevice);
+  if (ncclAllGather(dev, dev + 4096, PEER_HANDLE, ncclUint8, comm, 0) != ncclSuccess) return false;
+  if (cudaStreamSynchronize(0) != cudaSuccess) return false;
+  cudaMemcpy(all.data(), dev + 4096, all.size(), cudaMemcpyDeviceToHost);
+  int ok_open = open_peer_bases(c, P, me, all.data(), base, opened) ? 1 : 0;
   int* dflag = reinterpret_cast<int*>(dev + 8192);
   cudaMemcpy(dflag, &ok_open, 4, cudaMemcpyHostToDevice);
-  if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, 0) != ncclSuccess) ok_open = 0;
+  if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, comm, 0) != ncclSuccess) ok_open = 0;
   cudaStreamSynchronize(0);
   int all_ok = 0;
   cudaMemcpy(&all_ok, dflag, 4, cudaMemcpyDeviceToHost);
   if (!ok_open || !all_ok) {
     for (void* x : opened) dit_ipc_close(x);
+    opened.clear();
     cudaGetLastError();
-    return;
+    return false;
   }
-  auto at = [&](int r, const void* mine_ptr) {
-    return static_cast<void*>(base[r] + (static_cast<const uint8_t*>(mine_ptr) - c->ws));
-  };
-  for (int r = 0; r < P; ++r) {
-    c->peer_qkv[r] = at(r, c->qkv);
-    c->peer_o[r] = at(r, c->o);
-    c->peer_cat[r] = at(r, c->cat);
-    c->peer_flags.f[r] = static_cast<uint32_t*>(at(r, c->flags));
-  }
+  return true;
+}
+}  // namespace
+
+// Fused exchange setup over NCCL: map the peers' workspaces through the new communicator.  Any
+// failure leaves sp_fused off (the NCCL all-to-all path then runs) -- a capability check.
+static void setup_fused_peers(dit_ctx* c) {
+  uint8_t* base[8] = {};
+  std::vector<void*> opened;
+  if (!nccl_gather_and_open(c, c->comm, c->world, c->rank, base, opened)) return;
+  close_opened(c);
   c->ipc_opened = opened;
-  c->sp_fused = true;
-  c->peers_ready = true;
-  c->sp_epoch = 0;
+  bind_sp_peers(c, base, c->world);
 }
 
 extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
@@ -1044,6 +1128,32 @@ extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   c->sp_fused = false;
   const char* nccl_path = getenv("DIT_SP_NCCL");
   if (world > 1 && world <= 8 && !(nccl_path && nccl_path[0] == '1')) setup_fused_peers(c);
+  return DIT_OK;
+}
+
+extern "C" int sp_init_peers(dit_ctx* c, int32_t world, int32_t rank, const void* handles) {
+  if (!c) return DIT_EINVAL;
+  if (world < 2 || world > 8 || rank < 0 || rank >= world)
+    return c->fail(DIT_EINVAL, "sp_init_peers: world must be in [2, 8] and rank in [0, world), got %d/%d", world, rank);
+  if (!handles) return c->fail(DIT_EINVAL, "handles is NULL");
+  if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
+  if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
+  if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
+  uint8_t* base[8] = {};
+  std::vector<void*> opened;
+  if (!open_peer_bases(c, world, rank, static_cast<const uint8_t*>(handles), base, opened))
+    return c->fail(DIT_ECUDA, "a peer workspace could not be mapped (cudaIpcOpenMemHandle / size mismatch)");
+  close_opened(c);
+  c->ipc_opened = opened;
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->comm = nullptr;
+  c->local_group = nullptr;
+  c->force_sp = false;
+  c->world = world;
+  c->rank = rank;
+  c->plan_B = -1;
+  c->rope_key[0] = -1;
+  bind_sp_peers(c, base, world);
   return DIT_OK;
 }
 
@@ -1133,7 +1243,43 @@ extern "C" int lp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid)
   c->lp_group = nullptr;
   c->lp_world = world;
   c->lp_rank = rank;
+  c->lp_fused = false;
   c->plan_B = -1;
+  // fused v exchange: the final GEMM epilogue stores this branch's v into the peer's buffer as
+  // well (peer-mapped through CUDA IPC); else ncclAllGather (DIT_SP_NCCL=1 forces it)
+  const char* nccl_path = getenv("DIT_SP_NCCL");
+  if (!(nccl_path && nccl_path[0] == '1')) {
+    uint8_t* base[8] = {};
+    std::vector<void*> opened;
+    if (nccl_gather_and_open(c, comm, 2, rank, base, opened)) {
+      close_opened(c);
+      c->ipc_opened = opened;
+      bind_lp_peers(c, base);
+    }
+  }
+  return DIT_OK;
+}
+
+extern "C" int lp_init_peers(dit_ctx* c, int32_t world, int32_t rank, const void* handles) {
+  if (!c) return DIT_EINVAL;
+  if (world != 2) return c->fail(DIT_EPARALLEL, "latent parallelism splits the 2 CFG branches: world must be 2, got %d", world);
+  if (rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad rank %d", rank);
+  if (!handles) return c->fail(DIT_EINVAL, "handles is NULL");
+  if (c->world > 1 || c->force_sp) return c->fail(DIT_EPARALLEL, "sequence parallelism is active (sp_init)");
+  if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
+  uint8_t* base[8] = {};
+  std::vector<void*> opened;
+  if (!open_peer_bases(c, 2, rank, static_cast<const uint8_t*>(handles), base, opened))
+    return c->fail(DIT_ECUDA, "the peer workspace could not be mapped (cudaIpcOpenMemHandle / size mismatch)");
+  close_opened(c);
+  c->ipc_opened = opened;
+  if (c->lp_comm) ncclCommDestroy(c->lp_comm);
+  c->lp_comm = nullptr;
+  c->lp_group = nullptr;
+  c->lp_world = 2;
+  c->lp_rank = rank;
+  c->plan_B = -1;
+  bind_lp_peers(c, base);
   return DIT_OK;
 }
 
@@ -1145,6 +1291,19 @@ extern "C" int lp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   c->lp_group = g;
   c->lp_world = 2;
   c->lp_rank = rank;
+  // fused v exchange over the group's (same-process) pointers unless DIT_SP_NCCL=1; the peer
+  // resolves at the first dit_step, once both ranks have registered
+  const char* nccl_path = getenv("DIT_SP_NCCL");
+  c->lp_fused = !(nccl_path && nccl_path[0] == '1');
+  c->peers_ready = false;
+  if (c->lp_fused) {
+    cudaMemset(c->flags, 0, 8 * 4);
+    cudaDeviceSynchronize();
+    g->vcfg[rank] = c->vcfg;
+    g->flags[rank] = c->flags;
+    c->sp_epoch = 0;
+    c->lp_steps = 0;
+  }
   c->plan_B = -1;
   return DIT_OK;
 }
@@ -1347,7 +1506,9 @@ extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
     // LoRA: 2 r (in + out) per row per adapted linear
     const int aid = b->adapter_id ? b->adapter_id[r] : -1;
     if (aid < 0 || c->merged_adapter >= 0) continue;   // merged: the delta is inside the base GEMMs
-    const double rk = c->cfg.max_rank;  // rank of the adapter (pool rank bound)
+    auto slot = c->adapter_slot.find(aid);
+    if (slot == c->adapter_slot.end()) continue;       // unregistered: dit_step would reject it
+    const double rk = c->slot_rank_h[slot->second];    // the adapter's registered rank (padding excluded)
     f += c->Ld * 2 * rk * N * ((D + 3 * D) + (D + D) + (D + F) + (F + D));
     if (sd3) f -= 2 * rk * Nt * ((D + D) + (D + F) + (F + D));
     f += c->Ls * 2 * rk * N * ((D + 3 * D + F) + (D + F + D));
@@ -1358,6 +1519,7 @@ extern "C" double dit_step_flops(const dit_ctx* c, const dit_batch* b) {
 extern "C" int dit_last_launch_count(const dit_ctx* c) { return c ? c->last_launches : 0; }
 
 extern "C" int dit_sp_exchange(const dit_ctx* c) {
+  if (c && c->lp_world > 1) return c->lp_fused ? 2 : 1;
   if (!c || (c->world == 1 && !c->force_sp)) return 0;
   return c->sp_fused ? 2 : 1;
 }
@@ -1379,6 +1541,12 @@ extern "C" int dit_sp_exchange(const dit_ctx* c) {
 
 extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   if (!c) return DIT_EINVAL;
+  // ControlNet registrations apply to exactly one dit_step call: cleared on EVERY exit (a
+  // validation error or a failed launch included), so no stale borrowed pointer outlives it
+  struct CnClear {
+    dit_ctx* c;
+    ~CnClear() { c->cn.clear(); }
+  } cn_guard{c};
   if (!b) return c->fail(DIT_EINVAL, "batch is NULL");
   if (!c->weights_ready) return c->fail(DIT_ENOWEIGHTS, "base weights not (fully) loaded");
   const int B = b->batch;   // requests
@@ -1421,7 +1589,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
                    c->cfg.pos_embed_max);
   const int P = c->world;
   if (Ni % P || Nt % P) return c->fail(DIT_EPARALLEL, "world %d does not divide Ni=%d / Nt=%d", P, Ni, Nt);
-  if (P > 1 && !c->comm && !c->local_group) return c->fail(DIT_EPARALLEL, "sp_init not called");
+  if (P > 1 && !c->comm && !c->local_group && !c->peers_ready) return c->fail(DIT_EPARALLEL, "sp_init not called");
   if (!b->adapter_id || !b->sigma || !b->sigma_next || !b->guidance)
     return c->fail(DIT_EINVAL, "host arrays adapter_id/sigma/sigma_next/guidance required");
   if (!b->latents_in || !b->latents_out || !b->txt || !b->pooled) return c->fail(DIT_EINVAL, "NULL device pointer");
@@ -1432,6 +1600,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     if (a0 < b0 + lat_bytes && b0 < a0 + lat_bytes) return c->fail(DIT_EALIAS, "latents_out aliases latents_in");
   }
   if ((reinterpret_cast<uintptr_t>(b->txt) & 15)) return c->fail(DIT_EINVAL, "txt must be 16-byte aligned");
+  if (b->cfg_scale) {   // cfg_euler_kernel moves latents / v as float4
+    auto mis16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+    if (mis16(b->latents_in) || mis16(b->latents_out) || (b->v_out && mis16(b->v_out)))
+      return c->fail(DIT_EINVAL, "with cfg_scale, latents_in / latents_out / v_out must be 16-byte aligned");
+  }
   std::vector<int> req_slot(S, -1);   // pool slot of every sequence
   for (int i = 0; i < S; ++i) {
     const int aid = b->adapter_id[i % B];
@@ -1652,6 +1825,15 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       c->peer_qkv[r] = g->qkv[r];
       c->peer_o[r] = g->o[r];
       c->peer_cat[r] = g->cat[r];
+      c->peer_flags.f[r] = g->flags[r];
+    }
+    c->peers_ready = true;
+  }
+  if (lpar && c->lp_fused && !c->peers_ready) {   // in-process latent-parallel group
+    LocalGroup* g = c->lp_group;
+    for (int r = 0; r < 2; ++r) {
+      if (!g || !g->vcfg[r]) return c->fail(DIT_EPARALLEL, "rank %d of the local group has not called lp_init_local", r);
+      c->peer_vcfg[r] = static_cast<float*>(g->vcfg[r]);
       c->peer_flags.f[r] = g->flags[r];
     }
     c->peers_ready = true;
@@ -2056,34 +2238,47 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     e.v_out = b->v_out;
     e.dsig = c->p_dsig;
     const size_t vcount = (size_t)B * ni * C;   // one branch's v
+    // latent parallelism over peer stores: the two halves of vcfg alternate by step parity, so a
+    // peer one step ahead never overwrites the buffer this rank's combine is still reading
+    const size_t vpar = (lpar && c->lp_fused && (c->lp_steps & 1))
+                            ? 2 * (size_t)c->cfg.max_batch * c->cfg.max_img_tokens * C : 0;
+    float* vbuf = c->vcfg + vpar;
     if (cfgon) {   // v of every sequence into vcfg [cond B | uncond B]; Euler after the combine
       e.lat_in = nullptr;
       e.lat_out = nullptr;
-      e.v_out = c->vcfg + (lpar ? (size_t)c->lp_rank * vcount : 0);
+      e.v_out = vbuf + (lpar ? (size_t)c->lp_rank * vcount : 0);
+      if (lpar && c->lp_fused)   // ... and into the peer's buffer at the same place: the all-gather, fused
+        e.v_peer = c->peer_vcfg[1 - c->lp_rank] + vpar + (size_t)c->lp_rank * vcount;
     }
     GemmProblem p = base_problem(c, c->u, Mi, D, D, c->fin_lin, e);
     c->gemm_label = 17;
     CK(run_gemm(c, &p, 1, s));
     if (lpar) {   // latent parallelism: per-step gather of the two branches' v
       prof_begin(c, s);
-      if (c->lp_comm) {
-        ncclResult_t r = ncclAllGather(c->vcfg + (size_t)c->lp_rank * vcount, c->vcfg, vcount, ncclFloat32,
+      if (c->lp_fused) {   // both halves are in place once the peer's epilogue has released its flag
+        ++c->sp_epoch;
+        ++c->lp_steps;
+        cudaError_t e1 = sp_signal_launch(c->peer_flags, c->lp_rank, 2, c->sp_epoch, s);
+        cudaError_t e2 = sp_wait_launch(c->flags, c->lp_rank, 2, c->sp_epoch, s);
+        c->launches += 1;
+        if (e1 != cudaSuccess || e2 != cudaSuccess) return c->fail(DIT_ECUDA, "lp barrier launch failed");
+      } else if (c->lp_comm) {
+        ncclResult_t r = ncclAllGather(vbuf + (size_t)c->lp_rank * vcount, vbuf, vcount, ncclFloat32,
                                        c->lp_comm, s);
         if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
       } else {
-        c->lp_group->allgather(c->lp_rank, c->vcfg, vcount * 4, s);
+        c->lp_group->allgather(c->lp_rank, vbuf, vcount * 4, s);
       }
       prof_end(c, s, 5, 0.0);
       c->launches++;
     }
     if (cfgon)   // v = v_u + g (v_c - v_u); latents_out = latents_in + dsig v (reading C22)
-      CKC(cfg_euler_launch(c->vcfg, c->vcfg + vcount, c->p_cfg, c->p_dsig, b->latents_in, b->latents_out, b->v_out,
+      CKC(cfg_euler_launch(vbuf, vbuf + vcount, c->p_cfg, c->p_dsig, b->latents_in, b->latents_out, b->v_out,
                            B, ni * C, s));
   }
 
   for (int i = 0; i < S; ++i)
     if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
-  c->cn.clear();
   c->last_launches = c->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));
@@ -2133,6 +2328,7 @@ extern "C" int dit_fill_synthetic(void* dst, int64_t n, uint64_t seed, uint64_t 
 }
 
 namespace {
+// req_slot per SEQUENCE (CFG without latent parallelism: 2B sequences, sequence q = request q % B)
 int debug_prepare(dit_ctx* c, const dit_batch* b, std::vector<int>& req_slot, int& nt, int& ni) {
   if (!b || b->batch < 1 || b->batch > c->cfg.max_batch) return -DIT_EBATCH;
   const int P = c->world;
@@ -2140,9 +2336,11 @@ int debug_prepare(dit_ctx* c, const dit_batch* b, std::vector<int>& req_slot, in
   if (Ni <= 0 || Nt <= 0 || Ni % P || Nt % P) return -DIT_EPARALLEL;
   nt = Nt / P;
   ni = Ni / P;
-  req_slot.assign(b->batch, -1);
-  for (int i = 0; i < b->batch; ++i) {
-    const int aid = b->adapter_id ? b->adapter_id[i] : -1;
+  const int S = (b->cfg_scale && c->lp_world == 1) ? 2 * b->batch : b->batch;
+  if (S > c->cfg.max_batch) return -DIT_EBATCH;
+  req_slot.assign(S, -1);
+  for (int i = 0; i < S; ++i) {
+    const int aid = b->adapter_id ? b->adapter_id[i % b->batch] : -1;
     if (aid < 0 || c->merged_adapter >= 0) continue;
     auto it = c->adapter_slot.find(aid);
     if (it == c->adapter_slot.end()) return -DIT_EADAPTER;
@@ -2158,13 +2356,41 @@ extern "C" int dit_debug_row_adapter(dit_ctx* c, const dit_batch* b, int32_t* ou
   int nt, ni;
   int r = debug_prepare(c, b, rs, nt, ni);
   if (r < 0) return r;
-  const int B = b->batch;
-  const int rows = B * nt + B * ni;
+  const int S = (int)rs.size();
+  const int rows = S * nt + S * ni;
   if (cap < rows) return -DIT_EINVAL;
+  // the planner dit_step uses (build_rowspace), on scratch row spaces (the step's cache is untouched)
   int k = 0;
-  for (int x = 0; x < B * nt; ++x) out[k++] = rs[x / nt];
-  for (int x = 0; x < B * ni; ++x) out[k++] = rs[x / ni];
+  const int Ms[2] = {S * nt, S * ni}, rpr[2] = {nt, ni};
+  for (int q = 0; q < 2; ++q) {
+    RowSpace R;
+    std::vector<int> ht, hc;
+    std::vector<int2> hs;
+    if (build_rowspace(c, R, Ms[q], rpr[q], rs, ht, hc, hs) < 0) return -DIT_ESHAPE;
+    for (int x = 0; x < Ms[q]; ++x) out[k++] = R.h_row_slot[x];
+  }
   return rows;
+}
+
+// The integer tables the LAST dit_step uploaded for row space `which` (0 txt stream, 1 img stream,
+// 2 joint sequence), read back from the device: kind 0 row -> pool slot [M], 1 tile -> sorted
+// distinct slots [tiles_m][slot_cap] (unused entries 0), 2 distinct slots per tile [tiles_m],
+// 3 shrink work list (tile, slot) pairs [n_shrink][2].  Test-only (synchronous).
+extern "C" int dit_debug_plan(dit_ctx* c, int32_t which, int32_t kind, int32_t* out, int cap) {
+  if (!c || !out || which < 0 || which > 2 || kind < 0 || kind > 3) return -DIT_EINVAL;
+  if (c->plan_B < 0) return -DIT_ENOENT;
+  const RowSpace& R = c->rs[which];
+  const void* src = nullptr;
+  int n = 0;
+  switch (kind) {
+    case 0: src = R.row_slot; n = R.M; break;
+    case 1: src = R.tile_slots; n = R.tiles_m * c->slot_cap; break;
+    case 2: src = R.tile_cnt; n = R.tiles_m; break;
+    default: src = R.shrink_list; n = 2 * R.n_shrink; break;
+  }
+  if (n > cap) return -DIT_EINVAL;
+  if (n > 0 && cudaMemcpy(out, src, (size_t)n * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -DIT_ECUDA;
+  return n;
 }
 
 // Bench-only: one plain projection out = bf16(A W^T + bias) through the tcgen05 GEMM (the same

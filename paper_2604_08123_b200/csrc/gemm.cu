@@ -457,8 +457,10 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           const size_t off = (size_t)r * P.N + col + e;
           if (E.lat_out != nullptr) E.lat_out[off] = E.lat_in[off] + ds * y[e];   // (CFG: Euler after the combine)
           if (E.v_out != nullptr) E.v_out[off] = y[e];
+          if (E.v_peer != nullptr) E.v_peer[off] = y[e];   // latent parallelism: the fused all-gather
         }
       }
+      if (E.v_peer != nullptr) __threadfence_system();   // before the barrier kernel's release
     }
   }
   }

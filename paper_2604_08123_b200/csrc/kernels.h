@@ -74,6 +74,7 @@ struct EpiParams {
   const float* lat_in;
   float* lat_out;
   float* v_out;
+  float* v_peer;             // latent parallelism over peer memory: v also stored here (the peer's vcfg)
   const float* dsig;         // device [B] sigma_next - sigma
   // LoRA shrink
   const int* row_slot;       // device [M] pool slot of each row (-1 none)

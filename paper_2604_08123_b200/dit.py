@@ -61,10 +61,12 @@ EXPORTS = {
     "lora_merge": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p]),
     "lora_unmerge": (C.c_int, [C.c_void_p]),
     "controlnet_inject": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p]),
+    "controlnet_clear": (C.c_int, [C.c_void_p]),
     "controlnet_inject_flag": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p,
                                          C.c_uint32]),
     "dit_debug_delayed_publish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_uint64,
                                             C.c_void_p]),
+    "dit_debug_host_delay": (C.c_int, [C.c_void_p, C.c_uint64]),
     "controlnet_push": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32, C.c_void_p]),
     "dit_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dit_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
@@ -72,6 +74,9 @@ EXPORTS = {
     "sp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "lp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "lp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "dit_peer_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sp_init_peers": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "lp_init_peers": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
     "dit_last_launch_count": (C.c_int, [C.c_void_p]),
@@ -96,6 +101,7 @@ EXPORTS = {
     "dit_sp_layout": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_int64), C.c_int64]),
     "dit_debug_row_adapter": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
+    "dit_debug_plan": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int]),
     "dit_debug_shard_map": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.POINTER(C.c_int32), C.c_int]),
 }
 
@@ -252,6 +258,24 @@ class DiT:
         buf = C.create_string_buffer(nccl_uid, 128)
         _check(self.lib.lp_init(self.ctx, world, rank, buf), self.ctx)
 
+    def peer_handle(self) -> bytes:
+        """dit_peer_handle: this context's workspace handle (resets its arrival flags)."""
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        _check(self.lib.dit_peer_handle(self.ctx, buf), self.ctx)
+        return buf.raw
+
+    def sp_init_peers(self, world: int, rank: int, handles):
+        """handles: every rank's peer_handle() in rank order (any transport)."""
+        blob = b"".join(handles)
+        _check(self.lib.sp_init_peers(self.ctx, world, rank, C.create_string_buffer(blob, len(blob))), self.ctx)
+
+    def lp_init_peers(self, world: int, rank: int, handles):
+        blob = b"".join(handles)
+        _check(self.lib.lp_init_peers(self.ctx, world, rank, C.create_string_buffer(blob, len(blob))), self.ctx)
+
+    def sp_exchange(self) -> int:
+        return int(self.lib.dit_sp_exchange(self.ctx))
+
     def lp_init_local(self, group, rank: int):
         _check(self.lib.lp_init_local(self.ctx, group, rank), self.ctx)
 
@@ -308,6 +332,13 @@ class DiT:
             raise DitError(-n, "debug_row_adapter")
         return list(out[:n])
 
+    def debug_plan(self, which: int, kind: int, cap: int = 1 << 20):
+        out = (C.c_int32 * cap)()
+        n = self.lib.dit_debug_plan(self.ctx, which, kind, out, cap)
+        if n < 0:
+            raise DitError(-n, "debug_plan")
+        return list(out[:n])
+
     def debug_shard_map(self, batch: dit_batch, cap: int):
         out = (C.c_int32 * cap)()
         n = self.lib.dit_debug_shard_map(self.ctx, C.byref(batch), out, cap)
@@ -323,6 +354,7 @@ class DiT:
 
 
 IPC_HANDLE_BYTES = 72
+PEER_HANDLE_BYTES = 80
 
 
 def ipc_export(t) -> bytes:

@@ -90,13 +90,17 @@ def test_sd3_cfg_scale_zero_is_unconditional_bitwise(torch_cuda):
     assert np.abs(v1 - v_c).max() <= 1e-5 * np.abs(v_c).max()
 
 
-def test_latent_parallel_local_group_bitwise(torch_cuda):
+@pytest.mark.parametrize("exchange", ["fused", "allgather"])
+def test_latent_parallel_local_group_bitwise(torch_cuda, exchange, monkeypatch):
     """Latent parallelism: rank 0 runs the conditional, rank 1 the
-    unconditional pass, v all-gathered per step; both ranks' latents_out equal the one-GPU CFG
-    step bitwise (in-process 2-rank group on one GPU)."""
+    unconditional pass, v exchanged per step; both ranks' latents_out equal the one-GPU CFG
+    step bitwise (in-process 2-rank group on one GPU).  exchange "fused": the final GEMM's
+    epilogue stores v into the peer's buffer + a device flag barrier (3 steps: the step-parity
+    double buffer alternates); "allgather": the all-gather path."""
     import concurrent.futures as cf
     import torch
     from paper_2604_08123_b200 import dit as D
+    monkeypatch.setenv("DIT_SP_NCCL", "0" if exchange == "fused" else "1")
     cfg = CFGS["d64_noqk"]
     B, hh, ww, nt = 2, 12, 12, 40
     ni = hh * ww
@@ -118,12 +122,15 @@ def test_latent_parallel_local_group_bitwise(torch_cuda):
         with torch.cuda.stream(streams[r]):
             return ms[r].step(batch, lp_rank=r, sync=False)
 
-    with cf.ThreadPoolExecutor(2) as ex:
-        outs = list(ex.map(run, range(2)))
-    torch.cuda.synchronize()
-    for out, v in outs:
-        np.testing.assert_array_equal(v.cpu().numpy(), v1)
-        np.testing.assert_array_equal(out.cpu().numpy(), lat1)
+    for _ in range(3 if exchange == "fused" else 1):
+        with cf.ThreadPoolExecutor(2) as ex:
+            outs = list(ex.map(run, range(2)))
+        torch.cuda.synchronize()
+        for m in ms:
+            assert m.sp_exchange() == (2 if exchange == "fused" else 1)
+        for out, v in outs:
+            np.testing.assert_array_equal(v.cpu().numpy(), v1)
+            np.testing.assert_array_equal(out.cpu().numpy(), lat1)
     W = O.weights_to_f64(synth.make_weights_bf16(cfg))
     x_o, v_o = S.dit_step(cfg, W, batch, {0: oracle_adapter(cfg, 8, 0)[0]})
     check(v1, v_o, "v")
