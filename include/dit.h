@@ -131,8 +131,13 @@ int dit_load_weights(dit_ctx* ctx, const dit_tensor* tensors, int n);
  * `adapter_id` into the pool, enqueued on `stream` (a cudaStream_t).
  * tensors: "<module>.lora_A" [r][in] and "<module>.lora_B" [out][r] for every
  * adapted linear (synth.lora_targets: double qkv/proj/fc1/fc2 per stream,
- * single linear1/linear2).  Missing modules are treated as zero (no delta).
+ * single linear1/linear2), in device memory OR pinned host memory (copied with
+ * cudaMemcpyDefault).  Missing modules are treated as zero (no delta).
  * Applied unmerged: y += scale * (x A^T) B^T (reading C9).
+ * Asynchronous loading: `stream` may be a side
+ * stream while steps run on another; every later dit_step that uses the adapter
+ * waits for the copies on ITS OWN stream (an event, no host stall), so the
+ * adapter can be registered the moment it arrives and used by the next step.
  * Caller buffers may be freed once `stream` has synchronised.
  * Errors: DIT_EEXIST, DIT_ERANK, DIT_ENOSPC, DIT_EINVAL. */
 int lora_register(dit_ctx* ctx, int32_t adapter_id, int32_t rank, float scale,
@@ -153,7 +158,10 @@ int lora_unregister(dit_ctx* ctx, int32_t adapter_id);
  * >= dit_merge_bytes(cfg), 256-byte aligned, layout = the adapted linears in
  * pool order, each [out][in] bf16 at a 256-byte aligned offset; it must stay
  * alive until lora_unmerge.  The base weights are never written, so
- * lora_unmerge restores them exactly (a pointer switch).  While an adapter is
+ * lora_unmerge restores them exactly (a pointer switch).  `stream` may be a side
+ * stream: the merge waits for the adapter's registration copies and for the last
+ * step that read a previous merged copy, and every later dit_step waits for the
+ * merge on its own stream (events, no host stall).  While an adapter is
  * merged the ctx is a patched replica specialised to it:
  * every request of a dit_step must name that adapter (else DIT_EADAPTER) and
  * no per-step LoRA work runs; it cannot be unregistered.
@@ -162,7 +170,9 @@ int lora_unregister(dit_ctx* ctx, int32_t adapter_id);
  * DIT_ENOWEIGHTS, DIT_ECUDA.  Validation precedes any enqueue. */
 size_t dit_merge_bytes(const dit_config* cfg);
 int lora_merge(dit_ctx* ctx, int32_t adapter_id, void* merged, size_t bytes, void* stream);
-/* Restore the base weights.  Errors: DIT_ENOENT (nothing merged). */
+/* Restore the base weights.  Waits (host) for the last enqueued dit_step that
+ * read the merged copy, so `merged` may be freed once this returns.
+ * Errors: DIT_ENOENT (nothing merged). */
 int lora_unmerge(dit_ctx* ctx);
 
 /* -------------------------------------------------------------- ControlNet */

@@ -163,6 +163,11 @@ struct dit_ctx {
   std::map<int, int> adapter_slot;      // adapter id -> pool slot
   std::vector<float> slot_scale_h;
   std::vector<cudaEvent_t> slot_last_use;
+  // asynchronous adapter loading: lora_register / lora_merge run on the caller's
+  // side stream; the step waits on these events on ITS stream (no host stall)
+  std::vector<cudaEvent_t> slot_ready;   // recorded after lora_register's copies
+  cudaEvent_t merge_ready = nullptr;     // recorded after lora_merge's kernel
+  cudaEvent_t merged_last_use = nullptr; // recorded by every dit_step that reads the merged copy
   int merged_adapter = -1;           // lora_merge: adapter patched into tm_m copies (-1: none)
   // ControlNet registrations for the next step
   struct CnReg { const void* ptr; float scale; cudaEvent_t ready; const uint32_t* flag; uint32_t expect; };
@@ -473,6 +478,10 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   c->slot_rank_h.assign(std::max(cfg->max_adapters, 1), 0);
   c->slot_last_use.assign(std::max(cfg->max_adapters, 1), nullptr);
   for (auto& e : c->slot_last_use) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  c->slot_ready.assign(std::max(cfg->max_adapters, 1), nullptr);
+  for (auto& e : c->slot_ready) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->merge_ready, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->merged_last_use, cudaEventDisableTiming);
   c->dbl[0].resize(c->Ld);
   c->dbl[1].resize(c->Ld);
   c->sgl.resize(c->Ls);
@@ -498,6 +507,10 @@ extern "C" void dit_destroy(dit_ctx* c) {
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
   for (auto& e : c->slot_last_use)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->slot_ready)
+    if (e) cudaEventDestroy(e);
+  if (c->merge_ready) cudaEventDestroy(c->merge_ready);
+  if (c->merged_last_use) cudaEventDestroy(c->merged_last_use);
   for (void* ptr : c->ipc_opened) dit_ipc_close(ptr);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->lp_comm) ncclCommDestroy(c->lp_comm);
@@ -716,16 +729,19 @@ extern "C" int lora_register(dit_ctx* c, int32_t adapter_id, int32_t rank, float
     cudaMemsetAsync(static_cast<uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2, 0, (size_t)ra * P.in * 2, s);
     cudaMemsetAsync(static_cast<uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, 0, (size_t)P.out * ra * 2, s);
   }
+  // sources may be device memory or pinned host memory (cudaMemcpyDefault, UVA): an adapter can be
+  // loaded straight from host RAM over PCIe on a side stream while steps run
   for (auto& j : jobs) {
     LoraPool& P = c->pools[j.mod];
     if (j.isA) {
       cudaMemcpyAsync(static_cast<uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2, j.t->ptr, (size_t)rank * P.in * 2,
-                      cudaMemcpyDeviceToDevice, s);
+                      cudaMemcpyDefault, s);
     } else {
       cudaMemcpy2DAsync(static_cast<uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, (size_t)ra * 2, j.t->ptr,
-                        (size_t)rank * 2, (size_t)rank * 2, P.out, cudaMemcpyDeviceToDevice, s);
+                        (size_t)rank * 2, (size_t)rank * 2, P.out, cudaMemcpyDefault, s);
     }
   }
+  cudaEventRecord(c->slot_ready[slot], s);   // every dit_step using the slot waits on this, on its stream
   if (cudaGetLastError() != cudaSuccess) return c->fail(DIT_ECUDA, "adapter copy failed");
   c->adapter_slot[adapter_id] = slot;
   c->slot_scale_h[slot] = scale;
@@ -804,6 +820,10 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
   const int ra = c->r_alloc;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   auto lins = adapted_lins(c);
+  // a previous merged copy in `merged` may still be read by an in-flight step; the adapter's pool
+  // copy may still be in flight on its registration stream
+  cudaStreamWaitEvent(s, c->merged_last_use, 0);
+  cudaStreamWaitEvent(s, c->slot_ready[slot], 0);
   // validate everything before enqueuing anything
   std::vector<CUtensorMap> maps(lins.size());
   size_t off = 0;
@@ -852,7 +872,9 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
     lins[k].first->tm_m = maps[k];
     lins[k].first->has_m = true;
   }
+  cudaStreamWaitEvent(s, c->slot_last_use[slot], 0);   // keep slot_last_use covering earlier steps too
   cudaEventRecord(c->slot_last_use[slot], s);
+  cudaEventRecord(c->merge_ready, s);                    // the next dit_step waits on this (its stream)
   c->merged_adapter = adapter_id;
   c->plan_B = -1;
   return DIT_OK;
@@ -861,6 +883,8 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
 extern "C" int lora_unmerge(dit_ctx* c) {
   if (!c) return DIT_EINVAL;
   if (c->merged_adapter < 0) return c->fail(DIT_ENOENT, "no adapter is merged");
+  // the caller may free / reuse the merged buffer after this returns: wait for its last reader
+  if (cudaEventSynchronize(c->merged_last_use) != cudaSuccess) return c->fail(DIT_ECUDA, "merged copy still in use");
   for (auto& lm : adapted_lins(c)) lm.first->has_m = false;   // base weights were never written: exact restore
   c->merged_adapter = -1;
   c->plan_B = -1;
@@ -1628,6 +1652,16 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     if (pe != cudaSuccess) return c->fail(DIT_ECUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
   }
   c->launches = 0;
+  // asynchronously loaded / patched adapters: order this step after their copies on THIS stream
+  {
+    std::vector<int> waited;
+    for (int i = 0; i < S; ++i)
+      if (req_slot[i] >= 0 && std::find(waited.begin(), waited.end(), req_slot[i]) == waited.end()) {
+        cudaStreamWaitEvent(s, c->slot_ready[req_slot[i]], 0);
+        waited.push_back(req_slot[i]);
+      }
+    if (c->merged_adapter >= 0) cudaStreamWaitEvent(s, c->merge_ready, 0);
+  }
   const int D = c->D, H = c->H, d = c->d, F = c->F, C = c->C, Ct = c->Ct;
   const int nt = Nt / P, ni = Ni / P, N = nt + ni;
   const int Mt = S * nt, Mi = S * ni, Mj = S * N;
@@ -2279,6 +2313,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
 
   for (int i = 0; i < S; ++i)
     if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
+  if (c->merged_adapter >= 0) cudaEventRecord(c->merged_last_use, s);
   c->last_launches = c->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));
