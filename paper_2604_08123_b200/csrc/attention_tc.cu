@@ -529,316 +529,6 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   }
 }
 
-
-// ---------------------------------------------------------------------------------------------
-// v2: HALF-ROW softmax.  Same TMEM plan, TMA ring and ping-pong MMA schedule as attn_tc_kernel,
-// but every query row is owned by TWO threads: warps w and w + 4 of a tile share TMEM lane
-// quarter w % 4 (and therefore an SMSP) and take kv columns [0, 64) and [64, 128) of S.  The
-// row max is exchanged through shared memory behind a 64-thread named barrier, each half writes
-// its 32 P columns, and the PV MMA starts on the first half's P.  One thread per row left the
-// SMSP with a single dependent instruction stream per tile (~0.5 IPC: S ready -> P released
-// ~1100 clk against the 1024 clk the other tile's MMAs cover); two interleaved streams halve
-// the critical path, so the tensor pipe, not the softmax, bounds the kernel.
-//   warps 0-7   tile 0 (w: quarter w % 4, half w / 4), warps 8-15 tile 1
-//   warps 16-17 idle, 18 TMA producer, 19 TMEM allocator + MMA (highest ids)
-// 640 threads: setmaxnreg gives the 16 softmax warps SM2_REG_SOFTMAX registers and the last
-// warpgroup SM2_REG_OTHER (launch pool = 640 x 96).
-constexpr int SM2_WARPS_PER_TILE = 8;
-constexpr int THREADS2 = (NQ * SM2_WARPS_PER_TILE + 4) * 32;   // 640
-#ifndef SM2_REG_SOFTMAX
-#define SM2_REG_SOFTMAX 112
-#endif
-#ifndef SM2_REG_OTHER
-#define SM2_REG_OTHER 32
-#endif
-static_assert(16 * 32 * SM2_REG_SOFTMAX + 4 * 32 * SM2_REG_OTHER <= THREADS2 * 96, "register split exceeds the pool");
-template <int HD> __host__ __device__ constexpr int smem2_bytes() {
-  return tile_bytes<HD>() * (NQ + KST + VST) + 1024 + 256 + 2 * NQ * 4 * 2 * 32 * 4 + NQ * 4 * 2 * 32 * 4;
-}
-
-template <int HD, bool RAGGED>
-__global__ void __launch_bounds__(THREADS2, 1) attn_tc2_kernel(const __grid_constant__ Maps maps, const __grid_constant__ AttnParams p) {
-  constexpr int TILE_BYTES = tile_bytes<HD>();
-  constexpr int NPANEL = HD / 64;
-  constexpr int HO = HD / 2;                       // O columns per half-row thread
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + NQ * TILE_BYTES;
-  uint8_t* sV = sK + KST * TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;        // [KST]
-  uint64_t* k_empty = bars + 3;       // [KST]
-  uint64_t* v_full = bars + 5;        // [VST]
-  uint64_t* v_empty = bars + 7;       // [VST]
-  uint64_t* s_full = bars + 9;        // [NQ]
-  uint64_t* p_half = bars + 11;       // [NQ][2] P of kv [0,64) / [64,128) in TMEM
-  uint64_t* o_done = bars + 15;       // [NQ]
-  uint64_t* o_free = bars + 17;       // [NQ]
-  uint64_t* q_empty = bars + 19;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
-  // row-max exchange [parity][tile][quarter][half][lane], row-sum exchange [tile][quarter][half][lane]
-  float* xmax = reinterpret_cast<float*>(smem + tile_bytes<HD>() * (NQ + KST + VST) + 1024);
-  float* xsum = xmax + 2 * NQ * 4 * 2 * 32;
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int N = p.N;
-  const int nqb = (N + NQ * BQ - 1) / (NQ * BQ);
-  const int total = nqb * p.H * p.B;
-
-  constexpr int W_LOAD = NQ * SM2_WARPS_PER_TILE + 2, W_MMA = W_LOAD + 1;
-  if (warp == W_LOAD && lane == 0) {
-    tma_prefetch_desc(&maps.q);
-    tma_prefetch_desc(&maps.k);
-    tma_prefetch_desc(&maps.v);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_half[2 * i], 4);
-      mbar_init(&p_half[2 * i + 1], 4);
-      mbar_init(&o_done[i], 1);
-      mbar_init(&o_free[i], SM2_WARPS_PER_TILE);
-    }
-    fence_barrier_init();
-  }
-  if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (warp >= NQ * SM2_WARPS_PER_TILE) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SM2_REG_OTHER));
-    if (warp == W_LOAD) {
-      if (lane == 0) {
-        int g = 0, it = 0;
-        for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-          const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
-          const int nkv = kv_tiles<RAGGED>(p, bh / p.H);
-          if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
-          mbar_expect_tx(q_full, NQ * TILE_BYTES);
-          for (int t = 0; t < NQ; ++t)
-            for (int pn = 0; pn < NPANEL; ++pn)
-              tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + pn * PANEL, pn * 64, q0 + t * BQ, bh);
-          for (int j = 0; j < nkv; ++j, ++g) {
-            const int st = g & 1;
-            const uint32_t ph = (g >> 1) & 1;
-            mbar_wait(&k_empty[st], ph ^ 1);
-            mbar_expect_tx(&k_full[st], TILE_BYTES);
-            for (int pn = 0; pn < NPANEL; ++pn)
-              tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
-            mbar_wait(&v_empty[st], ph ^ 1);
-            mbar_expect_tx(&v_full[st], TILE_BYTES);
-            for (int pn = 0; pn < NPANEL; ++pn)
-              tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
-          }
-        }
-      }
-    } else if (warp == W_MMA) {
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BKV);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD) | (1u << 16);   // B (V) MN-major
-      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      auto issue_qk = [&](int t, int g) {
-        const int st = g & 1;
-        if (t == 0) mbar_wait(&k_full[st], (g >> 1) & 1);
-        tc_fence_after();
-        if constexpr (HD == 128)
-          tc_mma_ss_k128_warp<PANEL>(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
-                                     smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
-        else
-          tc_mma_ss_k64_warp(tm + COL_S + t * 128, smem_desc_k_sw128(smem_u32(sQ + t * TILE_BYTES)),
-                             smem_desc_k_sw128(smem_u32(sK + st * TILE_BYTES)), idesc_qk, 0);
-        tc_commit_warp(&s_full[t]);
-        if (t == NQ - 1) tc_commit_warp(&k_empty[st]);
-      };
-      auto issue_pv = [&](int t, int g, int j, int it) {
-        const int st = g & 1;
-        mbar_wait(&p_half[2 * t], g & 1);
-        if (j == 0 && it > 0) mbar_wait(&o_free[t], (it - 1) & 1);
-        if (t == 0) mbar_wait(&v_full[st], (g >> 1) & 1);
-        tc_fence_after();
-        const uint64_t vdesc = desc_mn_sw128(smem_u32(sV + st * TILE_BYTES), PANEL);
-        const uint32_t od = tm + COL_O + t * HD, pa = tm + COL_S + t * 128;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, (j | kk) != 0);
-        mbar_wait(&p_half[2 * t + 1], g & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 4; kk < 8; ++kk) tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, 1);
-        tc_commit_warp(&o_done[t]);
-        if (t == NQ - 1) tc_commit_warp(&v_empty[st]);
-      };
-      int g = 0, it = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-        const int nkv = kv_tiles<RAGGED>(p, (w / nqb) / p.H);
-        mbar_wait(q_full, it & 1);
-        issue_qk(0, g);
-        issue_qk(1, g);
-        if (nkv == 1) tc_commit_warp(q_empty);
-        for (int j = 0; j < nkv; ++j) {
-          issue_pv(0, g + j, j, it);
-          if (j + 1 < nkv) issue_qk(0, g + j + 1);
-          issue_pv(1, g + j, j, it);
-          if (j + 1 < nkv) {
-            issue_qk(1, g + j + 1);
-            if (j + 2 == nkv) tc_commit_warp(q_empty);
-          }
-        }
-        g += nkv;
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SM2_REG_SOFTMAX));
-    const int t = warp / SM2_WARPS_PER_TILE;
-    const int wi = warp % SM2_WARPS_PER_TILE;
-    const int wq = wi & 3;                         // TMEM lane quarter (= warp % 4)
-    const int hf = wi >> 2;                        // kv column half of S, O column half
-    const int row = wq * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const uint32_t colS = tmem + lane_base + COL_S + t * 128;
-    const uint32_t colO = tmem + lane_base + COL_O + t * HD + hf * HO;
-    const int bar_id = 1 + t * 4 + wq;             // named barrier of the two half-row warps
-    float* my_max = xmax + ((t * 4 + wq) * 2 + hf) * 32 + lane;          // + parity * NQ*4*2*32
-    const float* their_max = xmax + ((t * 4 + wq) * 2 + (hf ^ 1)) * 32 + lane;
-    constexpr int XPAR = NQ * 4 * 2 * 32;
-    const float sl2 = p.scale_log2;
-    int g = 0, it = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-      const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
-      const int b = bh / p.H, h = bh - b * p.H;
-      const int Nv = seq_len_of<RAGGED>(p, b), nkv = kv_tiles<RAGGED>(p, b);
-      float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j, ++g) {
-        mbar_wait(&s_full[t], g & 1);
-        tc_fence_after();
-        uint32_t sr[64];
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          tmem_ld32(colS + hf * 64 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        tmem_ld_wait();
-        const int kv_valid = Nv - j * BKV - hf * 64;
-        if (kv_valid < 64) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e >= kv_valid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float m8[8];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) m8[a] = fmaxf(__uint_as_float(sr[2 * a]), __uint_as_float(sr[2 * a + 1]));
-#pragma unroll
-        for (int e = 16; e < 64; e += 16)
-#pragma unroll
-          for (int a = 0; a < 8; ++a)
-            m8[a] = fmaxf(m8[a], fmaxf(__uint_as_float(sr[e + 2 * a]), __uint_as_float(sr[e + 2 * a + 1])));
-        const float mloc = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        // exchange with the other half of the row (slot by kv-tile parity: a half can run at most one
-        // tile ahead, and only after the partner passed this tile's barrier); the barrier also orders
-        // this half's S loads before the partner's P stores into S columns [32, 64)
-        const int par = (g & 1) * XPAR;
-        my_max[par] = mloc;
-        tc_fence_before();
-        named_bar_sync(bar_id, 64);
-        tc_fence_after();
-        const float mx = fmaxf(mloc, their_max[par]) * sl2;
-        const bool need = mx > m_used + RESCALE_THRESH;
-        const float m_new = need ? mx : m_used;
-        if (j > 0 && __any_sync(0xffffffff, need)) {
-          const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
-          mbar_wait(&o_done[t], (g - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < HO / 16; ++c) {
-            uint32_t r[16];
-            tmem_ld16(colO + c * 16, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-            tmem_st16(colO + c * 16, r);
-          }
-          tmem_st_wait();
-          l *= alpha;
-        }
-        m_used = m_new;
-        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
-        // this half's 64 exponentials -> 32 bf16 pairs = P columns [hf*32, hf*32 + 32); the row
-        // sum is accumulated as they are produced (two warps per SMSP leave issue slots for it,
-        // and the scores die as they go: no spill at SM2_REG_SOFTMAX registers)
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[32 * c + 2 * e]), __uint_as_float(sr[32 * c + 2 * e + 1])), sl2v, nm);
-            float2 pp;
-            constexpr int PM = HD == 64 ? ATTN_POLY_MOD64 : POLY_MOD, PR = HD == 64 ? ATTN_POLY_RES64 : POLY_RES;
-            if ((e % PM) >= PM - PR) {
-              pp = poly_exp2x2(x);
-            } else {
-              pp.x = mufu_exp2(x.x);
-              pp.y = mufu_exp2(x.y);
-            }
-            if (e & 1) acc1 = __fadd2_rn(acc1, pp);
-            else acc0 = __fadd2_rn(acc0, pp);
-            r[e] = pack_bf16(pp.x, pp.y);
-          }
-          tmem_st16(colS + hf * 32 + c * 16, r);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_half[2 * t + hf]);
-        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-      }
-      // epilogue: the row's two partial sums, then this half's O columns / l -> bf16
-      float* my_sum = xsum + ((t * 4 + wq) * 2 + hf) * 32 + lane;
-      const float* their_sum = xsum + ((t * 4 + wq) * 2 + (hf ^ 1)) * 32 + lane;
-      *my_sum = l;
-      named_bar_sync(bar_id, 64);
-      const float l_row = l + *their_sum;
-      const int n = q0 + t * BQ + row;
-      uint4* dst = n < N ? reinterpret_cast<uint4*>(attn_out_addr(p, b, n, h, HD) + hf * HO) : nullptr;
-      mbar_wait(&o_done[t], (g - 1) & 1);
-      tc_fence_after();
-      uint32_t o[HO];
-#pragma unroll
-      for (int c = 0; c < HO / 32; ++c) tmem_ld32(colO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32 * c]));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[t]);
-      // the partner reads my row sum before either of us writes the next item's (second barrier)
-      named_bar_sync(bar_id, 64);
-      if (dst != nullptr) {
-        const float inv = 1.0f / l_row;
-#pragma unroll
-        for (int q = 0; q < HO / 8; ++q) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-          dst[q] = u;
-        }
-        if (p.split == 3) __threadfence_system();   // fused exchange: peer stores, system scope
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == W_MMA) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
 }  // namespace attn_tc
 
 cudaError_t attention_set_trace(long long* buf) {
@@ -848,19 +538,10 @@ cudaError_t attention_set_trace(long long* buf) {
 template <int HD, bool RAGGED>
 static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   using namespace attn_tc;
-  // v2 (half-row softmax) by default; DIT_ATTN_V1=1 selects the one-thread-per-row kernel (comparison)
-  static int v1 = -1;
-  if (v1 < 0) {
-    const char* e = getenv("DIT_ATTN_V1");
-    v1 = (e && e[0] == '1') ? 1 : 0;
-  }
   constexpr int SMEM = smem_bytes<HD>();
-  constexpr int SMEM2 = smem2_bytes<HD>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_tc2_kernel<HD, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -880,10 +561,7 @@ static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   // persistent: one CTA per SM walks work items (query block fastest, so the CTAs running at
   // the same time share each head's K/V in L2)
   const int total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
-  if (v1)
-    attn_tc_kernel<HD, RAGGED><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
-  else
-    attn_tc2_kernel<HD, RAGGED><<<dim3(std::min(total, sms)), THREADS2, SMEM2, s>>>(m, p);
+  attn_tc_kernel<HD, RAGGED><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
 
