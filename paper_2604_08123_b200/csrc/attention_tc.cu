@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       tc_commit_warp(&s_full[t]);
       if (t == NQ - 1) tc_commit_warp(&k_empty[st]);
     };
-    auto issue_pv = [&](int t, int g, int j, int it) {
+    auto issue_pv = [&](int t, int g, int j, int it, int nkv) {
       const int st = g & 1;
       if (lane == 0 && tr) TRACE(15 + t, j);
       mbar_wait(&p_full[t], g & 1);
@@ -334,7 +334,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 #pragma unroll
         for (int kk = 6; kk < 8; ++kk) tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, 1);
       }
-      tc_commit_warp(&o_done[t]);
+      // O of this work item is final after its last PV: the only phase anyone waits on (the
+      // epilogue).  Earlier PVs need no barrier: the commit of the next QK into S_t covers them.
+      if (j == nkv - 1) tc_commit_warp(&o_done[t]);
       if (t == NQ - 1) tc_commit_warp(&v_empty[st]);
     };
     int g = 0, it = 0;
@@ -346,9 +348,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       issue_qk(1, g, 0);
       if (nkv == 1) tc_commit_warp(q_empty);
       for (int j = 0; j < nkv; ++j) {
-        issue_pv(0, g + j, j, it);
+        issue_pv(0, g + j, j, it, nkv);
         if (j + 1 < nkv) issue_qk(0, g + j + 1, j + 1);
-        issue_pv(1, g + j, j, it);
+        issue_pv(1, g + j, j, it, nkv);
         if (j + 1 < nkv) {
           issue_qk(1, g + j + 1, j + 1);
           if (j + 2 == nkv) tc_commit_warp(q_empty);   // last QK of this item issued
@@ -429,8 +431,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         const float m_new = need ? mx : m_used;
         if (j > 0 && __any_sync(0xffffffff, need)) {
           const float alpha = need ? mufu_exp2(m_used - m_new) : 1.0f;
-          mbar_wait(&o_done[t], (g - 1) & 1);
-          tc_fence_after();
+          // O_t holds PV(t, j-1): complete, since S_t(j) (waited above) was committed after it
 #pragma unroll 1
           for (int c = 0; c < HD / 16; ++c) {
             uint32_t r[16];
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       // (the output address first: its temporaries die before the 128 O registers go live)
       const int n = q0 + t * BQ + row;
       uint4* dst = n < N ? reinterpret_cast<uint4*>(attn_out_addr(p, b, n, h, HD)) : nullptr;
-      mbar_wait(&o_done[t], (g - 1) & 1);
+      mbar_wait(&o_done[t], it & 1);   // one phase per work item
       tc_fence_after();
       uint32_t o[HD];
 #pragma unroll
