@@ -537,9 +537,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == W_MMA) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
-  // (the cluster barrier already orders the allocator's address write; the CTA barrier makes that
-  // visible to compute-sanitizer's racecheck, which does not model barrier.cluster for shared::cta)
-  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
