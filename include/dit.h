@@ -170,9 +170,29 @@ int lora_unregister(dit_ctx* ctx, int32_t adapter_id);
  * DIT_ENOWEIGHTS, DIT_ECUDA.  Validation precedes any enqueue. */
 size_t dit_merge_bytes(const dit_config* cfg);
 int lora_merge(dit_ctx* ctx, int32_t adapter_id, void* merged, size_t bytes, void* stream);
+/* In-place hot patch ("hot-patch the base model in GPU memory";
+ * :1504-1509): W' = bf16(W + scale * B A) is written OVER the base weights of every
+ * adapted linear -- no second copy.  For an exact restore the merge logs, into the
+ * caller's device buffer `undo` (8-byte aligned, 8 bytes per entry), every element
+ * whose original value the inverse bf16(W' - scale * B A) would not give back
+ * (rounding W + d lost bits: W' in a higher binade than W, or a tie); lora_unmerge
+ * then applies the inverse everywhere and rewrites the logged elements, so the
+ * weights come back bit for bit.  The merge runs two passes on `stream`: a count
+ * (the host waits for it: *undo_entries receives the entries needed), then, only
+ * if entries * 8 <= undo_bytes, the patch (else DIT_ENOMEM and nothing is
+ * written).  It waits for every dit_step enqueued before it (they read the base
+ * weights); steps after it wait for it (events).  The borrowed base weights ARE
+ * MODIFIED until lora_unmerge; dit_load_weights is refused meanwhile.  Otherwise as
+ * lora_merge (a patched replica serving one adapter).  Errors: as lora_merge, plus
+ * DIT_ENOMEM (undo log too small), DIT_EINVAL (max_rank not 64 or 128 after
+ * padding / misaligned undo). */
+int lora_merge_inplace(dit_ctx* ctx, int32_t adapter_id, void* undo, size_t undo_bytes,
+                       uint64_t* undo_entries, void* stream);
 /* Restore the base weights.  Waits (host) for the last enqueued dit_step that
- * read the merged copy, so `merged` may be freed once this returns.
- * Errors: DIT_ENOENT (nothing merged). */
+ * read the merged weights, so `merged` may be freed once this returns; after an
+ * in-place merge it also restores the weights (inverse + undo log, on the legacy
+ * default stream, synchronised) before returning.
+ * Errors: DIT_ENOENT (nothing merged), DIT_ECUDA. */
 int lora_unmerge(dit_ctx* ctx);
 
 /* -------------------------------------------------------------- ControlNet */

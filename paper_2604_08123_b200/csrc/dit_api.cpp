@@ -168,6 +168,14 @@ struct dit_ctx {
   std::vector<cudaEvent_t> slot_ready;   // recorded after lora_register's copies
   cudaEvent_t merge_ready = nullptr;     // recorded after lora_merge's kernel
   cudaEvent_t merged_last_use = nullptr; // recorded by every dit_step that reads the merged copy
+  cudaEvent_t step_done = nullptr;       // recorded at the end of every dit_step (in-place merge waits)
+  // in-place merge (lora_merge_inplace): W' written over the base weights, undo log of the elements
+  // the inverse cannot recover
+  bool merged_inplace = false;
+  unsigned long long* inplace_log = nullptr;
+  unsigned long long inplace_entries = 0;
+  int inplace_tiles = 0, inplace_njobs = 0;
+  unsigned long long* mcount = nullptr;  // device counter (workspace)
   int merged_adapter = -1;           // lora_merge: adapter patched into tm_m copies (-1: none)
   // ControlNet registrations for the next step
   struct CnReg { const void* ptr; float scale; cudaEvent_t ready; const uint32_t* flag; uint32_t expect; };
@@ -337,7 +345,7 @@ Layout layout_of(const dit_config& c) {
   L.xb = cv.take((size_t)c.max_batch * c.max_img_tokens * c.in_channels * 2);
   // CFG: v of both branches, twice (latent parallelism over peer stores alternates buffers by step parity)
   L.vcfg = cv.take(4 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);
-  L.mjobs = cv.take((size_t)n_lora_modules(c) * merge_job_bytes());   // lora_merge job table
+  L.mjobs = cv.take((size_t)n_lora_modules(c) * merge_job_bytes() + 256);   // lora_merge job table + counter
   L.rope = cv.take((size_t)c.max_batch * N * (d / 2) * 8);   // one table per sequence for ragged batches
   L.mod = cv.take(8 * mod_total * 4);
   L.vec = cv.take(8 * D * 4);
@@ -412,6 +420,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   c->xb = reinterpret_cast<bf16_t*>(w + L.xb);
   c->vcfg = reinterpret_cast<float*>(w + L.vcfg);
   c->mjobs = w + L.mjobs;
+  c->mcount = reinterpret_cast<unsigned long long*>(w + L.mjobs + align_up((size_t)n_lora_modules(*cfg) * merge_job_bytes(), 256));
   c->rope = reinterpret_cast<float2*>(w + L.rope);
   c->mod = reinterpret_cast<float*>(w + L.mod);
   c->vec = reinterpret_cast<float*>(w + L.vec);
@@ -482,6 +491,7 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   for (auto& e : c->slot_ready) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->merge_ready, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->merged_last_use, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming);
   c->dbl[0].resize(c->Ld);
   c->dbl[1].resize(c->Ld);
   c->sgl.resize(c->Ls);
@@ -511,6 +521,7 @@ extern "C" void dit_destroy(dit_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->merge_ready) cudaEventDestroy(c->merge_ready);
   if (c->merged_last_use) cudaEventDestroy(c->merged_last_use);
+  if (c->step_done) cudaEventDestroy(c->step_done);
   for (void* ptr : c->ipc_opened) dit_ipc_close(ptr);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->lp_comm) ncclCommDestroy(c->lp_comm);
@@ -806,6 +817,37 @@ extern "C" size_t dit_merge_bytes(const dit_config* cfg) {
   return off;
 }
 
+namespace {
+// Job table of every adapted linear for the tensor-core merge kernel (merge_tc.cu), copied to the
+// workspace on `s` (staged: the host buffer is reusable at once).  out_maps == nullptr: in place
+// (the output map is the weight map itself).
+bool upload_merge_jobs(dit_ctx* c, int slot, const std::vector<CUtensorMap>* out_maps, cudaStream_t s, int* tiles) {
+  auto lins = adapted_lins(c);
+  const int ra = c->r_alloc;
+  const float scale = c->slot_scale_h[slot];
+  const size_t jb = merge_job_bytes();
+  std::vector<uint8_t> store(align_up(lins.size() * jb, 64) + 64);
+  uint8_t* host = reinterpret_cast<uint8_t*>(align_up(reinterpret_cast<uintptr_t>(store.data()), 64));
+  int t = 0;
+  long long elem = 0;
+  for (size_t k = 0; k < lins.size(); ++k) {
+    Lin& L = *lins[k].first;
+    const LoraPool& P = c->pools[lins[k].second];
+    if (!merge_job_fill(host + k * jb, L.tm, out_maps ? (*out_maps)[k] : L.tm,
+                        static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
+                        static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, L.out, L.in, ra, scale, t,
+                        L.w, elem))
+      return false;
+    t += merge_job_tiles(host + k * jb);
+    elem += (long long)L.out * L.in;
+  }
+  // pageable source: the runtime stages it before returning, so `store` may die right after
+  cudaMemcpyAsync(c->mjobs, host, lins.size() * jb, cudaMemcpyHostToDevice, s);
+  *tiles = t;
+  return true;
+}
+}  // namespace
+
 extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t bytes, void* stream) {
   if (!c) return DIT_EINVAL;
   auto it = c->adapter_slot.find(adapter_id);
@@ -839,23 +881,8 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
   const char* legacy = getenv("DIT_MERGE_MMA_SYNC");
   const bool use_tc = !(legacy && legacy[0] == '1') && (ra == 64 || ra == 128);
   if (use_tc) {   // one job per adapted linear, one persistent launch
-    const size_t jb = merge_job_bytes();
-    uint8_t* host = static_cast<uint8_t*>(aligned_alloc(64, align_up(lins.size() * jb, 64)));
-    if (!host) return c->fail(DIT_ENOMEM, "host job table");
     int tiles = 0;
-    for (size_t k = 0; k < lins.size(); ++k) {
-      Lin& L = *lins[k].first;
-      const LoraPool& P = c->pools[lins[k].second];
-      if (!merge_job_fill(host + k * jb, L.tm, maps[k], static_cast<const uint8_t*>(P.A) + (size_t)slot * ra * P.in * 2,
-                          static_cast<const uint8_t*>(P.B) + (size_t)slot * P.out * ra * 2, L.out, L.in, ra, scale,
-                          tiles)) {
-        free(host);
-        return c->fail(DIT_EINVAL, "tensor map for the merge operands failed");
-      }
-      tiles += merge_job_tiles(host + k * jb);
-    }
-    cudaMemcpyAsync(c->mjobs, host, lins.size() * jb, cudaMemcpyHostToDevice, s);   // (staged: host reusable)
-    free(host);
+    if (!upload_merge_jobs(c, slot, &maps, s, &tiles)) return c->fail(DIT_EINVAL, "tensor map for the merge operands failed");
     cudaError_t e = lora_merge_tc_launch(c->mjobs, (int)lins.size(), tiles, ra, c->num_sms, s);
     if (e != cudaSuccess) return c->fail(DIT_ECUDA, "lora_merge kernel: %s", cudaGetErrorString(e));
   } else {
@@ -880,12 +907,70 @@ extern "C" int lora_merge(dit_ctx* c, int32_t adapter_id, void* merged, size_t b
   return DIT_OK;
 }
 
+extern "C" int lora_merge_inplace(dit_ctx* c, int32_t adapter_id, void* undo, size_t undo_bytes,
+                                  uint64_t* undo_entries, void* stream) {
+  if (!c) return DIT_EINVAL;
+  auto it = c->adapter_slot.find(adapter_id);
+  if (it == c->adapter_slot.end()) return c->fail(DIT_ENOENT, "adapter %d not registered", adapter_id);
+  if (c->merged_adapter >= 0) return c->fail(DIT_EEXIST, "adapter %d is already merged", c->merged_adapter);
+  if (!c->weights_ready) return c->fail(DIT_ENOWEIGHTS, "base weights not (fully) loaded");
+  if ((undo_bytes > 0 && !undo) || (reinterpret_cast<uintptr_t>(undo) & 7))
+    return c->fail(DIT_EINVAL, "undo log must be an 8-byte aligned device buffer");
+  const int ra = c->r_alloc;
+  if (ra != 64 && ra != 128) return c->fail(DIT_EINVAL, "in-place merge needs r_alloc 64 or 128");
+  const int slot = it->second;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // every step enqueued so far reads the base weights; the adapter's copies may still be in flight
+  cudaStreamWaitEvent(s, c->step_done, 0);
+  cudaStreamWaitEvent(s, c->slot_ready[slot], 0);
+  int tiles = 0;
+  if (!upload_merge_jobs(c, slot, nullptr, s, &tiles)) return c->fail(DIT_EINVAL, "tensor map for the merge operands failed");
+  const int nj = (int)adapted_lins(c).size();
+  // pass 1: count the elements the inverse cannot recover (nothing is written)
+  cudaMemsetAsync(c->mcount, 0, 8, s);
+  cudaError_t e = lora_merge_tc_launch(c->mjobs, nj, tiles, ra, c->num_sms, s, 1, nullptr, c->mcount);
+  if (e != cudaSuccess) return c->fail(DIT_ECUDA, "merge count kernel: %s", cudaGetErrorString(e));
+  unsigned long long need = 0;
+  if (cudaMemcpyAsync(&need, c->mcount, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return c->fail(DIT_ECUDA, "merge count readback failed");
+  if (undo_entries) *undo_entries = need;
+  if (need * 8 > undo_bytes)
+    return c->fail(DIT_ENOMEM, "undo log needs %llu entries (%llu bytes), got %zu bytes; weights untouched", need,
+                   need * 8, undo_bytes);
+  // pass 2: W' over W, the unrecoverable elements logged
+  cudaMemsetAsync(c->mcount, 0, 8, s);
+  e = lora_merge_tc_launch(c->mjobs, nj, tiles, ra, c->num_sms, s, 2, static_cast<unsigned long long*>(undo), c->mcount);
+  if (e != cudaSuccess) return c->fail(DIT_ECUDA, "in-place merge kernel: %s", cudaGetErrorString(e));
+  cudaStreamWaitEvent(s, c->slot_last_use[slot], 0);
+  cudaEventRecord(c->slot_last_use[slot], s);
+  cudaEventRecord(c->merge_ready, s);
+  c->merged_adapter = adapter_id;
+  c->merged_inplace = true;
+  c->inplace_log = static_cast<unsigned long long*>(undo);
+  c->inplace_entries = need;
+  c->inplace_tiles = tiles;
+  c->inplace_njobs = nj;
+  c->plan_B = -1;
+  return DIT_OK;
+}
+
 extern "C" int lora_unmerge(dit_ctx* c) {
   if (!c) return DIT_EINVAL;
   if (c->merged_adapter < 0) return c->fail(DIT_ENOENT, "no adapter is merged");
   // the caller may free / reuse the merged buffer after this returns: wait for its last reader
   if (cudaEventSynchronize(c->merged_last_use) != cudaSuccess) return c->fail(DIT_ECUDA, "merged copy still in use");
-  for (auto& lm : adapted_lins(c)) lm.first->has_m = false;   // base weights were never written: exact restore
+  if (c->merged_inplace) {   // W = bf16(W' - s B A) everywhere, then the logged elements exactly
+    cudaStream_t s = nullptr;   // (legacy default stream; synchronised below)
+    cudaError_t e = lora_merge_tc_launch(c->mjobs, c->inplace_njobs, c->inplace_tiles, c->r_alloc, c->num_sms, s, 3,
+                                         nullptr, nullptr);
+    if (e == cudaSuccess) e = restore_log_launch(c->mjobs, c->inplace_njobs, c->inplace_log, c->inplace_entries, c->num_sms, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return c->fail(DIT_ECUDA, "restore: %s", cudaGetErrorString(e));
+    c->merged_inplace = false;
+    c->inplace_log = nullptr;
+    c->inplace_entries = 0;
+  }
+  for (auto& lm : adapted_lins(c)) lm.first->has_m = false;   // copy mode: base weights never written
   c->merged_adapter = -1;
   c->plan_B = -1;
   return DIT_OK;
@@ -2314,6 +2399,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   for (int i = 0; i < S; ++i)
     if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
   if (c->merged_adapter >= 0) cudaEventRecord(c->merged_last_use, s);
+  cudaEventRecord(c->step_done, s);
   c->last_launches = c->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));

@@ -240,12 +240,20 @@ cudaError_t controlnet_push_launch(void* dst, const void* src, size_t bytes, uin
 // linear: the host fills one job per linear (merge_job_fill: w_map / out_map = the [rows][cols]
 // box {64, 128} maps of W and of the output, tile_begin = running tile count) into device memory
 // (merge_job_bytes each, 64-byte aligned); ra in {64, 128}.  Same result as lora_merge_launch.
+// w / elem_base: the linear's weights and the index of its [0][0] in the concatenation of all
+// adapted linears (undo-log addresses of the in-place merge).  mode: 0 merge into out, 1 count the
+// elements the inverse cannot recover (*log_count +=), 2 merge in place (out = w) logging those
+// elements (value << 48 | index) at log[atomicAdd(log_count)], 3 restore W = bf16(W' - s BA) in place.
 size_t merge_job_bytes();
 bool merge_job_fill(void* job, const CUtensorMap& w_map, const CUtensorMap& out_map, const void* A, const void* Bm,
-                    int rows, int cols, int ra, float scale, int tile_begin);
+                    int rows, int cols, int ra, float scale, int tile_begin, const void* w, long long elem_base);
 int merge_job_tiles(const void* job);
 cudaError_t lora_merge_tc_launch(const void* jobs_dev, int njobs, int total_tiles, int ra, int num_sms,
-                                 cudaStream_t s);
+                                 cudaStream_t s, int mode = 0, unsigned long long* log = nullptr,
+                                 unsigned long long* log_count = nullptr);
+// after mode 3: rewrite the n logged elements exactly
+cudaError_t restore_log_launch(const void* jobs_dev, int njobs, const unsigned long long* log, unsigned long long n,
+                               int num_sms, cudaStream_t s);
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 

@@ -60,6 +60,8 @@ EXPORTS = {
     "dit_merge_bytes": (C.c_size_t, [C.POINTER(dit_config)]),
     "lora_merge": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p]),
     "lora_unmerge": (C.c_int, [C.c_void_p]),
+    "lora_merge_inplace": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64),
+                                     C.c_void_p]),
     "controlnet_inject": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p]),
     "controlnet_clear": (C.c_int, [C.c_void_p]),
     "controlnet_inject_flag": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float, C.c_void_p,
@@ -231,6 +233,26 @@ class DiT:
         self._merged = merged
         _check(self.lib.lora_merge(self.ctx, adapter_id, C.c_void_p(ptr + pad), merged.numel() - pad,
                                    self._stream(stream)), self.ctx)
+
+    def lora_merge_inplace(self, adapter_id: int, undo=None, stream=None) -> int:
+        """Hot-patch `adapter_id` over the base weights; `undo`: a device tensor (8-byte aligned) for the
+        undo log.  Returns the entries used.  With undo=None the log is sized by a first call that
+        returns DIT_ENOMEM with the count, then allocated here (kept until lora_unmerge)."""
+        import torch
+        n = C.c_uint64(0)
+        if undo is None:
+            r = self.lib.lora_merge_inplace(self.ctx, adapter_id, None, 0, C.byref(n), self._stream(stream))
+            if r == 0:
+                self._undo = None
+                return 0
+            if r != 2:
+                _check(r, self.ctx)
+            undo = torch.empty(max(1, n.value), dtype=torch.int64, device=f"cuda:{self.device}")
+        self._undo = undo
+        _check(self.lib.lora_merge_inplace(self.ctx, adapter_id, C.c_void_p(undo.data_ptr()),
+                                           undo.numel() * undo.element_size(), C.byref(n), self._stream(stream)),
+               self.ctx)
+        return n.value
 
     def lora_unmerge(self):
         _check(self.lib.lora_unmerge(self.ctx), self.ctx)

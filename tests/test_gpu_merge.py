@@ -116,3 +116,50 @@ def test_merge_error_paths(torch_cuda):
     assert codes(lambda: m.step(batch)) == 10                        # DIT_EADAPTER
     m.lora_unmerge()
     m.lora_unregister(1)
+
+
+@pytest.mark.parametrize("wide,rank", [(False, 8), (True, 100)])
+def test_inplace_merge_exact_restore(torch_cuda, wide, rank):
+    """In-place hot patch: W' over the base weights, no second copy.
+    The merged step equals the copy-merged step bitwise (same W'); lora_unmerge gives back every
+    base weight BIT FOR BIT (inverse + undo log of the unrecoverable elements); a too-small undo
+    log is refused with DIT_ENOMEM before anything is written."""
+    import dataclasses
+    torch = torch_cuda
+    from paper_2604_08123_b200.dit import DitError
+    cfg = (dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, rope_axes=(16, 56, 56)) if wide
+           else synth.TINY_SINGLE)
+    hh, ww, nt = (8, 8, 16) if wide else (4, 4, 8)
+    batch = synth.make_batch(cfg, 2, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([5, 5], dtype=np.int32)
+    ref = _model(cfg, 2, hh * ww, nt, rank=rank, adapters=1)
+    ref.register_synthetic_lora(5, rank=rank, index=1, scale=0.75)
+    ref.lora_merge(5)
+    lat_copy, v_copy = ref.step(batch)
+    ref.lora_unmerge()
+    ref.close()
+
+    m = _model(cfg, 2, hh * ww, nt, rank=rank, adapters=1)
+    m.register_synthetic_lora(5, rank=rank, index=1, scale=0.75)
+    base = dataclasses.replace(batch, adapter_id=np.array([-1, -1], dtype=np.int32))
+    _, v_base = m.step(base)
+    before = {k: t.clone() for k, t in m.weights.items()}
+    small = torch.empty(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(DitError) as e:
+        m.lora_merge_inplace(5, undo=small)          # 8 bytes: too small for any real adapter
+    assert e.value.code == 2
+    for k, t in m.weights.items():
+        assert torch.equal(t, before[k]), k          # refused before anything was written
+    n = m.lora_merge_inplace(5)
+    torch.cuda.synchronize()
+    changed = sum(int((m.weights[mod + ".w"] != before[mod + ".w"]).sum()) for mod, _, _ in synth.lora_targets(cfg))
+    assert changed > 0 and 0 < n < changed            # patched in place; only some elements logged
+    lat, v = m.step(batch)
+    np.testing.assert_array_equal(v, v_copy)
+    np.testing.assert_array_equal(lat, lat_copy)
+    m.lora_unmerge()
+    for k, t in m.weights.items():
+        assert torch.equal(t, before[k]), k          # exact restore
+    _, v_after = m.step(base)
+    np.testing.assert_array_equal(v_after, v_base)
+    m.close()
