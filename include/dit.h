@@ -356,6 +356,28 @@ typedef struct dit_batch {
  * cfg_scale NULL), DIT_ENOWEIGHTS, DIT_ECUDA, DIT_ENCCL. */
 int dit_step(dit_ctx* ctx, const dit_batch* batch, void* stream);
 
+/* ------------------------------------------------------------- CUDA graphs */
+/* dit_graph_create captures ONE dit_step on `batch` (shape, adapter ids, device
+ * pointers, and the ControlNet registrations made before it -- slots, blocks,
+ * ready events) on `stream` (a non-default cudaStream_t) into an instantiated CUDA
+ * graph; nothing executes.  Every host->device upload of the step (plan tables,
+ * per-step scalars, ControlNet tables) is a copy node reading the graph's own
+ * pinned block.  dit_graph_launch replays it: it re-runs the step's host logic
+ * on `batch` in staging mode (validation, sigma / sigma_next / guidance / CFG and
+ * ControlNet scales, residual pointers -> the block; the registrations are then
+ * cleared, as by dit_step), then cudaGraphLaunch -- one launch instead of ~450.
+ * `batch` must match the captured one in shape, adapter ids and device pointers,
+ * and the ControlNet registrations in (slot, block, event) (else DIT_EINVAL);
+ * the host stays at most one replay ahead of the device.  Adapters must be
+ * registered (or merged) before the capture; replays wait on their events.
+ * Not capturable (DIT_EPARALLEL / DIT_EINVAL): in-process groups, the fused peer
+ * exchanges (their epochs are per launch), device-flag ControlNet inputs.
+ * A graph is bound to its ctx; destroy it before the ctx. */
+typedef struct dit_graph dit_graph;
+int dit_graph_create(dit_ctx* ctx, const dit_batch* batch, void* stream, dit_graph** out);
+int dit_graph_launch(dit_graph* graph, const dit_batch* batch, void* stream);
+void dit_graph_destroy(dit_graph* graph);
+
 /* Algorithmic tensor FLOPs of one dit_step on `batch` (DESIGN.md §5 formula:
  * projections 2MNK, attention 4 N^2 D per request-block, LoRA 2r(in+out)). */
 double dit_step_flops(const dit_ctx* ctx, const dit_batch* batch);

@@ -169,6 +169,17 @@ struct dit_ctx {
   cudaEvent_t merge_ready = nullptr;     // recorded after lora_merge's kernel
   cudaEvent_t merged_last_use = nullptr; // recorded by every dit_step that reads the merged copy
   cudaEvent_t step_done = nullptr;       // recorded at the end of every dit_step (in-place merge waits)
+  // pinned staging of every per-step host->device upload (plan tables, parameters, ControlNet
+  // tables, segment table): a ring of PIN_RING blocks, block i reused only after its copies ran
+  static constexpr int PIN_RING = 4;
+  uint8_t* pin = nullptr;                // PIN_RING x stage_bytes, cudaHostAlloc
+  size_t stage_bytes = 0;
+  cudaEvent_t pin_ev[PIN_RING] = {};
+  int pin_next = 0;
+  // the block the current dit_step stages into (a ring block, or a graph's own block)
+  uint8_t* st_base = nullptr;
+  size_t st_off = 0;
+  cudaEvent_t st_event = nullptr;        // capture: recorded once the graph's staging copies are done
   // in-place merge (lora_merge_inplace): W' written over the base weights, undo log of the elements
   // the inverse cannot recover
   bool merged_inplace = false;
@@ -369,6 +380,19 @@ Layout layout_of(const dit_config& c) {
 
 }  // namespace
 
+namespace {
+// upper bound of one dit_step's staged host->device bytes (16-byte aligned pieces)
+size_t stage_bytes_of(const dit_config& c) {
+  const size_t N = (size_t)c.max_img_tokens + c.max_txt_tokens;
+  const size_t R = (size_t)c.max_batch * N;
+  const size_t tiles = (R + GEMM_TM - 1) / GEMM_TM + 4;
+  const size_t ncn = (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8;
+  const size_t nseg = 2 * c.depth_double + c.depth_single + 1 + 6;
+  return 3 * (R * 4 + tiles * c.max_batch * 4 + tiles * 4 + tiles * 8 * 8 + 64) + 8 * 64 + 64 * 4 + 16 * 4 +
+         ncn * (2 * sizeof(void*) + 8) + 64 + nseg * sizeof(SkinnySeg) + 4096;
+}
+}  // namespace
+
 extern "C" size_t dit_workspace_bytes(const dit_config* cfg) {
   if (!cfg_valid(cfg, nullptr)) return 0;
   return layout_of(*cfg).total;
@@ -492,6 +516,14 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   cudaEventCreateWithFlags(&c->merge_ready, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->merged_last_use, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming);
+  c->stage_bytes = align_up(stage_bytes_of(*cfg), 256);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&c->pin), c->stage_bytes * dit_ctx::PIN_RING, cudaHostAllocDefault) !=
+      cudaSuccess) {
+    g_create_error = "cudaHostAlloc of the pinned staging ring failed";
+    delete c;
+    return DIT_ECUDA;
+  }
+  for (auto& e : c->pin_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   c->dbl[0].resize(c->Ld);
   c->dbl[1].resize(c->Ld);
   c->sgl.resize(c->Ls);
@@ -522,6 +554,9 @@ extern "C" void dit_destroy(dit_ctx* c) {
   if (c->merge_ready) cudaEventDestroy(c->merge_ready);
   if (c->merged_last_use) cudaEventDestroy(c->merged_last_use);
   if (c->step_done) cudaEventDestroy(c->step_done);
+  for (auto& e : c->pin_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->pin) cudaFreeHost(c->pin);
   for (void* ptr : c->ipc_opened) dit_ipc_close(ptr);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->lp_comm) ncclCommDestroy(c->lp_comm);
@@ -1648,8 +1683,19 @@ extern "C" int dit_sp_exchange(const dit_ctx* c) {
     if (_e != cudaSuccess) return c->fail(DIT_ECUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
   } while (0)
 
+// mode: STEP_RUN a normal step; STEP_CAPTURE the same enqueue sequence under stream capture (every
+// upload forced, staged in the graph's own pinned block; waits on outside events as external
+// nodes); STEP_STAGE validation + host tables staged into the graph's block, nothing enqueued
+// (dit_graph_launch refreshes the block its graph's copy nodes read, then replays the graph).
+enum { STEP_RUN = 0, STEP_CAPTURE = 1, STEP_STAGE = 2 };
+static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode);
+
 extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   if (!c) return DIT_EINVAL;
+  return step_impl(c, b, reinterpret_cast<cudaStream_t>(stream), STEP_RUN);
+}
+
+static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
   // ControlNet registrations apply to exactly one dit_step call: cleared on EVERY exit (a
   // validation error or a failed launch included), so no stale borrowed pointer outlives it
   struct CnClear {
@@ -1730,8 +1776,41 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   for (auto& kv : c->cn)
     if (kv.first.first >= S) return c->fail(DIT_EINVAL, "ControlNet registered for slot %d >= sequences %d", kv.first.first, S);
 
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
+  const bool capture = mode == STEP_CAPTURE, stage_only = mode == STEP_STAGE;
+  // events recorded outside a capture are waited on as external nodes; ours recorded inside it
+  // must stay usable outside the graph (lora_unregister / lora_unmerge wait on them)
+  const unsigned wait_fl = capture ? cudaEventWaitExternal : 0;
+  auto record = [&](cudaEvent_t e) {
+    if (capture) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+  };
+  if (mode == STEP_RUN) {   // pinned ring block for this step's uploads
+    const int i = c->pin_next++ % dit_ctx::PIN_RING;
+    cudaEventSynchronize(c->pin_ev[i]);   // its copies of PIN_RING steps ago have run
+    c->st_base = c->pin + (size_t)i * c->stage_bytes;
+  }
+  c->st_off = 0;
+  // stage `bytes` from host `src` into the pinned block and (unless staging only) enqueue its copy
+  auto UP = [&](void* dst, const void* src, size_t bytes) -> bool {
+    if (c->st_off + bytes > c->stage_bytes) return false;
+    uint8_t* p = c->st_base + c->st_off;
+    memcpy(p, src, bytes);
+    c->st_off = align_up(c->st_off + bytes, 16);
+    if (!stage_only) cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s);
+    return true;
+  };
+  struct ProfOff {   // no per-launch profiling events inside a graph
+    dit_ctx* c;
+    bool saved;
+    ~ProfOff() { c->prof_on = saved; }
+  } prof_guard{c, c->prof_on};
+  if (capture) c->prof_on = false;
+  if (capture || stage_only) {   // a graph carries every upload (its replays must not rely on caches)
+    c->plan_B = -1;
+    c->rope_key[0] = -1;
+    c->segs_dirty = true;
+  }
   {
     cudaError_t pe = cudaGetLastError();
     if (pe != cudaSuccess) return c->fail(DIT_ECUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
@@ -1740,12 +1819,12 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   // asynchronously loaded / patched adapters: order this step after their copies on THIS stream
   {
     std::vector<int> waited;
-    for (int i = 0; i < S; ++i)
+    for (int i = 0; i < S && !stage_only; ++i)
       if (req_slot[i] >= 0 && std::find(waited.begin(), waited.end(), req_slot[i]) == waited.end()) {
-        cudaStreamWaitEvent(s, c->slot_ready[req_slot[i]], 0);
+        cudaStreamWaitEvent(s, c->slot_ready[req_slot[i]], wait_fl);
         waited.push_back(req_slot[i]);
       }
-    if (c->merged_adapter >= 0) cudaStreamWaitEvent(s, c->merge_ready, 0);
+    if (c->merged_adapter >= 0 && !stage_only) cudaStreamWaitEvent(s, c->merge_ready, wait_fl);
   }
   const int D = c->D, H = c->H, d = c->d, F = c->F, C = c->C, Ct = c->Ct;
   const int nt = Nt / P, ni = Ni / P, N = nt + ni;
@@ -1761,10 +1840,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     for (int r = 0; r < 3; ++r) {
       if (build_rowspace(c, c->rs[r], Ms[r], rpr[r], req_slot, ht, hc, hs) < 0)
         return c->fail(DIT_ESHAPE, "too many distinct adapters in one 128-row tile");
-      cudaMemcpyAsync(c->rs[r].row_slot, c->rs[r].h_row_slot.data(), Ms[r] * 4, cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(c->rs[r].tile_slots, ht.data(), ht.size() * 4, cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(c->rs[r].tile_cnt, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice, s);
-      if (!hs.empty()) cudaMemcpyAsync(c->rs[r].shrink_list, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice, s);
+      bool ok = UP(c->rs[r].row_slot, c->rs[r].h_row_slot.data(), Ms[r] * 4);
+      ok &= UP(c->rs[r].tile_slots, ht.data(), ht.size() * 4);
+      ok &= UP(c->rs[r].tile_cnt, hc.data(), hc.size() * 4);
+      if (!hs.empty()) ok &= UP(c->rs[r].shrink_list, hs.data(), hs.size() * 8);
+      if (!ok) return c->fail(DIT_ENOMEM, "staging block overflow (plan tables)");
     }
     if (!any_lora)
       for (int r = 0; r < 3; ++r) c->rs[r].n_shrink = 0;
@@ -1778,7 +1858,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   const bool rope_per_seq = ragged && c->cfg.arch == DIT_ARCH_FLUX;
   const int rope_stride = rope_per_seq ? N * (d / 2) : 0;
   const std::vector<int> hw_key = rope_per_seq ? seq_hw : std::vector<int>();
-  if (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w || c->plan_hw != hw_key) {
+  if (!stage_only && (c->rope_key[0] != nt || c->rope_key[1] != ni || c->rope_key[2] != b->img_w || c->plan_hw != hw_key)) {
     if (c->cfg.arch == DIT_ARCH_SD3)   // no RoPE: the QKV epilogue rotates by angle 0 (exact identity)
       CKC(rope_table_launch(c->rope, nt, ni, 0, 0, 1, 0, 0, d, 1.f, s));   // theta 1, width 1: angle 0
     else if (rope_per_seq)
@@ -1799,10 +1879,10 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       iv[q] = img_valid[q];
       iv[8 + q] = seq_valid[q];
     }
-    cudaMemcpyAsync(c->p_img_valid, iv.data(), 8 * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->p_seq_valid, iv.data() + 8, 8 * 4, cudaMemcpyHostToDevice, s);
+    UP(c->p_img_valid, iv.data(), 8 * 4);
+    UP(c->p_seq_valid, iv.data() + 8, 8 * 4);
   }
-  // ---- per-step parameter block (pageable source: safe to reuse after return)
+  // ---- per-step parameter block (staged in pinned memory: the host copies may be reused at once)
   {
     // per SEQUENCE (CFG: sequence q belongs to request q % B), CFG scale per request
     std::vector<float> pf(8 * 5 + 64, 0.f);
@@ -1814,14 +1894,14 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       pf[24 + q] = b->guidance[i];
     }
     for (int i = 0; i < B && cfgon; ++i) pf[32 + i] = b->cfg_scale[i];
-    cudaMemcpyAsync(c->p_cfg, pf.data() + 32, 8 * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->p_dsig, pf.data(), 8 * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->p_cn_scale, pf.data() + 8, 8 * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->p_sigma, pf.data() + 16, 8 * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->p_guid, pf.data() + 24, 8 * 4, cudaMemcpyHostToDevice, s);
+    UP(c->p_cfg, pf.data() + 32, 8 * 4);
+    UP(c->p_dsig, pf.data(), 8 * 4);
+    UP(c->p_cn_scale, pf.data() + 8, 8 * 4);
+    UP(c->p_sigma, pf.data() + 16, 8 * 4);
+    UP(c->p_guid, pf.data() + 24, 8 * 4);
     std::vector<float> ss(64, 0.f);
     for (size_t i = 0; i < c->slot_scale_h.size() && i < 64; ++i) ss[i] = c->slot_scale_h[i];
-    cudaMemcpyAsync(c->p_slot_scale, ss.data(), 64 * 4, cudaMemcpyHostToDevice, s);
+    UP(c->p_slot_scale, ss.data(), 64 * 4);
     c->cn_flags = false;
     if (!c->cn.empty()) {
       // [block][fan-in k][request] tables of the residuals registered for this step
@@ -1840,11 +1920,11 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
           ex[at] = kv.second[k].expect;
           c->cn_flags |= kv.second[k].flag != nullptr;
         }
-      cudaMemcpyAsync(c->p_cn_ptr, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(c->p_cn_kappa, kap.data(), kap.size() * 4, cudaMemcpyHostToDevice, s);
+      UP(c->p_cn_ptr, cp.data(), cp.size() * sizeof(void*));
+      UP(c->p_cn_kappa, kap.data(), kap.size() * 4);
       if (c->cn_flags) {
-        cudaMemcpyAsync(c->p_cn_flag, fl.data(), fl.size() * sizeof(void*), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(c->p_cn_expect, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice, s);
+        UP(c->p_cn_flag, fl.data(), fl.size() * sizeof(void*));
+        UP(c->p_cn_expect, ex.data(), ex.size() * 4);
       }
     }
   }
@@ -1867,9 +1947,12 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
     sg.push_back({c->g_out.w, c->g_out.b, D, 0});
     sg.push_back({c->y_in.w, c->y_in.b, D, 0});
     sg.push_back({c->y_out.w, c->y_out.b, D, 0});
-    cudaMemcpyAsync(c->segs, sg.data(), sg.size() * sizeof(SkinnySeg), cudaMemcpyHostToDevice, s);
+    if (!UP(c->segs, sg.data(), sg.size() * sizeof(SkinnySeg))) return c->fail(DIT_ENOMEM, "staging block overflow");
     c->segs_dirty = false;
   }
+  if (mode == STEP_RUN) cudaEventRecord(c->pin_ev[(c->pin_next - 1) % dit_ctx::PIN_RING], s);
+  if (capture && c->st_event) record(c->st_event);   // the graph's block may be restaged after this
+  if (stage_only) return DIT_OK;   // dit_graph_launch: the block its graph reads is refreshed
   const int mod_off_single = 12 * D * c->Ld;
   const int mod_off_final = mod_off_single + 3 * D * c->Ls;
 
@@ -2090,7 +2173,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
       if (kv.first.second == blk)
         for (auto& r : kv.second) {
           any = true;
-          if (r.ready) cudaStreamWaitEvent(s, r.ready, 0);
+          if (r.ready) cudaStreamWaitEvent(s, r.ready, wait_fl);
         }
     return any;
   };
@@ -2397,13 +2480,137 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
   }
 
   for (int i = 0; i < S; ++i)
-    if (req_slot[i] >= 0) cudaEventRecord(c->slot_last_use[req_slot[i]], s);
-  if (c->merged_adapter >= 0) cudaEventRecord(c->merged_last_use, s);
-  cudaEventRecord(c->step_done, s);
+    if (req_slot[i] >= 0) record(c->slot_last_use[req_slot[i]]);
+  if (c->merged_adapter >= 0) record(c->merged_last_use);
+  record(c->step_done);
   c->last_launches = c->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return c->fail(DIT_ECUDA, "step: %s", cudaGetErrorString(e));
   return DIT_OK;
+}
+
+// ------------------------------------------------------------------ CUDA graphs
+// One captured dit_step replayed with fresh per-step scalars (sigma, guidance, CFG / ControlNet
+// scales, ControlNet residual pointers): dit_graph_launch re-runs the step's host logic in staging
+// mode into the graph's own pinned block (which the graph's copy nodes read), then launches the
+// graph -- no per-kernel launch cost.
+struct dit_graph {
+  dit_ctx* c = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint8_t* block = nullptr;     // pinned, stage_bytes
+  cudaEvent_t staged = nullptr; // recorded by each replay once its copy nodes have read `block`
+  dit_batch key{};              // captured shape and device pointers
+  std::vector<int> ids, hw;
+  std::vector<std::pair<std::pair<int, int>, std::vector<cudaEvent_t>>> cn_key;   // (slot, block) -> events
+};
+
+namespace {
+std::vector<std::pair<std::pair<int, int>, std::vector<cudaEvent_t>>> cn_signature(const dit_ctx* c, bool* flags) {
+  std::vector<std::pair<std::pair<int, int>, std::vector<cudaEvent_t>>> v;
+  *flags = false;
+  for (auto& kv : c->cn) {
+    std::vector<cudaEvent_t> ev;
+    for (auto& r : kv.second) {
+      ev.push_back(r.ready);
+      *flags |= r.flag != nullptr;
+    }
+    v.push_back({kv.first, ev});
+  }
+  return v;
+}
+bool same_shape(const dit_graph* g, const dit_batch* b) {
+  const dit_batch& k = g->key;
+  if (b->batch != k.batch || b->img_h != k.img_h || b->img_w != k.img_w || b->txt_tokens != k.txt_tokens) return false;
+  if (b->latents_in != k.latents_in || b->latents_out != k.latents_out || b->txt != k.txt || b->pooled != k.pooled ||
+      b->v_out != k.v_out)
+    return false;
+  if ((b->cfg_scale == nullptr) != (k.cfg_scale == nullptr) || (b->img_hw == nullptr) != (k.img_hw == nullptr))
+    return false;
+  for (int i = 0; i < b->batch; ++i)
+    if (!b->adapter_id || b->adapter_id[i] != g->ids[i]) return false;
+  for (size_t i = 0; i < g->hw.size(); ++i)
+    if (b->img_hw[i] != g->hw[i]) return false;
+  return true;
+}
+}  // namespace
+
+extern "C" int dit_graph_create(dit_ctx* c, const dit_batch* b, void* stream, dit_graph** out) {
+  if (!c) return DIT_EINVAL;
+  if (!out || !b) return c->fail(DIT_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (c->local_group || c->lp_group) return c->fail(DIT_EPARALLEL, "in-process groups are not capturable");
+  if ((c->world > 1 && c->sp_fused) || (c->lp_world > 1 && c->lp_fused))
+    return c->fail(DIT_EPARALLEL, "the fused peer exchange's epochs are per launch: not capturable");
+  bool flags = false;
+  auto sig = cn_signature(c, &flags);
+  if (flags) return c->fail(DIT_EINVAL, "device-flag ControlNet inputs are single-use: not capturable");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (s == nullptr) return c->fail(DIT_EINVAL, "capture needs a non-default stream");
+  dit_graph* g = new dit_graph();
+  g->c = c;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&g->block), c->stage_bytes, cudaHostAllocDefault) != cudaSuccess) {
+    delete g;
+    return c->fail(DIT_ECUDA, "cudaHostAlloc of the graph's staging block failed");
+  }
+  g->key = *b;
+  g->ids.assign(b->adapter_id ? b->adapter_id : nullptr, b->adapter_id ? b->adapter_id + b->batch : nullptr);
+  if (b->img_hw) g->hw.assign(b->img_hw, b->img_hw + 2 * b->batch);
+  g->cn_key = sig;
+  cudaEventCreateWithFlags(&g->staged, cudaEventDisableTiming);
+  c->st_base = g->block;
+  c->st_event = g->staged;
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaFreeHost(g->block);
+    delete g;
+    return c->fail(DIT_ECUDA, "cudaStreamBeginCapture failed");
+  }
+  int r = step_impl(c, b, s, STEP_CAPTURE);
+  c->st_event = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  c->plan_B = -1;                        // the device tables now hold the graph's plan
+  c->rope_key[0] = -1;
+  if (r != DIT_OK || e != cudaSuccess ||
+      cudaGraphInstantiate(&g->exec, graph, cudaGraphInstantiateFlagAutoFreeOnLaunch) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaFreeHost(g->block);
+    cudaEventDestroy(g->staged);
+    delete g;
+    cudaGetLastError();
+    return r != DIT_OK ? r : c->fail(DIT_ECUDA, "graph capture / instantiation failed: %s", cudaGetErrorString(e));
+  }
+  cudaGraphDestroy(graph);
+  *out = g;
+  return DIT_OK;
+}
+
+extern "C" int dit_graph_launch(dit_graph* g, const dit_batch* b, void* stream) {
+  if (!g || !g->c) return DIT_EINVAL;
+  dit_ctx* c = g->c;
+  if (!b) return c->fail(DIT_EINVAL, "batch is NULL");
+  if (!same_shape(g, b)) return c->fail(DIT_EINVAL, "batch shape / pointers / adapters differ from the captured step");
+  bool flags = false;
+  if (cn_signature(c, &flags) != g->cn_key || flags)
+    return c->fail(DIT_EINVAL, "ControlNet registrations differ from the captured step (slots, blocks, events)");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // the previous replay's copy nodes may still have to read the block (the host runs <= 1 replay ahead)
+  if (cudaEventSynchronize(g->staged) != cudaSuccess) return c->fail(DIT_ECUDA, "previous replay failed");
+  c->st_base = g->block;
+  const int r = step_impl(c, b, s, STEP_STAGE);
+  if (r != DIT_OK) return r;
+  const cudaError_t e = cudaGraphLaunch(g->exec, s);
+  c->plan_B = -1;                        // device plan tables / rope now the graph's
+  c->rope_key[0] = -1;
+  c->launches = 1;
+  return e == cudaSuccess ? DIT_OK : c->fail(DIT_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+}
+
+extern "C" void dit_graph_destroy(dit_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->block) cudaFreeHost(g->block);
+  if (g->staged) cudaEventDestroy(g->staged);
+  delete g;
 }
 
 // ------------------------------------------------------------------ profiling exports

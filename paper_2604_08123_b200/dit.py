@@ -80,6 +80,9 @@ EXPORTS = {
     "sp_init_peers": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "lp_init_peers": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "dit_step": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
+    "dit_graph_create": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dit_graph_launch": (C.c_int, [C.c_void_p, C.POINTER(dit_batch), C.c_void_p]),
+    "dit_graph_destroy": (None, [C.c_void_p]),
     "dit_step_flops": (C.c_double, [C.c_void_p, C.POINTER(dit_batch)]),
     "dit_last_launch_count": (C.c_int, [C.c_void_p]),
     "dit_sp_exchange": (C.c_int, [C.c_void_p]),
@@ -329,6 +332,18 @@ class DiT:
 
     def dit_step(self, batch: dit_batch, stream=None):
         _check(self.lib.dit_step(self.ctx, C.byref(batch), self._stream(stream)), self.ctx)
+
+    def graph_create(self, batch: dit_batch, stream=None):
+        """Capture one dit_step on `batch` (dit_graph_create); returns the graph handle."""
+        g = C.c_void_p()
+        _check(self.lib.dit_graph_create(self.ctx, C.byref(batch), self._stream(stream), C.byref(g)), self.ctx)
+        return g
+
+    def graph_launch(self, graph, batch: dit_batch, stream=None):
+        _check(self.lib.dit_graph_launch(graph, C.byref(batch), self._stream(stream)), self.ctx)
+
+    def graph_destroy(self, graph):
+        self.lib.dit_graph_destroy(graph)
 
     def step_flops(self, batch: dit_batch) -> float:
         return float(self.lib.dit_step_flops(self.ctx, C.byref(batch)))
