@@ -27,7 +27,7 @@
 //               (setmaxnreg: 208 registers for the softmax warpgroups, 80 for
 //               warpgroup 2).  Row max, lazy O rescale (only when the running
 //               max grows by > 8 in log2 units), packed f32x2 FFMA, exp2 with
-//               1/ATTN_POLY_MOD of the pairs on a degree-3 polynomial (FMA pipe)
+//               1/ATTN_POLY_MOD (1/8) of the pairs on a degree-3 polynomial (FMA pipe)
 //               and the rest on MUFU, P packed to bf16 and stored with
 //               tcgen05.st in 16-column chunks; the row sum is accumulated after
 //               P is released (off the MMA's critical path); final O / l
@@ -64,7 +64,7 @@ static_assert(2 * 128 * ATTN_REG_SOFTMAX + 128 * ATTN_REG_OTHER <= THREADS * 168
 #define ATTN_FAKE 0
 #endif
 #ifndef ATTN_POLY_MOD
-#define ATTN_POLY_MOD 4
+#define ATTN_POLY_MOD 8
 #endif
 #ifndef ATTN_POLY_RES
 #define ATTN_POLY_RES 1
@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
             tc_fence_before();
             __syncwarp();
             if (tr) TRACE(8 + t, j);
+            if (trace != nullptr && it == 0 && lane == 0 && t == 0 && wq > 0) TRACE(16 + wq, j);   // arrive skew
             if (lane == 0) mbar_arrive(&p_full[t]);
           }
         }

@@ -54,3 +54,4 @@ if os.environ.get("TRACE"):
           " P arrive->MMA sees it", d(8, 3), " MMA issues PV0 -> next S0 wake", d(3, 6, 1), " period", d(6, 6, 1))
     print("MMA thread: k_full wait", d(14, 2), " p_full0 wait", d(15, 3), " p_full1 wait", d(16, 4),
           " PV0 issue start -> QK0 k_full wait start", d(5, 14, 1), " QK0 issued -> PV1 wait start", d(2, 16))
+    print("tile0 P-arrive skew vs warp 0 (warps 1,2,3):", d(8, 17), d(8, 18), d(8, 19), " S wake of warp0 -> MMA sees P0", d(6, 3))
