@@ -1,8 +1,7 @@
 cd $GRAFT_REPO_ROOT
 V=paper_2604_08123_b200/build/variants
 for rep in 1 2; do
-for n in base pm8 s2pm8 s2pm4 s1pm8; do
-  lib=$V/libdit_$n.so; [ $n = base ] && lib=
-  echo "== $n $(DIT_LIB_OVERRIDE=$lib timeout 120 python tools/attn_bench.py 8 24 4608 128 | tail -1)"
+for n in old new; do
+  lib=$V/libdit_oldgemm.so; [ $n = new ] && lib=
+  echo "== $n"; DIT_LIB_OVERRIDE=$lib timeout 200 python tools/resid_bench.py 2>&1 | head -3
 done; done
-for n in s2pm8; do DIT_LIB_OVERRIDE=$V/libdit_$n.so TRACE=1 python tools/attn_bench.py | tail -3; done
