@@ -494,6 +494,25 @@ DEVI void prefetch_epilogue_rows(const GemmProblem& P, const TileInfo& ti, int r
   }
 }
 
+#ifndef GEMM_TRACE
+#define GEMM_TRACE 0
+#endif
+#if GEMM_TRACE
+// timing experiment (variant builds only, tools/gemm_trace.py): clock64 stamps of CTA 0 per
+// tile -- 0 epilogue start, 1 / 2 epilogue end (warp 0 / 7), 3 / 4 MMA warp before / after the
+// accumulator-free wait, 5 last MMA of the tile issued
+__device__ long long* g_gemm_trace = nullptr;
+extern "C" int dit_debug_gemm_trace(long long* buf) {
+  return cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 1;
+}
+#define GTRACE(ev, it)                                                                            \
+  do {                                                                                            \
+    if (blockIdx.x == 0 && g_gemm_trace != nullptr && (it) < 64) g_gemm_trace[(ev) * 64 + (it)] = clock64(); \
+  } while (0)
+#else
+#define GTRACE(ev, it) do {} while (0)
+#endif
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -595,7 +614,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int nk_total = __shfl_sync(0xffffffffu, ti.nk_total, 0);
         const int acc = iter & 1;
         const uint32_t acc_phase = (iter >> 1) & 1;
+        if (lane == 0) GTRACE(3, iter);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (lane == 0) GTRACE(4, iter);
         tc_fence_after();
         const uint32_t d_tmem = __shfl_sync(0xffffffffu, tmem_base, 0) + acc * GEMM_BN;
         for (int kb = 0; kb < nk_total; ++kb) {
@@ -610,6 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
+        if (lane == 0) GTRACE(5, iter);
         commit_2sm_mc_warp(&tfull[acc]);
       }
     }
@@ -624,9 +646,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (iter >> 1) & 1;
       prefetch_epilogue_rows(args.p[ti.p], ti, row_in_tile, half * (GEMM_BN / 2));
       mbar_wait(&tfull[acc], acc_phase);
+      if (warp == 0 && lane == 0) GTRACE(0, iter);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * GEMM_BN;
       epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile, half * (GEMM_BN / 2));
+      if (lane == 0 && (warp == 0 || warp == 7)) GTRACE(warp == 0 ? 1 : 2, iter);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT
 V=paper_2604_08123_b200/build/variants
-for rep in 1 2; do
-for n in old new; do
-  lib=$V/libdit_oldgemm.so; [ $n = new ] && lib=
+for n in gtrace gtrace_coal; do echo "== $n"; DIT_LIB_OVERRIDE=$V/libdit_$n.so python tools/gemm_trace.py | grep -A2 "^resid\|^bias" ; done
+for rep in 1 2; do for n in base coal; do
+  lib=$V/libdit_$n.so; [ $n = base ] && lib=
   echo "== $n"; DIT_LIB_OVERRIDE=$lib timeout 200 python tools/resid_bench.py 2>&1 | head -3
 done; done
