@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 
 }  // namespace attn_tc
 
+
 cudaError_t attention_set_trace(long long* buf) {
   return cudaMemcpyToSymbol(attn_tc::g_attn_trace, &buf, sizeof(buf));
 }

@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
-V=paper_2604_08123_b200/build/variants
-for n in gtrace gtrace_coal; do echo "== $n"; DIT_LIB_OVERRIDE=$V/libdit_$n.so python tools/gemm_trace.py | grep -A2 "^resid\|^bias" ; done
-for rep in 1 2; do for n in base coal; do
-  lib=$V/libdit_$n.so; [ $n = base ] && lib=
-  echo "== $n"; DIT_LIB_OVERRIDE=$lib timeout 200 python tools/resid_bench.py 2>&1 | head -3
+DIT_ATTN_KERNEL=hr timeout 300 python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "attention or head_dim or ragged or tiny" 2>&1 | tail -3
+for rep in 1 2; do for k in v8 hr; do
+  echo "== $k $(DIT_ATTN_KERNEL=$k timeout 120 python tools/attn_bench.py 8 24 4608 128 | tail -1)"
+  echo "== $k $(DIT_ATTN_KERNEL=$k timeout 120 python tools/attn_bench.py 8 24 4429 64 | tail -1)"
 done; done
