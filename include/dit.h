@@ -65,7 +65,7 @@ typedef struct dit_config {
   int32_t rope_axes[3];    /* RoPE dims per position axis, sum = d (16, 56, 56)    */
   float rope_theta;        /* 10000                                                */
   int32_t guidance_embed;  /* 1 = guidance MLP present (Flux-Dev)                  */
-  int32_t max_batch;       /* B_max requests per dit_step         */
+  int32_t max_batch;       /* B_max sequences per dit_step, <= 16 */
   int32_t max_img_tokens;  /* largest Ni (global, before sharding)                */
   int32_t max_txt_tokens;  /* largest Nt (global, before sharding)                */
   int32_t max_rank;        /* largest LoRA rank (<= 128)                          */
@@ -85,6 +85,11 @@ typedef struct dit_config {
   int32_t qk_norm;
   int32_t pos_embed_max;   /* 192 for SD3 / SD3.5                                 */
   int32_t pos_embed_base;  /* 64 for SD3 / SD3.5                                  */
+  /* Largest sequence-parallel world the workspace is sized for: 0 = the default (8,
+   * with the all-to-all send / recv buffers, 16 B_max N D bytes), 1 = single GPU (no
+   * exchange buffers: 1.8 GB less at Flux 1024^2 with B_max 8; sp_init with world > 1,
+   * sp_init_local and sp_init_peers then fail with DIT_EPARALLEL), 2..64 = that cap. */
+  int32_t max_sp_world;
 } dit_config;
 
 enum { DIT_ARCH_FLUX = 0, DIT_ARCH_SD3 = 1 };

@@ -240,14 +240,14 @@ struct dit_ctx {
   float* p_cn_scale = nullptr;
   float* p_sigma = nullptr;
   float* p_guid = nullptr;
-  float* p_cfg = nullptr;            // [8] CFG scale per request
-  const void** p_cn_ptr = nullptr;   // [Ld + Ls][CN_FANIN][8]
+  float* p_cfg = nullptr;            // [MAX_SEQ] CFG scale per request
+  const void** p_cn_ptr = nullptr;   // [Ld + Ls][CN_FANIN][MAX_SEQ]
   float* p_slot_scale = nullptr;     // [max_adapters]
-  float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][8] cn_scale_b * inject scale
+  float* p_cn_kappa = nullptr;       // [Ld + Ls][CN_FANIN][MAX_SEQ] cn_scale_b * inject scale
   const uint32_t** p_cn_flag = nullptr;   // [Ld + Ls][CN_FANIN][8] device ready flags (controlnet_inject_flag)
-  uint32_t* p_cn_expect = nullptr;        // [Ld + Ls][CN_FANIN][8]
-  int* p_img_valid = nullptr;             // [8] ragged batch: image rows of each sequence
-  int* p_seq_valid = nullptr;             // [8] ragged batch: joint rows of each sequence
+  uint32_t* p_cn_expect = nullptr;        // [Ld + Ls][CN_FANIN][MAX_SEQ]
+  int* p_img_valid = nullptr;             // [MAX_SEQ] ragged batch: image rows of each sequence
+  int* p_seq_valid = nullptr;             // [MAX_SEQ] ragged batch: joint rows of each sequence
   std::vector<int> plan_hw;               // ragged grids the rope tables were built for
   bool cn_flags = false;                  // any flag registration in the current step
   RowSpace rs[3];                    // 0 txt stream, 1 img stream, 2 joint
@@ -323,10 +323,11 @@ bool cfg_valid(const dit_config* c, std::string* why) {
   if (c->txt_dim <= 0 || c->txt_dim % 8) return bad("txt_dim must be a positive multiple of 8");
   if (c->pooled_dim <= 0 || c->pooled_dim % 8) return bad("pooled_dim must be a positive multiple of 8");
   if (c->mlp_ratio <= 0) return bad("mlp_ratio must be positive");
-  if (c->max_batch < 1 || c->max_batch > 8) return bad("max_batch must be in [1, 8]");
+  if (c->max_batch < 1 || c->max_batch > MAX_SEQ) return bad("max_batch must be in [1, 16]");
   if (c->max_img_tokens < 1 || c->max_txt_tokens < 1) return bad("token maxima must be positive");
   if (c->max_rank < 0 || c->max_rank > 128) return bad("max_rank must be in [0, 128]");
   if (c->max_adapters < 0 || c->max_adapters > 64) return bad("max_adapters must be in [0, 64]");
+  if (c->max_sp_world < 0 || c->max_sp_world > 64) return bad("max_sp_world must be in [0, 64]");
   return true;
 }
 
@@ -349,7 +350,9 @@ Layout layout_of(const dit_config& c) {
   L.h = cv.take(R * D * 4);
   L.u = cv.take(R * D * 2);
   L.qkv = cv.take(3 * R * D * 2);
-  L.sp = cv.take(8 * R * D * 2);   // SP send/recv buffers: 8 B*N_loc*D*P elements at any P (incl. the forced P=1 test path)
+  // SP all-to-all send / recv buffers (8 B*N_loc*D*P elements at any P, incl. the forced P = 1
+  // test path); a single-GPU workspace (max_sp_world = 1) keeps only a 64 KB scratch
+  L.sp = cv.take(c.max_sp_world == 1 ? (size_t)65536 : 8 * R * D * 2);
   L.o = cv.take(R * D * 2);
   L.cat = cv.take(R * (D + F) * 2);
   L.sext = cv.take(R * (size_t)std::max(c.max_adapters, 1) * std::max<size_t>(r_alloc, 64) * 2);
@@ -358,14 +361,14 @@ Layout layout_of(const dit_config& c) {
   L.vcfg = cv.take(4 * (size_t)c.max_batch * c.max_img_tokens * c.in_channels * 4);
   L.mjobs = cv.take((size_t)n_lora_modules(c) * merge_job_bytes() + 256);   // lora_merge job table + counter
   L.rope = cv.take((size_t)c.max_batch * N * (d / 2) * 8);   // one table per sequence for ragged batches
-  L.mod = cv.take(8 * mod_total * 4);
-  L.vec = cv.take(8 * D * 4);
-  L.h1 = cv.take(8 * D * 4);
-  L.xprep = cv.take(8 * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
-  L.temb = cv.take(8 * 256 * 2);
+  L.mod = cv.take(MAX_SEQ * mod_total * 4);
+  L.vec = cv.take(MAX_SEQ * D * 4);
+  L.h1 = cv.take(MAX_SEQ * D * 4);
+  L.xprep = cv.take(MAX_SEQ * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
+  L.temb = cv.take(MAX_SEQ * 256 * 2);
   L.segs = cv.take((nseg + 6) * sizeof(SkinnySeg));
-  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8 * 2 * (sizeof(void*) + 4) + 2048);
-  L.rowspace = cv.take(3 * (R * 4 + tiles * 8 * 4 + tiles * 4 + tiles * 8 * 8) + 3 * 1024);
+  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * MAX_SEQ * 2 * (sizeof(void*) + 4) + 2048);
+  L.rowspace = cv.take(3 * (R * 4 + tiles * MAX_SEQ * 4 + tiles * 4 + tiles * MAX_SEQ * 8) + 3 * 1024);
   size_t per_slot = 0;
   if (c.max_adapters > 0 && r_alloc > 0) {
     auto add = [&](size_t in, size_t out) { per_slot += r_alloc * in * 2 + out * r_alloc * 2; };
@@ -386,9 +389,9 @@ size_t stage_bytes_of(const dit_config& c) {
   const size_t N = (size_t)c.max_img_tokens + c.max_txt_tokens;
   const size_t R = (size_t)c.max_batch * N;
   const size_t tiles = (R + GEMM_TM - 1) / GEMM_TM + 4;
-  const size_t ncn = (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * 8;
+  const size_t ncn = (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * MAX_SEQ;
   const size_t nseg = 2 * c.depth_double + c.depth_single + 1 + 6;
-  return 3 * (R * 4 + tiles * c.max_batch * 4 + tiles * 4 + tiles * 8 * 8 + 64) + 8 * 64 + 64 * 4 + 16 * 4 +
+  return 3 * (R * 4 + tiles * c.max_batch * 4 + tiles * 4 + tiles * MAX_SEQ * 8 + 64) + MAX_SEQ * 64 + 64 * 4 + 16 * 4 +
          ncn * (2 * sizeof(void*) + 8) + 64 + nseg * sizeof(SkinnySeg) + 4096;
 }
 }  // namespace
@@ -455,19 +458,19 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   {
     Carve cv;
     uint8_t* p = w + L.params;
-    c->p_dsig = reinterpret_cast<float*>(p + cv.take(8 * 4));
-    c->p_cn_scale = reinterpret_cast<float*>(p + cv.take(8 * 4));
-    c->p_sigma = reinterpret_cast<float*>(p + cv.take(8 * 4));
-    c->p_guid = reinterpret_cast<float*>(p + cv.take(8 * 4));
-    c->p_cfg = reinterpret_cast<float*>(p + cv.take(8 * 4));
+    c->p_dsig = reinterpret_cast<float*>(p + cv.take(MAX_SEQ * 4));
+    c->p_cn_scale = reinterpret_cast<float*>(p + cv.take(MAX_SEQ * 4));
+    c->p_sigma = reinterpret_cast<float*>(p + cv.take(MAX_SEQ * 4));
+    c->p_guid = reinterpret_cast<float*>(p + cv.take(MAX_SEQ * 4));
+    c->p_cfg = reinterpret_cast<float*>(p + cv.take(MAX_SEQ * 4));
     c->p_slot_scale = reinterpret_cast<float*>(p + cv.take(64 * 4));
-    const size_t ncn = (size_t)std::max(c->Ld + c->Ls, 1) * CN_FANIN * 8;
+    const size_t ncn = (size_t)std::max(c->Ld + c->Ls, 1) * CN_FANIN * MAX_SEQ;
     c->p_cn_ptr = reinterpret_cast<const void**>(p + cv.take(ncn * sizeof(void*)));
     c->p_cn_kappa = reinterpret_cast<float*>(p + cv.take(ncn * 4));
     c->p_cn_flag = reinterpret_cast<const uint32_t**>(p + cv.take(ncn * sizeof(void*)));
     c->p_cn_expect = reinterpret_cast<uint32_t*>(p + cv.take(ncn * 4));
-    c->p_img_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
-    c->p_seq_valid = reinterpret_cast<int*>(p + cv.take(8 * 4));
+    c->p_img_valid = reinterpret_cast<int*>(p + cv.take(MAX_SEQ * 4));
+    c->p_seq_valid = reinterpret_cast<int*>(p + cv.take(MAX_SEQ * 4));
     c->flags = reinterpret_cast<uint32_t*>(p + cv.take(8 * 4));
   }
   {
@@ -476,9 +479,9 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     uint8_t* p = w + L.rowspace;
     for (int s = 0; s < 3; ++s) {
       c->rs[s].row_slot = reinterpret_cast<int*>(p + cv.take(c->Rmax * 4));
-      c->rs[s].tile_slots = reinterpret_cast<int*>(p + cv.take(tiles * 8 * 4));
+      c->rs[s].tile_slots = reinterpret_cast<int*>(p + cv.take(tiles * MAX_SEQ * 4));
       c->rs[s].tile_cnt = reinterpret_cast<int*>(p + cv.take(tiles * 4));
-      c->rs[s].shrink_list = reinterpret_cast<int2*>(p + cv.take(tiles * 8 * 8));
+      c->rs[s].shrink_list = reinterpret_cast<int2*>(p + cv.take(tiles * MAX_SEQ * 8));
     }
   }
   c->slot_cap = cfg->max_batch;
@@ -1068,6 +1071,15 @@ extern "C" int dit_debug_delayed_publish(void* dst, const void* src, size_t byte
 }
 
 // ------------------------------------------------------------------ SP
+// the workspace's SP capacity (dit_config.max_sp_world): 1 = no exchange buffers, n > 1 = at most n ranks
+static int sp_world_ok(dit_ctx* c, int world) {
+  const int cap = c->cfg.max_sp_world;
+  if (cap == 1 && world > 1)
+    return c->fail(DIT_EPARALLEL, "workspace sized for one GPU (max_sp_world = 1): no sequence parallelism");
+  if (cap > 1 && world > cap) return c->fail(DIT_EPARALLEL, "world %d > max_sp_world %d", world, cap);
+  return DIT_OK;
+}
+
 extern "C" void* dit_local_group_create(int32_t world) {
   if (world < 1 || world > 64) return nullptr;
   LocalGroup* g = new LocalGroup();
@@ -1099,6 +1111,7 @@ extern "C" int sp_init_local(dit_ctx* c, void* grp, int32_t rank) {
   if (!c) return DIT_EINVAL;
   LocalGroup* g = static_cast<LocalGroup*>(grp);
   if (!g || rank < 0 || rank >= g->world) return c->fail(DIT_EINVAL, "bad local group / rank");
+  if (int e = sp_world_ok(c, g->world)) return e;
   if (c->H % g->world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", g->world, c->H);
   if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   const char* nccl_path = getenv("DIT_SP_NCCL");
@@ -1242,6 +1255,9 @@ static void setup_fused_peers(dit_ctx* c) {
 extern "C" int sp_init(dit_ctx* c, int32_t world, int32_t rank, const void* uid) {
   if (!c) return DIT_EINVAL;
   if (world < 1 || rank < 0 || rank >= world) return c->fail(DIT_EINVAL, "bad world/rank %d/%d", world, rank);
+  if (int e = sp_world_ok(c, world)) return e;
+  if (world == 1 && c->cfg.max_sp_world == 1 && getenv("DIT_FORCE_SP") && uid != nullptr)
+    return c->fail(DIT_EPARALLEL, "DIT_FORCE_SP needs the SP buffers (max_sp_world != 1)");
   if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
   if (c->lp_world > 1 && world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   // DIT_FORCE_SP=1 (test-only): a 1-rank NCCL communicator drives the full
@@ -1280,6 +1296,7 @@ extern "C" int sp_init_peers(dit_ctx* c, int32_t world, int32_t rank, const void
   if (world < 2 || world > 8 || rank < 0 || rank >= world)
     return c->fail(DIT_EINVAL, "sp_init_peers: world must be in [2, 8] and rank in [0, world), got %d/%d", world, rank);
   if (!handles) return c->fail(DIT_EINVAL, "handles is NULL");
+  if (int e = sp_world_ok(c, world)) return e;
   if (c->H % world) return c->fail(DIT_EPARALLEL, "world %d does not divide heads %d", world, c->H);
   if (c->lp_world > 1) return c->fail(DIT_EPARALLEL, "latent parallelism is active (lp_init)");
   if (cudaSetDevice(c->device) != cudaSuccess) return c->fail(DIT_ECUDA, "cudaSetDevice");
@@ -1874,38 +1891,39 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     c->plan_hw = hw_key;
   }
   if (ragged) {
-    std::vector<int> iv(16, 0);
+    std::vector<int> iv(2 * MAX_SEQ, 0);
     for (int q = 0; q < S; ++q) {
       iv[q] = img_valid[q];
-      iv[8 + q] = seq_valid[q];
+      iv[MAX_SEQ + q] = seq_valid[q];
     }
-    UP(c->p_img_valid, iv.data(), 8 * 4);
-    UP(c->p_seq_valid, iv.data() + 8, 8 * 4);
+    UP(c->p_img_valid, iv.data(), MAX_SEQ * 4);
+    UP(c->p_seq_valid, iv.data() + MAX_SEQ, MAX_SEQ * 4);
   }
   // ---- per-step parameter block (staged in pinned memory: the host copies may be reused at once)
   {
     // per SEQUENCE (CFG: sequence q belongs to request q % B), CFG scale per request
-    std::vector<float> pf(8 * 5 + 64, 0.f);
+    constexpr int M = MAX_SEQ;
+    std::vector<float> pf(M * 5 + 64, 0.f);
     for (int q = 0; q < S; ++q) {
       const int i = q % B;
       pf[q] = b->sigma_next[i] - b->sigma[i];
-      pf[8 + q] = b->cn_scale ? b->cn_scale[i] : 1.f;
-      pf[16 + q] = b->sigma[i];
-      pf[24 + q] = b->guidance[i];
+      pf[M + q] = b->cn_scale ? b->cn_scale[i] : 1.f;
+      pf[2 * M + q] = b->sigma[i];
+      pf[3 * M + q] = b->guidance[i];
     }
-    for (int i = 0; i < B && cfgon; ++i) pf[32 + i] = b->cfg_scale[i];
-    UP(c->p_cfg, pf.data() + 32, 8 * 4);
-    UP(c->p_dsig, pf.data(), 8 * 4);
-    UP(c->p_cn_scale, pf.data() + 8, 8 * 4);
-    UP(c->p_sigma, pf.data() + 16, 8 * 4);
-    UP(c->p_guid, pf.data() + 24, 8 * 4);
+    for (int i = 0; i < B && cfgon; ++i) pf[4 * M + i] = b->cfg_scale[i];
+    UP(c->p_cfg, pf.data() + 4 * M, M * 4);
+    UP(c->p_dsig, pf.data(), M * 4);
+    UP(c->p_cn_scale, pf.data() + M, M * 4);
+    UP(c->p_sigma, pf.data() + 2 * M, M * 4);
+    UP(c->p_guid, pf.data() + 3 * M, M * 4);
     std::vector<float> ss(64, 0.f);
     for (size_t i = 0; i < c->slot_scale_h.size() && i < 64; ++i) ss[i] = c->slot_scale_h[i];
     UP(c->p_slot_scale, ss.data(), 64 * 4);
     c->cn_flags = false;
     if (!c->cn.empty()) {
       // [block][fan-in k][request] tables of the residuals registered for this step
-      const size_t ncn = (size_t)(c->Ld + c->Ls) * CN_FANIN * 8;
+      const size_t ncn = (size_t)(c->Ld + c->Ls) * CN_FANIN * MAX_SEQ;
       std::vector<const void*> cp(ncn, nullptr);
       std::vector<float> kap(ncn, 0.f);
       std::vector<const uint32_t*> fl(ncn, nullptr);
@@ -1913,7 +1931,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
       c->cn_flags = false;
       for (auto& kv : c->cn)
         for (size_t k = 0; k < kv.second.size(); ++k) {
-          const size_t at = ((size_t)kv.first.second * CN_FANIN + k) * 8 + kv.first.first;
+          const size_t at = ((size_t)kv.first.second * CN_FANIN + k) * MAX_SEQ + kv.first.first;
           cp[at] = kv.second[k].ptr;
           kap[at] = kv.second[k].scale * (b->cn_scale ? b->cn_scale[kv.first.first % B] : 1.f);
           fl[at] = kv.second[k].flag;
@@ -1968,7 +1986,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     CKC(prep_x_launch(c->h1, S, D, 1, c->xprep, s));
     CKC(skinny_launch(c->xprep, D, cs + 3, 1, D, c->vec, D, S, 1, s));
   }
-  cudaMemsetAsync(c->xprep, 0, (size_t)8 * c->Cp * 2, s);
+  cudaMemsetAsync(c->xprep, 0, (size_t)MAX_SEQ * c->Cp * 2, s);
   cudaMemcpyAsync(c->xprep, b->pooled, (size_t)S * c->Cp * 2, cudaMemcpyDeviceToDevice, s);
   CKC(skinny_launch(c->xprep, c->Cp, cs + 4, 1, D, c->h1, D, S, 0, s));
   CKC(prep_x_launch(c->h1, S, D, 1, c->xprep, s));
@@ -2255,12 +2273,12 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
       eI.gate_off = mI + goff;
       if (cn_ptr) {
         eI.cn_ptr = cn_ptr;
-        eI.cn_scale = c->p_cn_kappa + (size_t)i * CN_FANIN * 8;
+        eI.cn_scale = c->p_cn_kappa + (size_t)i * CN_FANIN * MAX_SEQ;
         eI.cn_row0 = 0;   // the img-stream problem's rows are exactly the residual's rows
         eI.img_valid = ragged ? c->p_img_valid : nullptr;
         if (c->cn_flags) {
-          eI.cn_flag = c->p_cn_flag + (size_t)i * CN_FANIN * 8;
-          eI.cn_expect = c->p_cn_expect + (size_t)i * CN_FANIN * 8;
+          eI.cn_flag = c->p_cn_flag + (size_t)i * CN_FANIN * MAX_SEQ;
+          eI.cn_expect = c->p_cn_expect + (size_t)i * CN_FANIN * MAX_SEQ;
         }
       }
       GemmProblem p[2] = {base_problem(c, AT, Mt, K, lda, LT, eT), base_problem(c, AI, Mi, K, lda, LI, eI)};
@@ -2305,7 +2323,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     const bool has_cn = cn_wait(i);
     CK(shrink2(aT, aI, F, F, T.lora[3], I.lora[3], !po));
     CK(resid_pair(T.fc2, I.fc2, aT, aI, F, F, 5 * D, T.lora[3], I.lora[3],
-                  has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * CN_FANIN * 8) : nullptr));
+                  has_cn ? (const void* const*)(c->p_cn_ptr + (size_t)i * CN_FANIN * MAX_SEQ) : nullptr));
   }
 
   // ---- single-stream blocks on the joint sequence
@@ -2394,13 +2412,13 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
       e.mod_stride = c->mod_total;
       e.gate_off = mj + 2 * D;
       if (cn_wait(c->Ld + j)) {   // single-block ControlNet residual on the image rows (reading C20)
-        e.cn_ptr = (const void* const*)(c->p_cn_ptr + (size_t)(c->Ld + j) * CN_FANIN * 8);
-        e.cn_scale = c->p_cn_kappa + (size_t)(c->Ld + j) * CN_FANIN * 8;
+        e.cn_ptr = (const void* const*)(c->p_cn_ptr + (size_t)(c->Ld + j) * CN_FANIN * MAX_SEQ);
+        e.cn_scale = c->p_cn_kappa + (size_t)(c->Ld + j) * CN_FANIN * MAX_SEQ;
         e.cn_row0 = nt;           // joint rows are [txt; img] per request
         e.img_valid = ragged ? c->p_img_valid : nullptr;
         if (c->cn_flags) {
-          e.cn_flag = c->p_cn_flag + (size_t)(c->Ld + j) * CN_FANIN * 8;
-          e.cn_expect = c->p_cn_expect + (size_t)(c->Ld + j) * CN_FANIN * 8;
+          e.cn_flag = c->p_cn_flag + (size_t)(c->Ld + j) * CN_FANIN * MAX_SEQ;
+          e.cn_expect = c->p_cn_expect + (size_t)(c->Ld + j) * CN_FANIN * MAX_SEQ;
         }
       }
       GemmProblem p = base_problem(c, c->cat, Mj, D + F, D + F, SB.l2, e);

@@ -2,7 +2,7 @@
 //   * LN-modulate: u = (1 + scale_b) * LN(h) + shift_b, fp32 in, bf16 out,
 //     one warp per row, float4 loads, two-pass mean/variance in registers;
 //   * skinny GEMM for the conditioning MLPs and ALL adaLN modulations in one
-//     launch: out[b][n] = x[b] . W[n] + bias[n] for b < 8 on mma.sync with the
+//     launch: out[b][n] = x[b] . W[n] + bias[n] for b < B <= 16 on mma.sync with the
 //     weight rows streamed straight from HBM (16-byte loads, K permuted
 //     consistently between the A (weights) and B (x) fragments);
 //   * small helpers: sinusoid embedding, RoPE table, casts, synthetic fill.
@@ -419,7 +419,7 @@ cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void
 }
 
 // ------------------------------------------------------------------ skinny GEMM
-// One warp computes 16 output rows n (all 8 batch columns) over the full K.
+// One warp computes 16 output rows n (all batch columns: one n8 group, two when B > 8) over the full K.
 // Per 32-wide K chunk, thread (gid, tig) loads 16 B of W row gid and row gid+8
 // at k = base + 8*tig and 16 B of x row gid at the same k; two m16n8k16 MMAs
 // consume them with logical k slots {2tig,2tig+1,2tig+8,2tig+9} mapped to
@@ -442,8 +442,11 @@ __global__ void __launch_bounds__(256) skinny_kernel(const bf16* __restrict__ x,
   const bf16* w0 = reinterpret_cast<const bf16*>(sg.w) + (size_t)min(srow + gid, sg.rows - 1) * K;
   const bf16* w1 = reinterpret_cast<const bf16*>(sg.w) + (size_t)min(srow + gid + 8, sg.rows - 1) * K;
   const bf16* xr = x + (size_t)gid * K;
+  const bf16* xr2 = x + (size_t)(gid + 8) * K;   // batch columns 8..15 (B > 8)
   float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc2[4] = {0.f, 0.f, 0.f, 0.f}, acc3[4] = {0.f, 0.f, 0.f, 0.f};
   const int Kpad = (K + 31) & ~31;
+  const bool two = B > 8;   // (uniform) second n8 group of batch columns; the weights are read once
 #pragma unroll 4
   for (int k = 8 * tig; k < Kpad; k += 32) {
     const bool ok = k < K;
@@ -457,15 +460,22 @@ __global__ void __launch_bounds__(256) skinny_kernel(const bf16* __restrict__ x,
     uint32_t fa2[4] = {a0.z, a1.z, a0.w, a1.w};
     uint32_t fb2[2] = {xv.z, xv.w};
     mma_bf16_16816(acc1, fa2, fb2);
+    if (two) {
+      const uint4 xw = ok ? __ldg(reinterpret_cast<const uint4*>(xr2 + k)) : z;
+      uint32_t fb3[2] = {xw.x, xw.y};
+      mma_bf16_16816(acc2, fa, fb3);
+      uint32_t fb4[2] = {xw.z, xw.w};
+      mma_bf16_16816(acc3, fa2, fb4);
+    }
   }
   // C fragment: c0,c1 = (row gid, batch 2tig, 2tig+1), c2,c3 = (row gid+8, ...)
   const bf16* bias = reinterpret_cast<const bf16*>(sg.bias);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int rr = srow + gid + (e >= 2 ? 8 : 0);
-    const int bb = 2 * tig + (e & 1);
+  for (int e = 0; e < 8; ++e) {
+    const int rr = srow + gid + ((e & 3) >= 2 ? 8 : 0);
+    const int bb = 2 * tig + (e & 1) + (e >= 4 ? 8 : 0);
     if (rr < sg.rows && bb < B) {
-      float v = acc0[e] + acc1[e] + __bfloat162float(bias[rr]);
+      float v = (e < 4 ? acc0[e & 3] + acc1[e & 3] : acc2[e & 3] + acc3[e & 3]) + __bfloat162float(bias[rr]);
       float* o = out + (size_t)bb * out_stride + sg.out_off + rr;
       if (accumulate) v += *o;
       *o = v;
@@ -486,7 +496,7 @@ cudaError_t skinny_launch(const void* x, int K, const SkinnySeg* segs_dev, int n
 // ------------------------------------------------------------------ small helpers
 __global__ void prep_x_kernel(const float* x, int B, int K, int silu, bf16* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 8 * K) return;
+  if (i >= MAX_SEQ * K) return;
   const int b = i / K;
   float v = 0.f;
   if (b < B) {
@@ -496,14 +506,14 @@ __global__ void prep_x_kernel(const float* x, int B, int K, int silu, bf16* out)
   out[i] = __float2bfloat16_rn(v);
 }
 cudaError_t prep_x_launch(const float* x, int B, int K, int silu, void* out, cudaStream_t s) {
-  prep_x_kernel<<<(8 * K + 255) / 256, 256, 0, s>>>(x, B, K, silu, reinterpret_cast<bf16*>(out));
+  prep_x_kernel<<<(MAX_SEQ * K + 255) / 256, 256, 0, s>>>(x, B, K, silu, reinterpret_cast<bf16*>(out));
   return cudaGetLastError();
 }
 
 // e(t) = [cos(1000 t w_k), sin(1000 t w_k)], w_k = 10000^(-k/128), k < 128 (fp64 args).
 __global__ void temb_kernel(const float* vals, int B, bf16* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 8 * 256) return;
+  if (i >= MAX_SEQ * 256) return;
   const int b = i / 256, j = i % 256;
   double v = 0.0;
   if (b < B) {
@@ -515,7 +525,7 @@ __global__ void temb_kernel(const float* vals, int B, bf16* out) {
   out[i] = __float2bfloat16_rn((float)v);
 }
 cudaError_t temb_launch(const float* vals, int B, void* out, cudaStream_t s) {
-  temb_kernel<<<8, 256, 0, s>>>(vals, B, reinterpret_cast<bf16*>(out));
+  temb_kernel<<<MAX_SEQ, 256, 0, s>>>(vals, B, reinterpret_cast<bf16*>(out));
   return cudaGetLastError();
 }
 

@@ -414,12 +414,12 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           (E.img_valid == nullptr || nloc - E.cn_row0 < E.img_valid[b])) {   // (ragged: residual has Ni_b rows)
         const size_t roff = (size_t)(nloc - E.cn_row0) * E.D + col;
         cn0 = reinterpret_cast<const bf16*>(E.cn_ptr[b]);
-        cn1 = reinterpret_cast<const bf16*>(E.cn_ptr[8 + b]);
+        cn1 = reinterpret_cast<const bf16*>(E.cn_ptr[MAX_SEQ + b]);
         if (cn0 != nullptr) { kap0 = E.cn_scale[b]; cn0 += roff; }
-        if (cn1 != nullptr) { kap1 = E.cn_scale[8 + b]; cn1 += roff; }
+        if (cn1 != nullptr) { kap1 = E.cn_scale[MAX_SEQ + b]; cn1 += roff; }
         if (E.cn_flag != nullptr) {   // deferred fetch with device flags
           cn_acquire(E.cn_flag[b], E.cn_expect[b]);
-          cn_acquire(E.cn_flag[8 + b], E.cn_expect[8 + b]);
+          cn_acquire(E.cn_flag[MAX_SEQ + b], E.cn_expect[MAX_SEQ + b]);
         }
       }
       if (valid == 32) {
@@ -484,7 +484,7 @@ DEVI void prefetch_epilogue_rows(const GemmProblem& P, const TileInfo& ti, int r
   if (E.cn_ptr != nullptr && nloc >= E.cn_row0 && (E.img_valid == nullptr || nloc - E.cn_row0 < E.img_valid[b])) {
 #pragma unroll
     for (int k = 0; k < CN_FANIN; ++k) {
-      const bf16* cn = reinterpret_cast<const bf16*>(E.cn_ptr[8 * k + b]);
+      const bf16* cn = reinterpret_cast<const bf16*>(E.cn_ptr[MAX_SEQ * k + b]);
       if (cn != nullptr) {
         cn += (size_t)(nloc - E.cn_row0) * E.D + col;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(cn));

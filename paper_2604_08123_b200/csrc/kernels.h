@@ -14,6 +14,7 @@ constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_MAX_PROBLEMS = 2;
 constexpr int CN_FANIN = 2;   // ControlNet residuals summed per (request, block) (multi-ControlNet fan-in)
+constexpr int MAX_SEQ = 16;   // B_max: sequences per dit_step (per-sequence parameter tables are sized by it)
 #ifndef GEMM_GROUP_M_DEF
 #define GEMM_GROUP_M_DEF 16
 #endif
@@ -43,12 +44,12 @@ struct EpiParams {
   int mod_stride;
   int gate_off;              // column offset of the gate vector inside mod rows
   // ControlNet residual (EPI_RESID img stream)
-  const void* const* cn_ptr; // device [CN_FANIN][8] residual pointers (nullptr = none), bf16 [rows][D]
-  const float* cn_scale;     // device [CN_FANIN][8] kappa_b * inject scale
+  const void* const* cn_ptr; // device [CN_FANIN][MAX_SEQ] residual pointers (nullptr = none), bf16 [rows][D]
+  const float* cn_scale;     // device [CN_FANIN][MAX_SEQ] kappa_b * inject scale
   int cn_row0;               // request-local row of residual row 0 (0: img-stream GEMM; Nt_loc: joint rows)
-  const uint32_t* const* cn_flag;  // device [CN_FANIN][8] ready flags (nullptr = resident / event-ordered)
-  const uint32_t* cn_expect;       // device [CN_FANIN][8] value the flag must reach
-  const int* img_valid;            // device [8] valid image rows per sequence (ragged batch; nullptr = all)
+  const uint32_t* const* cn_flag;  // device [CN_FANIN][MAX_SEQ] ready flags (nullptr = resident / event-ordered)
+  const uint32_t* cn_expect;       // device [CN_FANIN][MAX_SEQ] value the flag must reach
+  const int* img_valid;            // device [MAX_SEQ] valid image rows per sequence (ragged batch; nullptr = all)
   // bf16 outputs
   void* out;
   int ld_out;
@@ -257,7 +258,7 @@ cudaError_t restore_log_launch(const void* jobs_dev, int njobs, const unsigned l
 cudaError_t lora_merge_launch(const void* W, const void* A, const void* Bm, void* out, int rows, int cols, int ra,
                               float scale, cudaStream_t s);
 
-// out[b][n] (+)= sum_k x[b][k] * W[n][k] + bias[n] for b < 8, with x bf16 [8][K]
+// out[b][n] (+)= sum_k x[b][k] * W[n][k] + bias[n] for b < B <= MAX_SEQ, with x bf16 [MAX_SEQ][K]
 // (zero rows beyond B).  Segment table lets one launch cover many weights.
 struct SkinnySeg {
   const void* w;       // bf16 [rows][K]

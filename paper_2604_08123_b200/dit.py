@@ -28,7 +28,7 @@ class dit_config(C.Structure):
                 ("rope_theta", C.c_float), ("guidance_embed", C.c_int32), ("max_batch", C.c_int32),
                 ("max_img_tokens", C.c_int32), ("max_txt_tokens", C.c_int32), ("max_rank", C.c_int32),
                 ("max_adapters", C.c_int32), ("arch", C.c_int32), ("qk_norm", C.c_int32),
-                ("pos_embed_max", C.c_int32), ("pos_embed_base", C.c_int32)]
+                ("pos_embed_max", C.c_int32), ("pos_embed_base", C.c_int32), ("max_sp_world", C.c_int32)]
 
 
 ARCH = {"flux": 0, "sd3": 1}
@@ -142,7 +142,8 @@ def _check(code, ctx=None):
         raise DitError(code, msg)
 
 
-def make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_adapters=0) -> dit_config:
+def make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_adapters=0,
+                max_sp_world=0) -> dit_config:
     c = dit_config()
     c.hidden, c.heads = cfg.hidden, cfg.heads
     c.depth_double, c.depth_single = cfg.depth_double, cfg.depth_single
@@ -158,6 +159,7 @@ def make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_
     c.qk_norm = int(getattr(cfg, "qk_norm", True))
     c.pos_embed_max = getattr(cfg, "pos_embed_max", 192)
     c.pos_embed_base = getattr(cfg, "pos_embed_base", 64)
+    c.max_sp_world = max_sp_world
     return c
 
 
@@ -181,12 +183,13 @@ def _arr(ctype, vals):
 class DiT:
     """One context (one GPU): borrowed weights, adapter pool, ControlNet slots."""
 
-    def __init__(self, cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_adapters=0, device=0):
+    def __init__(self, cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_adapters=0, device=0,
+                 max_sp_world=0):
         import torch
         self.lib = load_library()
         self.cfg = cfg
         self.device = device
-        self.c_cfg = make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank, max_adapters)
+        self.c_cfg = make_config(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank, max_adapters, max_sp_world)
         nbytes = self.lib.dit_workspace_bytes(C.byref(self.c_cfg))
         if nbytes == 0:
             raise DitError(1, "invalid config")

@@ -21,10 +21,10 @@ def _bits_to_bf16_tensor(bits: np.ndarray, device):
 
 class SyntheticDiT(DiT):
     def __init__(self, cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank=0, max_adapters=0, device=0,
-                 seed: Optional[int] = None):
+                 seed: Optional[int] = None, max_sp_world=0):
         import torch
         import synth
-        super().__init__(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank, max_adapters, device)
+        super().__init__(cfg, max_batch, max_img_tokens, max_txt_tokens, max_rank, max_adapters, device, max_sp_world)
         seed = synth.WEIGHT_SEED if seed is None else seed
         dev = f"cuda:{device}"
         ws = {}

@@ -38,8 +38,16 @@ def test_workspace_bytes_host_only():
     nb = lib.dit_workspace_bytes(C.byref(big))
     # activations for B=8 x 4608 rows + 4 adapter slots of ~448 MB: a few GB, well under 180 GB
     assert 3e9 < nb < 20e9, nb
-    bad = dit.make_config(synth.TINY, 9, 16, 8)           # B_max > 8
+    b16 = dit.make_config(synth.TINY, 16, 16, 8)          # B_max = 16 (e.g. 8 CFG requests)
+    assert lib.dit_workspace_bytes(C.byref(b16)) > n
+    bad = dit.make_config(synth.TINY, 17, 16, 8)          # B_max > 16
     assert lib.dit_workspace_bytes(C.byref(bad)) == 0
+    # a single-GPU workspace drops the SP all-to-all buffers: 16 B_max N D bytes (1.8 GB here)
+    one = dit.make_config(synth.FLUX, 8, 4096, 512, 64, 4, max_sp_world=1)
+    n1 = lib.dit_workspace_bytes(C.byref(one))
+    assert nb - n1 == 16 * 8 * 4608 * 3072 - 65536, nb - n1
+    badsp = dit.make_config(synth.TINY, 2, 16, 8, max_sp_world=65)
+    assert lib.dit_workspace_bytes(C.byref(badsp)) == 0
     bad2 = dit.make_config(synth.TINY, 2, 16, 8)
     bad2.rope_axes[0] = 6                                   # axes no longer sum to head dim
     assert lib.dit_workspace_bytes(C.byref(bad2)) == 0
