@@ -507,6 +507,10 @@ def run_gpu(args):
                      "frac": (achieved / peaks["bf16_sus"]) if achieved else None, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside the long step)",
+                     # the sustained peak is cuBLAS back-to-back at the power-capped clock (~1.33 GHz);
+                     # attention-heavy steps (cfg5) let the GEMMs clock higher, so frac can exceed 1 --
+                     # the burst-peak fraction bounds it from the other side
+                     "frac_of_burst_peak": (achieved / peaks["bf16"]) if achieved else None,
                      "launches": g_n, "share_of_step": g_ms / prof_total if prof_total else None},
         "kernels": {
             "gemm": {"ms_per_step": g_ms / args.steps, "tflops": achieved, "launches_per_step": g_n / args.steps},
