@@ -235,7 +235,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   const int nqb = (N + NQ * BQ - 1) / (NQ * BQ);
   const int total = nqb * p.H * p.B;               // work items: (query block, head, request), block fastest
 
-  constexpr int W_LOAD = NQ * SM_WARPS_PER_TILE + 2, W_MMA = W_LOAD + 1;   // highest ids: SMSP arbiter priority
+#ifndef ATTN_ROLE_BASE
+#define ATTN_ROLE_BASE 2
+#endif
+  // producer / MMA warps: above every softmax warp (SMSP arbiter priority); ATTN_ROLE_BASE picks
+  // which two of warps 8-11 (SMSPs 0-3) they take
+  constexpr int W_LOAD = NQ * SM_WARPS_PER_TILE + ATTN_ROLE_BASE, W_MMA = W_LOAD + 1;
   if (warp == W_LOAD && lane == 0) {
     tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);

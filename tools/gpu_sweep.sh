@@ -1,6 +1,7 @@
 cd $GRAFT_REPO_ROOT
-timeout 120 python tools/resid_bench.py 2>&1 | head -3
-timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider -x 2>&1 | tail -4
-for rep in 1 2; do for cl in 2 4; do
-  echo "== cl$cl $(DIT_GEMM_CL=$cl timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],4), d["clocks"]["sm_mhz"], round(d["kernels"]["gemm"]["tflops"]), {k:round(v["tflops"]) for k,v in d["kernels"]["gemm_by_type"].items()})')"
+V=paper_2604_08123_b200/build/variants
+for rep in 1 2; do for n in base rb0 rb1; do
+  lib=$V/libdit_$n.so; [ $n = base ] && lib=
+  echo "== $n $(DIT_LIB_OVERRIDE=$lib timeout 120 python tools/attn_bench.py 8 24 4608 128 | tail -1)"
 done; done
+for n in base rb0; do lib=$V/libdit_$n.so; [ $n = base ] && lib=; DIT_LIB_OVERRIDE=$lib TRACE=1 python tools/attn_bench.py | tail -3; done
