@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1516,12 +1517,48 @@ cudaEvent_t prof_event(dit_ctx* c) {
   }
   return c->ev_pool[c->ev_next++];
 }
-void prof_begin(dit_ctx* c, cudaStream_t s) {
+// NVTX ranges (nsys timelines): one per dit_step, per block and per launch, named
+// by the profiling kind.  Header-only NVTX v3: without an attached tool a push / pop is a few ns.
+// DIT_NVTX=0 turns them off.
+bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = getenv("DIT_NVTX");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+const char* kind_name(int kind) {
+  static const char* const names[19] = {"gemm",        "attention",   "lnmod",       "modulation", "other",
+                                        "sp_exchange", "sp_layout",   "",            "",           "",
+                                        "gemm:embed",  "gemm:dbl_qkv", "gemm:dbl_proj", "gemm:dbl_fc1", "gemm:dbl_fc2",
+                                        "gemm:sgl_linear1", "gemm:sgl_linear2", "gemm:final", "gemm:lora_shrink"};
+  return kind >= 0 && kind < 19 ? names[kind] : "launch";
+}
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  NvtxRange(const char* fmt, int i) : on(nvtx_on()) {
+    if (on) {
+      char buf[64];
+      snprintf(buf, sizeof(buf), fmt, i);
+      nvtxRangePushA(buf);
+    }
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+
+void prof_begin(dit_ctx* c, cudaStream_t s, int kind) {
+  if (nvtx_on()) nvtxRangePushA(kind_name(kind));
   if (!c->prof_on) return;
   c->prof_a = prof_event(c);
   cudaEventRecord(c->prof_a, s);
 }
 void prof_end(dit_ctx* c, cudaStream_t s, int kind, double flops) {
+  if (nvtx_on()) nvtxRangePop();
   if (!c->prof_on) return;
   cudaEvent_t b = prof_event(c);
   cudaEventRecord(b, s);
@@ -1613,7 +1650,7 @@ int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s, double flop
   a.num_problems = k;
   a.total_tiles = t;
   if (t == 0) return DIT_OK;
-  prof_begin(c, s);
+  prof_begin(c, s, c->gemm_label);
   cudaError_t e = gemm_launch(a, c->num_sms, s);
   prof_end(c, s, c->gemm_label, flops);
   c->launches++;
@@ -1693,7 +1730,7 @@ extern "C" int dit_sp_exchange(const dit_ctx* c) {
 #define CKC(x) CKK(x, 4, 0.0)
 #define CKK(x, kind, flops)                                                          \
   do {                                                                               \
-    prof_begin(c, s);                                                                \
+    prof_begin(c, s, kind);                                                          \
     cudaError_t _e = (x);                                                            \
     prof_end(c, s, kind, flops);                                                     \
     c->launches++;                                                                   \
@@ -1713,6 +1750,7 @@ extern "C" int dit_step(dit_ctx* c, const dit_batch* b, void* stream) {
 }
 
 static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
+  NvtxRange nv_step(mode == STEP_CAPTURE ? "dit_step (capture)" : mode == STEP_STAGE ? "dit_step (stage)" : "dit_step");
   // ControlNet registrations apply to exactly one dit_step call: cleared on EVERY exit (a
   // validation error or a failed launch included), so no stale borrowed pointer outlives it
   struct CnClear {
@@ -2061,7 +2099,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
   // fused exchange barrier: my stores into the peers are done -> tell them; wait for theirs
   auto exchange_barrier = [&]() -> int {
     ++c->sp_epoch;
-    prof_begin(c, s);
+    prof_begin(c, s, 5);
     cudaError_t e1 = sp_signal_launch(c->peer_flags, c->rank, P, c->sp_epoch, s);
     cudaError_t e2 = sp_wait_launch(c->flags, c->rank, P, c->sp_epoch, s);
     prof_end(c, s, 5, 0.0);
@@ -2070,7 +2108,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     return DIT_OK;
   };
   auto a2a = [&](const void* snd, void* rcv, size_t count) -> int {
-    prof_begin(c, s);
+    prof_begin(c, s, 5);
     if (c->comm) {
       ncclResult_t r = ncclAlltoAll(snd, rcv, count, ncclBfloat16, c->comm, s);
       if (r != ncclSuccess) return c->fail(DIT_ENCCL, "ncclAlltoAll: %s", ncclGetErrorString(r));
@@ -2163,7 +2201,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
       lp.seg_shift_off[0] = shI;
       lp.seg_scale_off[0] = scI;
     }
-    prof_begin(c, s);
+    prof_begin(c, s, 2);
     cudaError_t e = lnmod_launch(lp, s);
     prof_end(c, s, 2, 0.0);
     c->launches++;
@@ -2198,6 +2236,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
 
   // ---- double-stream blocks
   for (int i = 0; i < c->Ld; ++i) {
+    NvtxRange nv_blk("double block %d", i);
     const DoubleStream& I = c->dbl[0][i];
     const DoubleStream& T = c->dbl[1][i];
     const int mI = (i * 2 + 0) * 6 * D, mT = (i * 2 + 1) * 6 * D;
@@ -2328,6 +2367,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
 
   // ---- single-stream blocks on the joint sequence
   for (int j = 0; j < c->Ls; ++j) {
+    NvtxRange nv_blk("single block %d", j);
     const SingleBlk& SB = c->sgl[j];
     const int mj = mod_off_single + j * 3 * D;
     {
@@ -2474,7 +2514,7 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     c->gemm_label = 17;
     CK(run_gemm(c, &p, 1, s));
     if (lpar) {   // latent parallelism: per-step gather of the two branches' v
-      prof_begin(c, s);
+      prof_begin(c, s, 5);
       if (c->lp_fused) {   // both halves are in place once the peer's epilogue has released its flag
         ++c->sp_epoch;
         ++c->lp_steps;
