@@ -168,12 +168,26 @@ DEVI float2 poly_exp2x2(float2 x) {
 
 DEVI void named_bar_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
-// Debug timeline (clock64 stamps of one CTA), enabled by dit_debug_attention_trace.
+// Debug timeline (clock64 stamps of one CTA): compiled in only with -DATTN_TRACE=1 (a variant build,
+// `python tools/variant.py trace attention_tc.cu -DATTN_TRACE=1`; enabled at run time by
+// dit_debug_attention_trace).  Even predicated off, the stamps cost ~35 issue slots per softmax warp
+// and kv tile on the critical path, so the product build has none.
 __device__ long long* g_attn_trace = nullptr;
+#ifndef ATTN_TRACE
+#define ATTN_TRACE 0
+#endif
+#if ATTN_TRACE
+#define TRACE_PTR (blockIdx.x == 0 ? g_attn_trace : nullptr)
 #define TRACE(ev, j)                                                                       \
   do {                                                                                     \
     if (trace) trace[(ev) * 64 + ((j) & 63)] = clock64();                                  \
   } while (0)
+#else
+#define TRACE_PTR (static_cast<long long*>(nullptr))
+#define TRACE(ev, j) \
+  do {               \
+  } while (0)
+#endif
 
 struct Maps {
   CUtensorMap q, k, v;   // 3D {HD, N, B*H}, box {64, 128, 1}
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   const uint32_t tmem = *tmem_slot;
   if (warp >= NQ * SM_WARPS_PER_TILE) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REG_OTHER));
-   long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;   // loaded after setmaxnreg (no spill)
+   long long* const trace = TRACE_PTR;   // loaded after setmaxnreg (no spill)
    if (warp == W_LOAD) {
     if (lane == 0) {
       int g = 0, it = 0;                           // kv-tile counter (ring position), item counter
@@ -366,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
    }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ATTN_REG_SOFTMAX));
-    long long* trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
+    long long* const trace = TRACE_PTR;
     // softmax: warps 0-3 own query tile 0, warps 4-7 tile 1; one query row per thread
     // (TMEM lane = row), all 128 score columns of it in registers: no cross-warp exchange.
     const int t = warp >> 2;

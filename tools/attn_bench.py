@@ -1,4 +1,6 @@
-"""Attention kernel alone: TFLOP/s at the bench shape (B=8, H=24, N=4608, d=128) + a parity spot check vs torch SDPA."""
+"""Attention kernel alone: TFLOP/s at the bench shape (B=8, H=24, N=4608, d=128) + a parity spot check vs torch SDPA.
+TRACE=1 prints the clock64 timeline of CTA 0; it needs a trace build of the kernel:
+python tools/variant.py trace attention_tc.cu -DATTN_TRACE=1, then DIT_LIB_OVERRIDE=<that .so>."""
 import ctypes as C
 import os
 import sys
