@@ -254,7 +254,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
 #endif
   // producer / MMA warps: above every softmax warp (SMSP arbiter priority); ATTN_ROLE_BASE picks
   // which two of warps 8-11 (SMSPs 0-3) they take
-  constexpr int W_LOAD = NQ * SM_WARPS_PER_TILE + ATTN_ROLE_BASE, W_MMA = W_LOAD + 1;
+#ifndef ATTN_ROLE_LOW
+#define ATTN_ROLE_LOW 0
+#endif
+  // ATTN_ROLE_LOW = 1: the producer / MMA warpgroup takes warps 0-3 (LOWEST arbiter priority) and
+  // the softmax warpgroups warps 4-11
+  constexpr int SM_W0 = ATTN_ROLE_LOW ? 4 : 0;   // first softmax warp
+  constexpr int W_LOAD = ATTN_ROLE_LOW ? ATTN_ROLE_BASE : NQ * SM_WARPS_PER_TILE + ATTN_ROLE_BASE, W_MMA = W_LOAD + 1;
   if (warp == W_LOAD && lane == 0) {
     tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp >= NQ * SM_WARPS_PER_TILE) {
+  if (ATTN_ROLE_LOW ? warp < SM_W0 : warp >= NQ * SM_WARPS_PER_TILE) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REG_OTHER));
    long long* const trace = TRACE_PTR;   // loaded after setmaxnreg (no spill)
    if (warp == W_LOAD) {
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     long long* const trace = TRACE_PTR;
     // softmax: warps 0-3 own query tile 0, warps 4-7 tile 1; one query row per thread
     // (TMEM lane = row), all 128 score columns of it in registers: no cross-warp exchange.
-    const int t = warp >> 2;
+    const int t = (warp - SM_W0) >> 2;
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
