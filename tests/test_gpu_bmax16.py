@@ -108,3 +108,35 @@ def test_batch_limits_and_single_gpu_workspace(torch_cuda):
         assert rc != 0 and "max_sp_world" in lib.dit_last_error(m.ctx).decode()
     finally:
         lib.dit_local_group_destroy(group)
+
+
+@pytest.mark.parametrize("exchange", ["fused", "a2a"])
+def test_sequence_parallel_sixteen_sequences_bitwise(torch_cuda, exchange, monkeypatch):
+    """Ulysses SP (P = 2, in-process group) over 12 requests with d = 128 heads: every per-sequence
+    index map of the exchange (fused peer stores / all-to-all + gather / scatter) beyond the old
+    8-sequence cap; bitwise equal to the single-rank step (pin P10)."""
+    import torch
+    from paper_2604_08123_b200 import dit as D
+    from tests.test_gpu_parity import _shard_step
+    monkeypatch.setenv("DIT_SP_NCCL", "1" if exchange == "a2a" else "0")
+    cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, depth_single=1, rope_axes=(16, 56, 56))
+    B, hh, ww, nt, P = 12, 8, 8, 16, 2
+    ref = _model(cfg, 16, hh * ww, nt, rank=8, adapters=1)
+    ref.register_synthetic_lora(5, rank=8, index=0)
+    batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1)
+    batch.adapter_id = np.array([5, -1] * 6, dtype=np.int32)
+    lat1, v1 = ref.step(batch)
+    group = D.load_library().dit_local_group_create(P)
+    models = []
+    for r in range(P):
+        m = _model(cfg, 16, hh * ww, nt, rank=8, adapters=1)
+        m.register_synthetic_lora(5, rank=8, index=0)
+        m.sp_init_local(group, r)
+        models.append(m)
+    latP, vP = _shard_step(models, batch, P)
+    np.testing.assert_array_equal(vP, v1)
+    np.testing.assert_array_equal(latP, lat1)
+    for m in models:
+        m.close()
+    D.load_library().dit_local_group_destroy(group)
+    torch.cuda.synchronize()
