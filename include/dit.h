@@ -85,10 +85,11 @@ typedef struct dit_config {
   int32_t qk_norm;
   int32_t pos_embed_max;   /* 192 for SD3 / SD3.5                                 */
   int32_t pos_embed_base;  /* 64 for SD3 / SD3.5                                  */
-  /* Largest sequence-parallel world the workspace is sized for: 0 = the default (8,
-   * with the all-to-all send / recv buffers, 16 B_max N D bytes), 1 = single GPU (no
+  /* Sequence-parallel capacity of the workspace: 0 = default (the all-to-all send / recv
+   * buffers, 16 B_max N D bytes, are carved; no cap on the world size), 1 = single GPU (no
    * exchange buffers: 1.8 GB less at Flux 1024^2 with B_max 8; sp_init with world > 1,
-   * sp_init_local and sp_init_peers then fail with DIT_EPARALLEL), 2..64 = that cap. */
+   * sp_init_local and sp_init_peers then fail with DIT_EPARALLEL), 2..64 = buffers carved,
+   * worlds above the value refused with DIT_EPARALLEL. */
   int32_t max_sp_world;
 } dit_config;
 
