@@ -1588,6 +1588,8 @@ GemmProblem base_problem(dit_ctx* c, const void* A, int M, int K, int lda, const
   P.num_tiles = P.tiles_m * P.tiles_n;
   P.epi = epi;
   P.slot_cap = c->slot_cap;
+  if (epi.kind == EPI_RESID)   // h [R_max][D] fp32 for the epilogue's TMA reduce-add
+    P.tmH_ok = make_tmap_2d_f32(&P.tmH, epi.h, (uint64_t)epi.D, (uint64_t)c->Rmax, (uint64_t)epi.D * 4, 32, 32) ? 1 : 0;
   return P;
 }
 
@@ -2837,6 +2839,7 @@ extern "C" int dit_debug_gemm_resid(const void* A, const void* W, const void* bi
   P.epi.mod = gate;
   P.epi.mod_stride = 0;
   P.epi.gate_off = 0;
+  P.tmH_ok = make_tmap_2d_f32(&P.tmH, h, (uint64_t)N, (uint64_t)M, (uint64_t)N * 4, 32, 32) ? 1 : 0;
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.p[0] = P;

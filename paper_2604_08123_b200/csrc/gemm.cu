@@ -36,7 +36,13 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 320;
 constexpr int W_LOAD = 8, W_MMA = 9;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+#ifndef GEMM_RESID_TMA
+#define GEMM_RESID_TMA 1
+#endif
+// gated residual via TMA reduce-add: per epilogue warp a 32 x 32 fp32 staging box (4 KB, 1024-B
+// aligned for SWIZZLE_128B) after a 1 KB barrier area
+constexpr int EPI_BOX_OFF = STAGES * STAGE_BYTES + 1024;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + (GEMM_RESID_TMA ? 1024 + 8 * 4096 : 256);
 size_t gemm_smem_bytes() { return SMEM_BYTES; }
 
 struct TileInfo {
@@ -137,10 +143,10 @@ DEVI void cn_add8(float4 (&h4)[8], const bf16* cn, float kap) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const uint2 c2 = __ldcg(reinterpret_cast<const uint2*>(cn) + q);
-    h4[q].x += kap * bf16_lo(c2.x);
-    h4[q].y += kap * bf16_hi(c2.x);
-    h4[q].z += kap * bf16_lo(c2.y);
-    h4[q].w += kap * bf16_hi(c2.y);
+    h4[q].x = fmaf(kap, bf16_lo(c2.x), h4[q].x);
+    h4[q].y = fmaf(kap, bf16_hi(c2.x), h4[q].y);
+    h4[q].z = fmaf(kap, bf16_lo(c2.y), h4[q].z);
+    h4[q].w = fmaf(kap, bf16_hi(c2.y), h4[q].w);
   }
 }
 
@@ -183,7 +189,8 @@ DEVI void norm_rope_half(float (&y)[64], float rs, const bf16* g, const float4* 
 #ifndef GEMM_EPI_FAKE
 #define GEMM_EPI_FAKE 0
 #endif
-DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase, int row_in_tile, int c_lo) {
+DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase, int row_in_tile, int c_lo,
+                        float4* box) {
   const EpiParams& E = P.epi;
   const int r = ti.m * GEMM_TM + row_in_tile;
   const bool row_ok = r < P.M;
@@ -367,6 +374,17 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
     return;
   }
 
+#if GEMM_RESID_TMA
+  // the warp's 32 rows: one contiguous block of h rows (same request, all < M) -> TMA reduce-add
+  const int lw = row_in_tile & 31;
+  const int rw0 = r - lw;
+  const bool boxed = E.kind == EPI_RESID && P.tmH_ok && rw0 + 31 < P.M &&
+                     rw0 / E.rows_per_req == (rw0 + 31) / E.rows_per_req;
+  const int jrow0 = boxed ? (rw0 / E.rows_per_req) * E.joint_n + E.joint_off + rw0 % E.rows_per_req : 0;
+#else
+  constexpr bool boxed = false;
+  constexpr int lw = 0, jrow0 = 0;
+#endif
 #pragma unroll 1
   for (int c2 = c_lo; c2 < c_hi; c2 += 64) {
     if (n0 + c2 >= P.N) break;
@@ -380,8 +398,9 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
     const int c0 = c2 + hh * 32;
     const int col = n0 + c0;
     if (col >= P.N) break;
-    if (!row_ok) continue;
     const int valid = min(32, P.N - col);
+    const bool tma_chunk = boxed && valid == 32;   // warp-uniform
+    if (!row_ok && !tma_chunk) continue;
     float bv[32], y[32];
     load_bias32(bias, col, P.N, bv);
 #pragma unroll
@@ -422,30 +441,56 @@ DEVI void epilogue_tile(const GemmProblem& P, const TileInfo& ti, uint32_t tbase
           cn_acquire(E.cn_flag[MAX_SEQ + b], E.cn_expect[MAX_SEQ + b]);
         }
       }
+      // h += v with v = g (acc + bias) (+ kappa R per ControlNet), v rounded once and added to h
+      // with a single rounding on EVERY path (TMA reduce-add, vector and scalar fallbacks), so a
+      // row's result does not depend on which path its warp takes (batch / shard invariance)
       if (valid == 32) {
-        float4 h4[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) h4[q] = reinterpret_cast<float4*>(hp)[q];
+        float4 v4[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 g4 = __ldg(reinterpret_cast<const float4*>(gp) + q);
-          h4[q].x += g4.x * y[4 * q];
-          h4[q].y += g4.y * y[4 * q + 1];
-          h4[q].z += g4.z * y[4 * q + 2];
-          h4[q].w += g4.w * y[4 * q + 3];
+          v4[q] = make_float4(__fmul_rn(g4.x, y[4 * q]), __fmul_rn(g4.y, y[4 * q + 1]), __fmul_rn(g4.z, y[4 * q + 2]),
+                              __fmul_rn(g4.w, y[4 * q + 3]));
         }
-        if (cn0 != nullptr) cn_add8(h4, cn0, kap0);
-        if (cn1 != nullptr) cn_add8(h4, cn1, kap1);
+        if (cn0 != nullptr) cn_add8(v4, cn0, kap0);
+        if (cn1 != nullptr) cn_add8(v4, cn1, kap1);
+        if (tma_chunk) {
+          // the warp's swizzled 32 x 32 box, then ONE TMA reduce-add h[jrow0 .. +32)[col .. +32) += box:
+          // the SM never loads h
+#if GEMM_RESID_TMA
 #pragma unroll
-        for (int q = 0; q < 8; ++q) reinterpret_cast<float4*>(hp)[q] = h4[q];
+          for (int q = 0; q < 8; ++q) box[lw * 8 + (q ^ (lw & 7))] = v4[q];
+          __syncwarp();
+          fence_async_shared();
+          if (lw == 0) {
+            asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&P.tmH)),
+                         "r"(smem_u32(box)), "r"(col), "r"(jrow0)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // box reusable
+          }
+          __syncwarp();
+#endif
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 h4 = reinterpret_cast<float4*>(hp)[q];
+            h4.x = __fadd_rn(h4.x, v4[q].x);
+            h4.y = __fadd_rn(h4.y, v4[q].y);
+            h4.z = __fadd_rn(h4.z, v4[q].z);
+            h4.w = __fadd_rn(h4.w, v4[q].w);
+            reinterpret_cast<float4*>(hp)[q] = h4;
+          }
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) {   // static indices keep y in registers
           if (e < valid) {
-            float hv = hp[e] + gp[e] * y[e];
-            if (cn0 != nullptr) hv += kap0 * __bfloat162float(__ldcg(cn0 + e));
-            if (cn1 != nullptr) hv += kap1 * __bfloat162float(__ldcg(cn1 + e));
-            hp[e] = hv;
+            float v = __fmul_rn(gp[e], y[e]);
+            if (cn0 != nullptr) v = fmaf(kap0, __bfloat162float(__ldcg(cn0 + e)), v);
+            if (cn1 != nullptr) v = fmaf(kap1, __bfloat162float(__ldcg(cn1 + e)), v);
+            hp[e] = __fadd_rn(hp[e], v);
           }
         }
       }
@@ -639,6 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int wq = warp & 3;              // TMEM lane quarter this warp may access
     const int half = warp >> 2;           // column half of the tile
     const int row_in_tile = (int)cta * GEMM_BM + wq * 32 + lane;
+    float4* epi_box = reinterpret_cast<float4*>(smem + EPI_BOX_OFF + warp * 4096);
     int iter = 0;
     for (int t = cid; t < args.total_tiles; t += ncl, ++iter) {
       const TileInfo ti = decode_tile(args, t);
@@ -649,7 +695,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (warp == 0 && lane == 0) GTRACE(0, iter);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(wq * 32) << 16) + acc * GEMM_BN;
-      epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile, half * (GEMM_BN / 2));
+      epilogue_tile(args.p[ti.p], ti, tbase, row_in_tile, half * (GEMM_BN / 2), epi_box);
       if (lane == 0 && (warp == 0 || warp == 7)) GTRACE(warp == 0 ? 1 : 2, iter);
       tc_fence_before();
       __syncwarp();
@@ -660,6 +706,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_cta(&tempty[acc], 0);
       }
     }
+#if GEMM_RESID_TMA
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // reduce-adds complete
+#endif
   }
   tc_fence_before();
   cluster_sync();
@@ -703,6 +752,19 @@ bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t oute
     return false;
   }
   return true;
+}
+
+bool make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                      uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,

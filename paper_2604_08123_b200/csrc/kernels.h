@@ -88,6 +88,8 @@ struct GemmProblem {
   CUtensorMap tmB;       // B [N][K] bf16, box {64, 128} (each CTA of the pair loads half of N)
   CUtensorMap tmAx;      // LoRA K-extension A: S [M][slots*r_alloc], box {64, 128}
   CUtensorMap tmBx;      // LoRA K-extension B: pool viewed [slot*N][r_alloc], box {64, 128}
+  CUtensorMap tmH;       // EPI_RESID: fp32 residual stream h [rows][D], box {32, 32} (TMA reduce-add)
+  int tmH_ok;
   int M, N, K;
   int tiles_m, tiles_n;  // tiles_m: 256-row pair tiles
   int tile_begin;        // first global tile index of this problem
@@ -112,6 +114,9 @@ struct GemmArgs {
 // Encode a 2D/3D bf16 tensor map with SWIZZLE_128B (box inner = 64 elements).
 bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
                   uint32_t box_inner, uint32_t box_outer);
+// fp32 2D map, SWIZZLE_128B (box inner = 32 elements = 128 B)
+bool make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                      uint32_t box_inner, uint32_t box_outer);
 bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                   uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
 

@@ -1,6 +1,7 @@
 cd $GRAFT_REPO_ROOT
-DIT_ATTN_SI=1 timeout 300 python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "attention or head_dim or ragged or tiny" -x 2>&1 | tail -3
-for rep in 1 2 3; do for si in 0 1; do
-  echo "== si=$si $(DIT_ATTN_SI=$si timeout 120 python tools/attn_bench.py 8 24 4608 128 | tail -1)"
-  echo "== si=$si $(DIT_ATTN_SI=$si timeout 120 python tools/attn_bench.py 8 24 4429 64 | tail -1)"
-done; done
+V=paper_2604_08123_b200/build/variants
+timeout 1200 python -m pytest -q -p no:cacheprovider tests -m gpu 2>&1 | tail -3
+for n in base rtma0 base rtma0; do
+  lib=$V/libdit_$n.so; [ $n = base ] && lib=
+  echo "== $n $(DIT_LIB_OVERRIDE=$lib timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],4), d["clocks"]["sm_mhz"], round(d["kernels"]["gemm"]["tflops"]), {k:round(v["tflops"]) for k,v in d["kernels"]["gemm_by_type"].items() if k in ("dbl_proj","dbl_fc2","sgl_linear2")})')"
+done
