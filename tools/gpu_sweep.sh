@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT
 V=paper_2604_08123_b200/build/variants
-for rep in 1 2; do for n in base lnb7 ln7; do
+timeout 1200 python -m pytest -q -p no:cacheprovider tests -m gpu 2>&1 | tail -3
+for n in base otma0 base otma0 base otma0; do
   lib=$V/libdit_$n.so; [ $n = base ] && lib=
-  echo "== $n $(DIT_LIB_OVERRIDE=$lib timeout 300 python bench.py --steps 6 --warmup 3 --no-cpu-baseline | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],4), d["clocks"]["sm_mhz"], "lnmod", round(d["kernels"]["lnmod"]["ms_per_step"],2))')"
-done; done
-DIT_LIB_OVERRIDE=$V/libdit_lnb7.so timeout 300 python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "tiny or ragged or batch" 2>&1 | tail -2
+  echo "== $n $(DIT_LIB_OVERRIDE=$lib timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],4), d["clocks"]["sm_mhz"], round(d["kernels"]["gemm"]["tflops"]), {k:round(v["tflops"]) for k,v in d["kernels"]["gemm_by_type"].items() if k in ("dbl_fc1","sgl_linear1","dbl_qkv","dbl_proj")})')"
+done
