@@ -438,15 +438,6 @@ int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, 
 int dit_debug_gemm(const void* A, const void* W, const void* bias, void* out, int32_t M, int32_t N, int32_t K,
                    void* stream);
 
-/* Bench/test-only: lead (k-blocks) of the GEMM's k-block lockstep for every later GEMM launch of
- * this process (a cluster's TMA producer holds back while it is more than `lead`
- * k-blocks ahead of the slowest cluster of its launch, so the tiles that share an A or B panel
- * read it from L2 instead of HBM).  A scheduling hint only -- results are bitwise identical for
- * every value, and a wait longer than 0.5 ms (a cluster not resident) switches it off for that
- * launch.  lead <= 0 turns it off.  Overrides the DIT_GEMM_LOCK_D environment default; returns the
- * previous lead. */
-int dit_debug_gemm_lock(int32_t lead);
-
 /* Bench-only: h[M][N] (device fp32) += gate[N] (device fp32) * (A W^T + bias) through the step's
  * GEMM with its gated-residual epilogue (N % 32 == 0).  Asynchronous on stream. */
 int dit_debug_gemm_resid(const void* A, const void* W, const void* bias, float* h, const float* gate, int32_t M,

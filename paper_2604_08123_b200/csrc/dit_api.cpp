@@ -207,7 +207,6 @@ struct dit_ctx {
   void* peer_cat[8] = {};
   PeerFlags peer_flags = {};
   uint32_t* flags = nullptr;         // [8] arrival epochs, written by the peers
-  uint32_t* gemm_sync = nullptr;     // [GEMM_SYNC_WORDS] the GEMM's k-block lockstep state (this context's launches)
   uint32_t sp_epoch = 0;
   std::vector<void*> ipc_opened;
   // latent (CFG) parallelism: rank 0 conditional, rank 1 unconditional branch
@@ -369,7 +368,7 @@ Layout layout_of(const dit_config& c) {
   L.xprep = cv.take(MAX_SEQ * std::max<size_t>({D, 256, (size_t)c.pooled_dim}) * 2);
   L.temb = cv.take(MAX_SEQ * 256 * 2);
   L.segs = cv.take((nseg + 6) * sizeof(SkinnySeg));
-  L.params = cv.take(GEMM_SYNC_WORDS * 4 + 4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * MAX_SEQ * 2 * (sizeof(void*) + 4) + 2048);
+  L.params = cv.take(4096 + (size_t)std::max(c.depth_double + c.depth_single, 1) * CN_FANIN * MAX_SEQ * 2 * (sizeof(void*) + 4) + 2048);
   L.rowspace = cv.take(3 * (R * 4 + tiles * MAX_SEQ * 4 + tiles * 4 + tiles * MAX_SEQ * 8) + 3 * 1024);
   size_t per_slot = 0;
   if (c.max_adapters > 0 && r_alloc > 0) {
@@ -474,8 +473,6 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     c->p_img_valid = reinterpret_cast<int*>(p + cv.take(MAX_SEQ * 4));
     c->p_seq_valid = reinterpret_cast<int*>(p + cv.take(MAX_SEQ * 4));
     c->flags = reinterpret_cast<uint32_t*>(p + cv.take(8 * 4));
-    c->gemm_sync = reinterpret_cast<uint32_t*>(p + cv.take(GEMM_SYNC_WORDS * 4));
-    cudaMemset(c->gemm_sync, 0, GEMM_SYNC_WORDS * 4);
   }
   {
     const size_t tiles = (c->Rmax + GEMM_BM - 1) / GEMM_BM + 4;
@@ -1654,7 +1651,6 @@ int run_gemm(dit_ctx* c, GemmProblem* probs, int np, cudaStream_t s, double flop
   }
   a.num_problems = k;
   a.total_tiles = t;
-  a.sync = c->gemm_sync;
   if (t == 0) return DIT_OK;
   prof_begin(c, s, c->gemm_label);
   cudaError_t e = gemm_launch(a, c->num_sms, s);
@@ -2817,8 +2813,6 @@ extern "C" int dit_debug_gemm(const void* A, const void* W, const void* bias, vo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return gemm_launch(a, sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
 }
-
-extern "C" int dit_debug_gemm_lock(int32_t lead) { return gemm_set_lock_default(lead); }
 
 // Bench-only: the gated-residual projection of the step alone: h[M][N] (fp32) += gate[N] * (A W^T +
 // bias) through the same GEMM + EPI_RESID epilogue (profiling the epilogue's cost).

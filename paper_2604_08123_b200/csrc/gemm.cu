@@ -23,8 +23,6 @@
 // img and txt streams of a double block share one launch), rasterised in
 // groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
 #include <cstdio>
-#include <cstdlib>
-#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -38,20 +36,6 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 320;
 constexpr int W_LOAD = 8, W_MMA = 9;
-// k-block lockstep (see the producer): check interval, give-up time, wait-time statistics build
-#ifndef GEMM_LOCK_W
-#define GEMM_LOCK_W 8
-#endif
-#ifndef GEMM_LOCK_STATS
-#define GEMM_LOCK_STATS 0
-#endif
-#ifndef GEMM_HEAVY_GROUP_DEF
-#define GEMM_HEAVY_GROUP_DEF 0
-#endif
-#ifndef GEMM_LOCK_D_DEF
-#define GEMM_LOCK_D_DEF 0
-#endif
-constexpr uint64_t LOCK_TIMEOUT_NS = 500000;
 #ifndef GEMM_RESID_TMA
 #define GEMM_RESID_TMA 1
 #endif
@@ -77,10 +61,10 @@ DEVI TileInfo decode_tile(const GemmArgs& A, int t) {
     ti.slot = e.y;
     ti.n = 0;
   } else {
-    int per_group = P.group_m * P.tiles_n;   // tiles_m counts 256-row pair tiles
+    int per_group = GEMM_GROUP_M * P.tiles_n;   // tiles_m counts 256-row pair tiles
     int g = local / per_group;
-    int first_m = g * P.group_m;
-    int gm = min(P.group_m, P.tiles_m - first_m);
+    int first_m = g * GEMM_GROUP_M;
+    int gm = min(GEMM_GROUP_M, P.tiles_m - first_m);
     int within = local - g * per_group;
     ti.m = first_m + within % gm;
     ti.n = within / gm;
@@ -574,16 +558,6 @@ extern "C" int dit_debug_gemm_trace(long long* buf) {
 #define GTRACE(ev, it) do {} while (0)
 #endif
 
-// k-block lockstep helpers: each lane loads the progress words of clusters lane, lane + 32, lane + 64
-// (absent clusters read as "done"); a word of another launch (epoch) counts as no progress
-DEVI void poll_progress(const uint32_t* sync, int ncl, int lane, uint32_t (&v)[3]) {
-#pragma unroll
-  for (int q = 0; q < 3; ++q) v[q] = lane + 32 * q < ncl ? ld_relaxed_gpu(sync + gemm_sync_prog(lane + 32 * q)) : 0xFFFFFFFFu;
-}
-DEVI uint32_t prog_view(uint32_t v, uint32_t epoch) {
-  return v == 0xFFFFFFFFu ? 0xFFFFFu : ((v >> 20) == epoch ? (v & 0xFFFFFu) : 0u);
-}
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -631,62 +605,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == W_LOAD) {
-    // k-block lockstep (L2 locality): the leader's producer publishes its progress
-    // (k-blocks issued so far) every LOCK_W k-blocks and holds back while it leads the slowest cluster by
-    // more than lock_d k-blocks, so the ~20 distinct A / B panels a round of tiles streams are
-    // fetched from HBM once and re-read from L2 by the tiles that share them (free-running
-    // clusters drift apart by whole tiles over a K = 12288-15360 loop and re-fetch them).  A
-    // hint only: a wait longer than LOCK_TIMEOUT_NS (a cluster not resident) turns it off for
-    // the launch.  The peer CTA's producer follows its leader through the stage ring.
-    uint32_t* const sync = args.sync;
-    const bool lock = sync != nullptr && args.lock_d > 0 && leader && ncl <= GEMM_LOCK_MAX_CL;
-    bool lock_on = lock;
-    const uint32_t epoch = lock ? (ld_relaxed_gpu(sync) & 0xFFFu) : 0u;
-    uint64_t wait_ns = 0;
-    uint32_t wait_cnt = 0;
-    uint32_t max_lead = 0;
-    uint32_t pend[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};   // no view yet: no wait at the first check
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t kdone = 0;
-    for (int t = cid; t < args.total_tiles; t += ncl) {
-      const TileInfo ti = decode_tile(args, t);
-      const GemmProblem& P = args.p[ti.p];
-      const int a_row = ti.m * GEMM_TM + (int)cta * GEMM_BM;
-      for (int kb = 0; kb < ti.nk_total; ++kb, ++kdone) {
-        if (lock_on && (kdone % GEMM_LOCK_W) == 0) {
-          // the other clusters' progress was loaded at the previous check (its L2 latency, ~1-2 us
-          // under the GEMM's own TMA traffic, must not sit on the producer's issue path: a
-          // blocking poll every few k-blocks starved the MMA); block only when that stale view
-          // says this cluster leads by more than lock_d
-          const uint32_t s = min(kdone, 0xFFFFEu);
-          if (lane == 0) st_relaxed_gpu(sync + gemm_sync_prog(cid), (epoch << 20) | s);
-          const uint32_t need = s >= (uint32_t)args.lock_d ? s - (uint32_t)args.lock_d : 0u;
-          uint32_t mn = __reduce_min_sync(0xffffffffu, min(min(prog_view(pend[0], epoch), prog_view(pend[1], epoch)),
-                                                              prog_view(pend[2], epoch)));
-#if GEMM_LOCK_STATS
-          if (s > mn + 8u) max_lead = max(max_lead, s - mn - 8u);   // (the view is one check old)
-#endif
-          if (mn < need) {
-            const uint64_t t0 = globaltimer_ns();
-            while (true) {
-              __nanosleep(128);
-              poll_progress(sync, ncl, lane, pend);
-              mn = __reduce_min_sync(0xffffffffu, min(min(prog_view(pend[0], epoch), prog_view(pend[1], epoch)),
-                                                     prog_view(pend[2], epoch)));
-              if (mn >= need) break;
-              if (__any_sync(0xffffffffu, globaltimer_ns() - t0 > LOCK_TIMEOUT_NS)) {
-                lock_on = false;   // some cluster is not progressing (not resident?): stop waiting
-                if (lane == 0) st_relaxed_gpu(sync + gemm_sync_prog(cid), (epoch << 20) | 0xFFFFFu);
-                break;
-              }
-            }
-            wait_ns += globaltimer_ns() - t0;
-            ++wait_cnt;
-          }
-          poll_progress(sync, ncl, lane, pend);   // consumed at the next check
-        }
-        if (lane == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < args.total_tiles; t += ncl) {
+        const TileInfo ti = decode_tile(args, t);
+        const GemmProblem& P = args.p[ti.p];
+        const int a_row = ti.m * GEMM_TM + (int)cta * GEMM_BM;
+        for (int kb = 0; kb < ti.nk_total; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader)
             mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -709,34 +635,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             tma_load_2d_2sm(&P.tmAx, &full[stage], a_dst, slot * P.epi.r_alloc + ek * GEMM_BK, a_row);
             tma_load_2d_2sm(&P.tmBx, &full[stage], b_dst, ek * GEMM_BK, slot * P.N + ti.n * GEMM_BN + (int)cta * 128);
           }
-        }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
-    if (sync != nullptr && lane == 0) {
-      if (lock) st_relaxed_gpu(sync + gemm_sync_prog(cid), (epoch << 20) | 0xFFFFFu);   // done: never the slowest
-#if GEMM_LOCK_STATS
-      if (lock) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(sync + GEMM_SYNC_STATS), (unsigned long long)wait_ns);
-        atomicAdd(reinterpret_cast<unsigned long long*>(sync + GEMM_SYNC_STATS + 2), (unsigned long long)wait_cnt);
-        if (!lock_on) atomicAdd(sync + GEMM_SYNC_STATS + 4, 1u);
-        atomicMax(sync + GEMM_SYNC_STATS + 5, max_lead);
-      }
-#endif
-      // the last CTA of the launch advances the epoch for the next launch on this buffer
-      __threadfence();
-      if (atomicAdd(sync + 1, 1u) == gridDim.x - 1) {
-        sync[1] = 0;
-        st_relaxed_gpu(sync, ld_relaxed_gpu(sync) + 1u);
-      }
-    }
-    (void)wait_ns;
-    (void)wait_cnt;
-    (void)max_lead;
   } else if (warp == W_MMA) {
     // whole warp walks the tile loop; one elected lane issues inside the asm blocks, so the
     // descriptors stay warp-uniform (a lane-0 branch costs R2UR/elect loops per MMA)
@@ -876,65 +781,16 @@ bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uin
   return r == CUDA_SUCCESS;
 }
 
-__device__ __align__(128) uint32_t g_gemm_sync[GEMM_SYNC_WORDS];   // lockstep state of launches that bring none
-
-// DIT_GEMM_LOCK_D: the default lead (k-blocks) of the k-block lockstep (<= 0: off);
-// dit_debug_gemm_lock overrides it
-static int g_lock_d = -1000000;
-static int lock_d_default() {
-  if (g_lock_d == -1000000) {
-    const char* e = getenv("DIT_GEMM_LOCK_D");
-    g_lock_d = e != nullptr ? atoi(e) : GEMM_LOCK_D_DEF;
-  }
-  return g_lock_d > 0 ? g_lock_d : -1;
-}
-// GEMM_LOCK_STATS variant builds (tools/lock_bench.py): {total wait ns, wait events, clusters that
-// timed out} of the launches on the process-wide buffer since the last call; resets them
-extern "C" int dit_debug_gemm_lock_stats(unsigned long long* out3) {
-  uint32_t w[6] = {};
-  if (cudaMemcpyFromSymbol(w, g_gemm_sync, sizeof(w), GEMM_SYNC_STATS * 4) != cudaSuccess) return 1;
-  out3[0] = w[0] | ((unsigned long long)w[1] << 32);
-  out3[1] = w[2] | ((unsigned long long)w[3] << 32);
-  out3[2] = w[4] | ((unsigned long long)w[5] << 32);   // timeouts | max observed lead (k-blocks) << 32
-  const uint32_t z[6] = {};
-  return cudaMemcpyToSymbol(g_gemm_sync, z, sizeof(z), GEMM_SYNC_STATS * 4) == cudaSuccess ? 0 : 1;
-}
-
-int gemm_set_lock_default(int d) {
-  const int prev = lock_d_default();
-  g_lock_d = d > 0 ? d : -1;
-  return prev > 0 ? prev : 0;
-}
-
-cudaError_t gemm_launch(const GemmArgs& args_in, int num_sms, cudaStream_t s) {
+cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s) {
   static bool attr = false;
-  static uint32_t* default_sync = nullptr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaGetSymbolAddress(reinterpret_cast<void**>(&default_sync), g_gemm_sync);
-    if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (args_in.total_tiles <= 0) return cudaSuccess;
-  GemmArgs args = args_in;
-  if (args.sync == nullptr) args.sync = default_sync;
-  if (args.lock_d == 0) args.lock_d = lock_d_default();
+  if (args.total_tiles <= 0) return cudaSuccess;
   const int pairs = num_sms / 2;
   const int clusters = args.total_tiles < pairs ? args.total_tiles : pairs;
-  // rasterisation: groups of GEMM_GROUP_M M-tiles sweep all N; DIT_GEMM_HEAVY_GROUP=1 gives the
-  // K-heavy GEMMs (K >= 8192) groups of clusters / tiles_n M-tiles, so one round of tiles covers
-  // every N-tile of its M-panels (each A panel streamed once while the weight stays in L2)
-  static int heavy = -1;
-  if (heavy < 0) {
-    const char* e = getenv("DIT_GEMM_HEAVY_GROUP");
-    heavy = e != nullptr ? atoi(e) : GEMM_HEAVY_GROUP_DEF;
-  }
-  for (int i = 0; i < args.num_problems; ++i) {
-    GemmProblem& P = args.p[i];
-    P.group_m = GEMM_GROUP_M;
-    if (heavy > 0 && P.K >= 8192 && !P.shrink && P.tiles_n > 0) P.group_m = std::max(1, clusters / P.tiles_n);
-  }
   gemm_kernel<<<2 * clusters, NUM_THREADS, SMEM_BYTES, s>>>(args);
   return cudaGetLastError();
 }

@@ -93,7 +93,6 @@ struct GemmProblem {
   int M, N, K;
   int tiles_m, tiles_n;  // tiles_m: 256-row pair tiles
   int tile_begin;        // first global tile index of this problem
-  int group_m;           // rasterisation group (pair tiles along M per N sweep; set by gemm_launch)
   int num_tiles;
   // LoRA: per m-tile list of pool slots (device [tiles_m][slot_cap]) + counts
   const int* tile_slots;
@@ -110,20 +109,7 @@ struct GemmArgs {
   GemmProblem p[GEMM_MAX_PROBLEMS];
   int num_problems;
   int total_tiles;
-  // k-block lockstep of the clusters (an L2-locality hint, never a correctness dependency):
-  // sync = device [GEMM_SYNC_WORDS] u32, zeroed once by its owner: {epoch, done count, stats} in
-  // line 0, then one 128-byte line per cluster holding its progress (one line each: 74 clusters
-  // polling words of a few shared lines serialised at their L2 slices and starved the producers);
-  // lock_d = lead (k-blocks) a cluster may have over the slowest one (0: the DIT_GEMM_LOCK_D
-  // default, < 0: off)
-  uint32_t* sync;
-  int lock_d;
 };
-constexpr int GEMM_LOCK_MAX_CL = 96;
-constexpr int GEMM_SYNC_STATS = 2;        // u64 wait ns, u64 waits, u32 timeouts, u32 max lead (GEMM_LOCK_STATS builds)
-constexpr int GEMM_SYNC_LINE = 32;        // words per progress line
-constexpr int GEMM_SYNC_WORDS = GEMM_SYNC_LINE * (1 + GEMM_LOCK_MAX_CL);
-__host__ __device__ constexpr int gemm_sync_prog(int cluster) { return GEMM_SYNC_LINE * (1 + cluster); }
 
 // Encode a 2D/3D bf16 tensor map with SWIZZLE_128B (box inner = 64 elements).
 bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
@@ -134,9 +120,7 @@ bool make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
 bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                   uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
 
-// args.sync == nullptr: a process-wide buffer of this module (debug / bench launches)
 cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s);
-int gemm_set_lock_default(int lead);   // returns the previous default lead (0 = off)
 size_t gemm_smem_bytes();
 
 // ------------------------------------------------------------------ attention

@@ -99,7 +99,6 @@ EXPORTS = {
     "dit_debug_attention_trace": (C.c_int, [C.c_void_p]),
     "dit_debug_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  C.c_void_p]),
-    "dit_debug_gemm_lock": (C.c_int, [C.c_int32]),
     "dit_debug_gemm_resid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                        C.c_int32, C.c_int32, C.c_void_p]),
     "dit_debug_attention": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
