@@ -43,7 +43,13 @@ namespace attn_tc {
 
 constexpr int BQ = 128, NQ = 2, BKV = 128;
 constexpr int PANEL = 128 * 64 * 2;              // 16 KB: 128 rows x 64 bf16 (one 128-byte swizzle span)
-constexpr int KST = 2, VST = 2;
+#ifndef ATTN_KST
+#define ATTN_KST 2
+#endif
+#ifndef ATTN_VST
+#define ATTN_VST 2
+#endif
+constexpr int KST = ATTN_KST, VST = ATTN_VST;   // K / V ring stages (the kv-tile counter g indexes both)
 // per head dim: 128 rows x HD bf16 per tile (HD / 64 swizzle panels)
 template <int HD> __host__ __device__ constexpr int tile_bytes() { return 128 * HD * 2; }
 template <int HD> __host__ __device__ constexpr int smem_bytes() { return tile_bytes<HD>() * (NQ + KST + VST) + 1024 + 256; }
@@ -79,6 +85,12 @@ constexpr int POLY_MOD = ATTN_POLY_MOD, POLY_RES = ATTN_POLY_RES;   // every POL
 #define ATTN_POLY_RES64 3
 #endif
 constexpr uint32_t COL_S = 0, COL_O = 256;
+// split P arrive: bit c set = the softmax warps release P columns of kv [0, 32 (c + 1)) after
+// chunk c (the MMA warp starts the PV on them); the last chunk is always released at the end
+#ifndef ATTN_PMASK
+#define ATTN_PMASK 4
+#endif
+constexpr int PMASK = ATTN_PMASK & 7;
 constexpr float RESCALE_THRESH = 8.0f;
 
 DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -229,17 +241,16 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   uint8_t* sV = sK + KST * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;        // [KST]
-  uint64_t* k_empty = bars + 3;       // [KST]
-  uint64_t* v_full = bars + 5;        // [VST]
-  uint64_t* v_empty = bars + 7;       // [VST]
-  uint64_t* s_full = bars + 9;        // [NQ]
-  uint64_t* p_full = bars + 11;       // [NQ]
-  uint64_t* o_done = bars + 13;       // [NQ]
-  uint64_t* p_tail = bars + 15;       // [NQ] last quarter of P stored (split P arrive)
-  uint64_t* o_free = bars + 17;       // [NQ] epilogue has read O (next work item may overwrite it)
-  uint64_t* q_empty = bars + 19;      // last QK of a work item done (Q tiles reusable)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* k_full = bars + 1;                    // [KST]
+  uint64_t* k_empty = k_full + KST;               // [KST]
+  uint64_t* v_full = k_empty + KST;               // [VST]
+  uint64_t* v_empty = v_full + VST;               // [VST]
+  uint64_t* s_full = v_empty + VST;               // [NQ]
+  uint64_t* p_arr = s_full + NQ;                  // [NQ][4] P of kv chunk c (32 keys) released (PMASK)
+  uint64_t* o_done = p_arr + 4 * NQ;              // [NQ]
+  uint64_t* o_free = o_done + NQ;                 // [NQ] epilogue has read O (next work item may overwrite it)
+  uint64_t* q_empty = o_free + NQ;                // last QK of a work item done (Q tiles reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int N = p.N;
@@ -267,15 +278,18 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     tma_prefetch_desc(&maps.v);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VST; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < NQ; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], SM_WARPS_PER_TILE);
+      for (int c = 0; c < 4; ++c) mbar_init(&p_arr[4 * i + c], SM_WARPS_PER_TILE);
       mbar_init(&o_done[i], 1);
-      mbar_init(&p_tail[i], SM_WARPS_PER_TILE);
       mbar_init(&o_free[i], SM_WARPS_PER_TILE);
     }
     fence_barrier_init();
@@ -300,18 +314,18 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           for (int pn = 0; pn < NPANEL; ++pn)
             tma_load_3d(&maps.q, q_full, sQ + t * TILE_BYTES + pn * PANEL, pn * 64, q0 + t * BQ, bh);
         for (int j = 0; j < nkv; ++j, ++g) {
-          const int st = g & 1;
-          const uint32_t ph = (g >> 1) & 1;
+          const int st = g % KST, sv = g % VST;
+          const uint32_t ph = (g / KST) & 1, pv = (g / VST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
           if (it == 0) TRACE(0, j);
           mbar_expect_tx(&k_full[st], TILE_BYTES);
           for (int pn = 0; pn < NPANEL; ++pn)
             tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
-          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_wait(&v_empty[sv], pv ^ 1);
           if (it == 0) TRACE(1, j);
-          mbar_expect_tx(&v_full[st], TILE_BYTES);
+          mbar_expect_tx(&v_full[sv], TILE_BYTES);
           for (int pn = 0; pn < NPANEL; ++pn)
-            tma_load_3d(&maps.v, &v_full[st], sV + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
+            tma_load_3d(&maps.v, &v_full[sv], sV + sv * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
         }
       }
     }
@@ -324,9 +338,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     bool tr = false;
     // g: global kv-tile index (K/V ring stage + phase, and the s/p/o barrier phases)
     auto issue_qk = [&](int t, int g, int j) {
-      const int st = g & 1;
+      const int st = g % KST;
       if (t == 0 && lane == 0 && tr) TRACE(14, j);
-      if (t == 0) mbar_wait(&k_full[st], (g >> 1) & 1);
+      if (t == 0) mbar_wait(&k_full[st], (g / KST) & 1);
       if (t == 0 && lane == 0 && tr) TRACE(2, j);
       tc_fence_after();
       if constexpr (HD == 128)
@@ -339,25 +353,31 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       if (t == NQ - 1) tc_commit_warp(&k_empty[st]);
     };
     auto issue_pv = [&](int t, int g, int j, int it, int nkv) {
-      const int st = g & 1;
+      const int st = g % VST;
       if (lane == 0 && tr) TRACE(15 + t, j);
-      mbar_wait(&p_full[t], g & 1);
+      constexpr int c_first = (PMASK & 1) ? 0 : (PMASK & 2) ? 1 : (PMASK & 4) ? 2 : 3;
+      mbar_wait(&p_arr[4 * t + c_first], g & 1);
       if (lane == 0 && tr) TRACE(3 + t, j);
       if (j == 0 && it > 0) mbar_wait(&o_free[t], (it - 1) & 1);   // previous item's O read out
-      if (t == 0) mbar_wait(&v_full[st], (g >> 1) & 1);
+      if (t == 0) mbar_wait(&v_full[st], (g / VST) & 1);
       if (t == 0 && lane == 0 && tr) TRACE(5, j);
       tc_fence_after();
       {
-        // P columns of kv [0, 96) are released first (split arrive), the last 32 after
+        // P is released in chunks of 32 keys (PMASK); each chunk's two K = 16 MMAs wait for it
         const uint64_t vdesc = desc_mn_sw128(smem_u32(sV + st * TILE_BYTES), PANEL);
         const uint32_t od = tm + COL_O + t * HD, pa = tm + COL_S + t * 128;
 #pragma unroll
-        for (int kk = 0; kk < 6; ++kk)
-          tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, (j | kk) != 0);
-        mbar_wait(&p_tail[t], g & 1);
-        tc_fence_after();
+        for (int c = 0; c < 4; ++c) {
+          if (c > c_first && (c == 3 || ((PMASK >> (c - 1)) & 1))) {   // a new release point covers chunk c
+            int e = c;
+            while (e < 3 && !((PMASK >> e) & 1)) ++e;
+            mbar_wait(&p_arr[4 * t + e], g & 1);
+            tc_fence_after();
+          }
 #pragma unroll
-        for (int kk = 6; kk < 8; ++kk) tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, 1);
+          for (int kk = 2 * c; kk < 2 * c + 2; ++kk)
+            tc_mma_ts_warp(od, pa + kk * 8, vdesc + (uint64_t)(kk * 128), idesc_pv, (j | kk) != 0);
+        }
       }
       // O of this work item is final after its last PV: the only phase anyone waits on (the
       // epilogue).  Earlier PVs need no barrier: the commit of the next QK into S_t covers them.
@@ -424,8 +444,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (tr) TRACE(8 + t, j);
-          if (lane == 0) mbar_arrive(&p_full[t]);
-          if (lane == 0) mbar_arrive(&p_tail[t]);
+          for (int c = 0; c < 4; ++c)
+            if (lane == 0 && (c == 3 || ((PMASK >> c) & 1))) mbar_arrive(&p_arr[4 * t + c]);
           l = 1.f;
           continue;
         }
@@ -492,13 +512,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
             r[e] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(colS + c * 16, r);
-          if (c == 2) {   // kv [0, 96) of P are in TMEM: let the PV MMA start on them
+          if (c < 3 && ((PMASK >> c) & 1)) {   // kv [0, 32 (c + 1)) of P are in TMEM: let the PV MMA start on them
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (tr) TRACE(8 + t, j);
             if (trace != nullptr && it == 0 && lane == 0 && t == 0 && wq > 0) TRACE(16 + wq, j);   // arrive skew
-            if (lane == 0) mbar_arrive(&p_full[t]);
+            if (lane == 0) mbar_arrive(&p_arr[4 * t + c]);
           }
         }
         tmem_st_wait();
@@ -506,7 +526,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         __syncwarp();
         uint64_t tok = 0;
         if (lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(smem_u32(&p_tail[t])) : "memory");
+          asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(smem_u32(&p_arr[4 * t + 3])) : "memory");
         // row sum off the critical path (the PV MMA is already running): seeded with a zero
         // derived from the arrive's state token, so ptxas cannot hoist it above the arrive
         tok = __shfl_sync(0xffffffffu, tok, 0);
