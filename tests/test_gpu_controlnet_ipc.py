@@ -11,6 +11,7 @@ stores go over NVLink).
 """
 import dataclasses
 import multiprocessing as mp
+import os
 import time
 
 import numpy as np
@@ -21,14 +22,14 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-def _producer(h_res, h_flag, bits, value, conn):
+def _producer(h_res, h_flag, bits, value, dev, conn):
     import torch
     from paper_2604_08123_b200 import dit
     from paper_2604_08123_b200.synthetic import _bits_to_bf16_tensor
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(dev)
     dst = dit.ipc_open(h_res)
     flag = dit.ipc_open(h_flag)
-    src = _bits_to_bf16_tensor(bits, "cuda:0")
+    src = _bits_to_bf16_tensor(bits, f"cuda:{dev}")
     torch.cuda.synchronize()
     conn.send("ready")
     conn.recv()                       # the consumer has enqueued its dit_step
@@ -44,6 +45,12 @@ def test_controlnet_push_from_another_process(request):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    if os.environ.get("DIT_SHARED_GPU_RANKS") == "1":
+        pdev = 0
+    elif torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs: a producer process on the consumer's GPU risks Xid 109")
+    else:
+        pdev = 1
     from paper_2604_08123_b200 import SyntheticDiT
     cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=256, heads=2, rope_axes=(16, 56, 56))
     B, hh, ww, nt = 2, 8, 8, 16
@@ -58,7 +65,7 @@ def test_controlnet_push_from_another_process(request):
     from paper_2604_08123_b200 import dit
     ctx = mp.get_context("spawn")
     parent, child = ctx.Pipe()
-    p = ctx.Process(target=_producer, args=(dit.ipc_export(R), dit.ipc_export(flag[1:2]), bits, 7, child))
+    p = ctx.Process(target=_producer, args=(dit.ipc_export(R), dit.ipc_export(flag[1:2]), bits, 7, pdev, child))
     p.start()
     try:
         assert parent.poll(120) and parent.recv() == "ready"

@@ -10,9 +10,18 @@ consecutive steps (the flag epochs advance).  Latent parallelism (PAPER.md:365-3
 rank 0 the conditional, rank 1 the unconditional pass, v stored into the peer by the final
 GEMM's epilogue; both ranks' latents equal the one-GPU CFG step bitwise over three steps (the
 step-parity v buffers alternate).
+
+One GPU per rank: ranks whose kernels wait on one another (the flag barriers) must not share a
+GPU as separate processes -- nothing makes their contexts run at the same time, and on this
+B200 / driver stack two or four such processes on one GPU have raised Xid 109 (context-switch
+timeout; /opt/skills/guides/B200_PROFILING.md).  With fewer GPUs than ranks these tests skip;
+`profiles/r2_multiproc_tests.log` records them passing with both ranks on one GPU before that
+rule was applied, and the in-process group tests (one context, no context switches) cover the
+same exchanges on a single GPU.
 """
 import dataclasses
 import multiprocessing as mp
+import os
 import socket
 
 import numpy as np
@@ -26,23 +35,38 @@ SP_CFG = dataclasses.replace(synth.TINY_SINGLE, hidden=512, heads=4, depth_singl
 LP_CFG = dataclasses.replace(synth.SD3_TINY, hidden=256, heads=4, depth_double=2, pos_embed_max=16)
 
 
+def _gpus_or_skip(world):
+    """Rank r runs on cuda:r; DIT_SHARED_GPU_RANKS=1 forces every rank onto cuda:0 (the hazard
+    above -- for a deliberate local check only)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    if os.environ.get("DIT_SHARED_GPU_RANKS") == "1":
+        return 1
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs: waiting ranks as processes on one GPU risk Xid 109")
+    return world
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _sp_rank(rank, world, port, steps, q):
+def _sp_rank(rank, world, port, steps, ngpu, q):
     import torch
     import torch.distributed as dist
     from paper_2604_08123_b200 import SyntheticDiT
     from paper_2604_08123_b200.synthetic import _bits_to_bf16_tensor
     try:
-        torch.cuda.set_device(0)
+        dev = rank % ngpu
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         cfg = SP_CFG
         B, hh, ww, nt = 2, 16, 16, 64
-        m = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt, max_rank=8, max_adapters=1)
+        m = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt, max_rank=8, max_adapters=1,
+                         device=dev)
         m.register_synthetic_lora(5, rank=8, index=0)
         hs = [None] * world
         dist.all_gather_object(hs, m.peer_handle())
@@ -53,8 +77,8 @@ def _sp_rank(rank, world, port, steps, q):
         batch.adapter_id = np.array([5, -1], dtype=np.int32)
         nil, ntl = hh * ww // world, nt // world
         lat = torch.from_numpy(np.ascontiguousarray(batch.latents[:, rank * nil:(rank + 1) * nil])).cuda()
-        txt = _bits_to_bf16_tensor(np.ascontiguousarray(batch.txt[:, rank * ntl:(rank + 1) * ntl]), "cuda:0")
-        pooled = _bits_to_bf16_tensor(batch.pooled, "cuda:0")
+        txt = _bits_to_bf16_tensor(np.ascontiguousarray(batch.txt[:, rank * ntl:(rank + 1) * ntl]), f"cuda:{dev}")
+        pooled = _bits_to_bf16_tensor(batch.pooled, f"cuda:{dev}")
         outs = []
         for _ in range(steps):
             out, v = torch.empty_like(lat), torch.empty_like(lat)
@@ -75,18 +99,20 @@ def _sp_rank(rank, world, port, steps, q):
         raise
 
 
-def _lp_rank(rank, port, steps, q):
+def _lp_rank(rank, port, steps, ngpu, q):
     import torch
     import torch.distributed as dist
     from paper_2604_08123_b200 import SyntheticDiT
     try:
-        torch.cuda.set_device(0)
+        dev = rank % ngpu
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
         cfg = LP_CFG
         B, hh, ww, nt = 2, 12, 12, 40
         batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1, cfg_scale=6.0)
         batch.adapter_id = np.array([-1, 0], dtype=np.int32)
-        m = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt, max_rank=8, max_adapters=1)
+        m = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt, max_rank=8, max_adapters=1,
+                         device=dev)
         m.register_synthetic_lora(0, rank=8, index=0)
         hs = [None, None]
         dist.all_gather_object(hs, m.peer_handle())
@@ -152,12 +178,10 @@ def _reference_steps(cfg, B, hh, ww, nt, batch, steps, adapter_id, max_batch):
 
 
 def test_sequence_parallel_two_processes_bitwise():
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
     world, steps = 2, 2
+    ngpu = _gpus_or_skip(world)
     port = _free_port()
-    got = _spawn(_sp_rank, lambda r: (r, world, port, steps), world)
+    got = _spawn(_sp_rank, lambda r: (r, world, port, steps, ngpu), world)
     cfg = SP_CFG
     B, hh, ww, nt = 2, 16, 16, 64
     batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1)
@@ -171,12 +195,10 @@ def test_sequence_parallel_two_processes_bitwise():
 
 
 def test_latent_parallel_two_processes_bitwise():
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
     steps = 3
+    ngpu = _gpus_or_skip(2)
     port = _free_port()
-    got = _spawn(_lp_rank, lambda r: (r, port, steps), 2)
+    got = _spawn(_lp_rank, lambda r: (r, port, steps, ngpu), 2)
     cfg = LP_CFG
     B, hh, ww, nt = 2, 12, 12, 40
     batch = synth.make_batch(cfg, B, hh, ww, nt, n_adapters=1, cfg_scale=6.0)
