@@ -433,6 +433,16 @@ int sp_init_local(dit_ctx* ctx, void* group, int32_t rank);
 int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N, int32_t d,
                         void* out, void* stream);
 
+/* Bench/test-only: dit_debug_attention with the split tail chosen explicitly (split_tail = 1:
+ * when the persistent grid's last round of work items is at most half full, each tail item's keys
+ * are split into 2-4 parts whose partial O / max / sum a last part merges in part order --
+ * deterministic, within fp32 rounding of the unsplit result; 0: never).  dit_step uses it when
+ * the context was created with DIT_ATTN_SPLIT_TAIL=1 (opt-in: the tail items' rounding then
+ * depends on the batch composition, so bitwise batch invariance no longer holds for them).
+ * Asynchronous on stream. */
+int dit_debug_attention_ex(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N, int32_t d,
+                           void* out, int32_t split_tail, void* stream);
+
 /* Bench/test-only: out = bf16(A W^T + bias) through the step's tcgen05 GEMM (A [M][K],
  * W [N][K], bias [N], out [M][N], all device bf16; K % 64 == 0).  Asynchronous on stream. */
 int dit_debug_gemm(const void* A, const void* W, const void* bias, void* out, int32_t M, int32_t N, int32_t K,

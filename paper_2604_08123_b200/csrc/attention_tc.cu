@@ -230,7 +230,47 @@ DEVI int seq_len_of(const AttnParams& p, int b) { return RAGGED ? p.seq_valid[b]
 template <bool RAGGED>
 DEVI int kv_tiles(const AttnParams& p, int b) { return (seq_len_of<RAGGED>(p, b) + BKV - 1) / BKV; }
 
-template <int HD, bool RAGGED>
+// Persistent schedule of one CTA.  Work items (query block of 256, head, request) are dealt
+// round-robin; with p.split_tail (opt-in) the items of the last, partial round are each split into
+// S key ranges (S = min(4, CTAs / tail items) >= 2) so the tail round runs S times shorter: every
+// CTA first walks its full-round items, then at most one (tail item, key part) unit.  A part
+// leaves O / m / l of its range in p.tail_ws; the last part to finish (per query tile) merges the
+// S partials in part order (deterministic) and writes the output.  The split changes the
+// floating-point order of the tail items only -- results are reproducible run to run but no
+// longer bitwise independent of the batch composition, hence opt-in (SURVEY.md §8 caveat on
+// P3 / P9 / P10).
+template <bool SPLIT>
+struct TailSched {
+  int total, G, full, rem, S;
+  // (everything from the kernel parameters and gridDim -- uniform sources -- so the producer / MMA
+  // warps keep the schedule in uniform registers after setmaxnreg)
+  DEVI explicit TailSched(const AttnParams& p) : G((int)gridDim.x) {
+    total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
+    rem = SPLIT ? total % G : 0;
+    S = SPLIT ? min(min(4, G / max(rem, 1)), (p.N + BKV - 1) / BKV) : 1;   // the host launches SPLIT only when S >= 2
+    full = SPLIT ? total - rem : total;
+  }
+  // k-th unit of this CTA (k = 0, 1, ... in order, w carried between calls): item w, key part (0
+  // when not split); false when there is none
+  DEVI bool unit(int k, int& w, int& part) const {
+    if (!SPLIT) {   // (the plain walk, incremental: the same code as before the split existed)
+      w = k == 0 ? (int)blockIdx.x : w + G;
+      return w < total;
+    }
+    const int wf = (int)blockIdx.x + k * G;
+    part = 0;
+    if (wf < full) { w = wf; return true; }
+    if (k != full / G || (int)blockIdx.x >= rem * S) return false;
+    w = full + (int)blockIdx.x / S;
+    part = (int)blockIdx.x % S;
+    return true;
+  }
+  DEVI bool split(int w) const { return SPLIT && w >= full; }
+  DEVI int kv0(int part, int nkv) const { return SPLIT ? part * nkv / S : 0; }
+  DEVI int kv1(int part, int nkv) const { return SPLIT ? (part + 1) * nkv / S : nkv; }
+};
+
+template <int HD, bool RAGGED, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ AttnParams p) {
   constexpr int TILE_BYTES = tile_bytes<HD>();
   constexpr int NPANEL = HD / 64;
@@ -251,6 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
   uint64_t* o_free = o_done + NQ;                 // [NQ] epilogue has read O (next work item may overwrite it)
   uint64_t* q_empty = o_free + NQ;                // last QK of a work item done (Q tiles reusable)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
+  uint32_t* tail_last = tmem_slot + 1;            // [NQ] split tail: this CTA merges the tile's parts
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int N = p.N;
@@ -304,10 +345,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
    long long* const trace = TRACE_PTR;   // loaded after setmaxnreg (no spill)
    if (warp == W_LOAD) {
     if (lane == 0) {
+      const TailSched<SPLIT> sched(p);   // (built after setmaxnreg: no spills)
       int g = 0, it = 0;                           // kv-tile counter (ring position), item counter
-      for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+      for (int w = 0, part = 0; sched.unit(it, w, part); ++it) {
         const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
-        const int nkv = kv_tiles<RAGGED>(p, bh / p.H);
+        const int nkv_all = kv_tiles<RAGGED>(p, bh / p.H);
+        const int j0 = sched.split(w) ? sched.kv0(part, nkv_all) : 0;
+        const int nkv = sched.split(w) ? sched.kv1(part, nkv_all) - j0 : nkv_all;
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
         mbar_expect_tx(q_full, NQ * TILE_BYTES);
         for (int t = 0; t < NQ; ++t)
@@ -320,12 +364,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
           if (it == 0) TRACE(0, j);
           mbar_expect_tx(&k_full[st], TILE_BYTES);
           for (int pn = 0; pn < NPANEL; ++pn)
-            tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
+            tma_load_3d(&maps.k, &k_full[st], sK + st * TILE_BYTES + pn * PANEL, pn * 64, (j0 + j) * BKV, bh);
           mbar_wait(&v_empty[sv], pv ^ 1);
           if (it == 0) TRACE(1, j);
           mbar_expect_tx(&v_full[sv], TILE_BYTES);
           for (int pn = 0; pn < NPANEL; ++pn)
-            tma_load_3d(&maps.v, &v_full[sv], sV + sv * TILE_BYTES + pn * PANEL, pn * 64, j * BKV, bh);
+            tma_load_3d(&maps.v, &v_full[sv], sV + sv * TILE_BYTES + pn * PANEL, pn * 64, (j0 + j) * BKV, bh);
         }
       }
     }
@@ -384,9 +428,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       if (j == nkv - 1) tc_commit_warp(&o_done[t]);
       if (t == NQ - 1) tc_commit_warp(&v_empty[st]);
     };
+    const TailSched<SPLIT> sched(p);
     int g = 0, it = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-      const int nkv = kv_tiles<RAGGED>(p, (w / nqb) / p.H);
+    for (int w = 0, part = 0; sched.unit(it, w, part); ++it) {
+      const int nkv_all = kv_tiles<RAGGED>(p, (w / nqb) / p.H);
+      const int nkv = sched.split(w) ? sched.kv1(part, nkv_all) - sched.kv0(part, nkv_all) : nkv_all;
       tr = trace != nullptr && it == 0;
       mbar_wait(q_full, it & 1);
       issue_qk(0, g, 0);
@@ -416,12 +462,16 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const uint32_t colS = tmem + lane_base + COL_S + t * 128;
     const uint32_t colO = tmem + lane_base + COL_O + t * HD;
     const float sl2 = p.scale_log2;
+    const TailSched<SPLIT> sched(p);
     int g = 0, it = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+    for (int w = 0, part = 0; sched.unit(it, w, part); ++it) {
       const bool tr = trace != nullptr && it == 0 && lane == 0 && wq == 0;
       const int bh = w / nqb, q0 = (w - bh * nqb) * (NQ * BQ);
       const int b = bh / p.H, h = bh - b * p.H;
-      const int Nv = seq_len_of<RAGGED>(p, b), nkv = kv_tiles<RAGGED>(p, b);
+      const int nkv_all = kv_tiles<RAGGED>(p, b);
+      const bool split = sched.split(w);
+      const int j0 = split ? sched.kv0(part, nkv_all) : 0;
+      const int Nv = seq_len_of<RAGGED>(p, b) - j0 * BKV, nkv = split ? sched.kv1(part, nkv_all) - j0 : nkv_all;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j, ++g) {
         mbar_wait(&s_full[t], g & 1);
@@ -455,7 +505,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
         for (int c = 0; c < 4; ++c) tmem_ld32(colS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
         tmem_ld_wait();
         if (tr) TRACE(10 + t, j);
-        const int kv_valid = Nv - j * BKV;
+        const int kv_valid = Nv - j * BKV;   // (Nv counts from this unit's first key tile)
         if (kv_valid < BKV) {
 #pragma unroll
           for (int e = 0; e < 128; ++e)
@@ -553,6 +603,60 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
+      if (split) {
+        // split tail: leave this part's O (unnormalised, relative to m_used) and (m_used, l), then
+        // the last of the S parts of this query tile merges them in part order
+        const int ti = (w - sched.full) * NQ + t;
+        float* mine = p.tail_ws + ((size_t)((w - sched.full) * sched.S + part) * NQ + t) * BQ * (HD + 4) + (size_t)row * (HD + 4);
+#pragma unroll
+        for (int q = 0; q < HD / 4; ++q)
+          reinterpret_cast<float4*>(mine)[q] = make_float4(__uint_as_float(o[4 * q]), __uint_as_float(o[4 * q + 1]),
+                                                           __uint_as_float(o[4 * q + 2]), __uint_as_float(o[4 * q + 3]));
+        reinterpret_cast<float4*>(mine)[HD / 4] = make_float4(m_used, l, 0.f, 0.f);
+        __threadfence();
+        named_bar_sync(1 + t, BQ);
+        if (row == 0) tail_last[t] = atomicAdd(p.tail_cnt + ti, 1u) == (uint32_t)sched.S - 1 ? 1u : 0u;
+        named_bar_sync(1 + t, BQ);
+        if (tail_last[t] == 0u) continue;
+        __threadfence();
+        if (row == 0) p.tail_cnt[ti] = 0;   // (next launch)
+        const float* base = p.tail_ws + ((size_t)((w - sched.full) * sched.S) * NQ + t) * BQ * (HD + 4) + (size_t)row * (HD + 4);
+        const size_t pstride = (size_t)NQ * BQ * (HD + 4);   // floats between consecutive parts
+        float f[4], M = -INFINITY, lt = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          f[s2] = -INFINITY;
+          if (s2 < sched.S) {
+            const float4 ml = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride) + HD / 4);
+            f[s2] = ml.x;
+            M = fmaxf(M, ml.x);
+          }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          f[s2] = f[s2] == -INFINITY ? 0.f : exp2f(f[s2] - M);
+          if (s2 < sched.S) lt = fmaf(f[s2], __ldcg(base + s2 * pstride + HD + 1), lt);
+        }
+#pragma unroll
+        for (int q = 0; q < HD / 4; ++q) {
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) {
+            if (s2 < sched.S) {
+              const float4 v4 = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride) + q);
+              acc.x = fmaf(f[s2], v4.x, acc.x);
+              acc.y = fmaf(f[s2], v4.y, acc.y);
+              acc.z = fmaf(f[s2], v4.z, acc.z);
+              acc.w = fmaf(f[s2], v4.w, acc.w);
+            }
+          }
+          o[4 * q] = __float_as_uint(acc.x);
+          o[4 * q + 1] = __float_as_uint(acc.y);
+          o[4 * q + 2] = __float_as_uint(acc.z);
+          o[4 * q + 3] = __float_as_uint(acc.w);
+        }
+        l = lt;
+      }
       if (dst != nullptr) {
         const float inv = 1.0f / l;
 #pragma unroll
@@ -589,7 +693,9 @@ static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   constexpr int SMEM = smem_bytes<HD>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD, RAGGED, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e == cudaSuccess && !RAGGED)
+      e = cudaFuncSetAttribute(attn_tc_kernel<HD, RAGGED, !RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -609,7 +715,20 @@ static cudaError_t attention_tc_launch_hd(const AttnParams& p, cudaStream_t s) {
   // persistent: one CTA per SM walks work items (query block fastest, so the CTAs running at
   // the same time share each head's K/V in L2)
   const int total = (p.N + NQ * BQ - 1) / (NQ * BQ) * p.H * p.B;
-  attn_tc_kernel<HD, RAGGED><<<dim3(std::min(total, sms)), THREADS, SMEM, s>>>(m, p);
+  const int G = std::min(total, sms);
+  // split tail (opt-in): when the last round is at most half full (S >= 2 key parts per tail item);
+  // the split instantiation runs the full rounds as fast as the plain one (measured: d = 128
+  // 1341 vs 1341 TF/s at B = 8, H = 24, N = 4608) and shortens the tail round S-fold
+  bool split = false;
+  if (!RAGGED && p.split_tail && p.tail_ws && p.tail_cnt && total > G && total % G != 0) {
+    const int rem = total % G, nkv = (p.N + BKV - 1) / BKV;
+    const int S = std::min(std::min(4, G / rem), nkv);
+    split = S >= 2 && rem * S <= ATTN_TAIL_UNITS;
+  }
+  if (split)
+    attn_tc_kernel<HD, RAGGED, !RAGGED><<<dim3(G), THREADS, SMEM, s>>>(m, p);
+  else
+    attn_tc_kernel<HD, RAGGED, false><<<dim3(G), THREADS, SMEM, s>>>(m, p);
   return cudaGetLastError();
 }
 

@@ -207,6 +207,10 @@ struct dit_ctx {
   void* peer_cat[8] = {};
   PeerFlags peer_flags = {};
   uint32_t* flags = nullptr;         // [8] arrival epochs, written by the peers
+  // attention split tail (opt-in, DIT_ATTN_SPLIT_TAIL=1 at dit_create): partials + merge counters
+  bool attn_split_tail = false;
+  float* attn_tail_ws = nullptr;
+  uint32_t* attn_tail_cnt = nullptr;
   uint32_t sp_epoch = 0;
   std::vector<void*> ipc_opened;
   // latent (CFG) parallelism: rank 0 conditional, rank 1 unconditional branch
@@ -436,6 +440,16 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
   c->Nmax = cfg->max_img_tokens + cfg->max_txt_tokens;
   c->Rmax = cfg->max_batch * c->Nmax;
   c->r_alloc = cfg->max_rank > 0 ? (int)align_up(cfg->max_rank, 64) : 64;
+  {
+    const char* st = getenv("DIT_ATTN_SPLIT_TAIL");
+    if (st && st[0] == '1') {
+      const size_t wsb = attn_tail_ws_bytes(std::max(cfg->hidden / std::max(cfg->heads, 1), 64));
+      if (cudaMalloc(&c->attn_tail_ws, wsb) == cudaSuccess &&
+          cudaMalloc(&c->attn_tail_cnt, ATTN_TAIL_UNITS * 2 * 4) == cudaSuccess &&
+          cudaMemset(c->attn_tail_cnt, 0, ATTN_TAIL_UNITS * 2 * 4) == cudaSuccess)
+        c->attn_split_tail = true;
+    }
+  }
   c->mod_total = 12 * c->D * c->Ld + 3 * c->D * c->Ls + 2 * c->D;
   uint8_t* w = c->ws;
   c->h = reinterpret_cast<float*>(w + L.h);
@@ -561,6 +575,8 @@ extern "C" void dit_destroy(dit_ctx* c) {
   for (auto& e : c->pin_ev)
     if (e) cudaEventDestroy(e);
   if (c->pin) cudaFreeHost(c->pin);
+  if (c->attn_tail_ws) cudaFree(c->attn_tail_ws);
+  if (c->attn_tail_cnt) cudaFree(c->attn_tail_cnt);
   for (void* ptr : c->ipc_opened) dit_ipc_close(ptr);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->lp_comm) ncclCommDestroy(c->lp_comm);
@@ -2148,6 +2164,9 @@ static int step_impl(dit_ctx* c, const dit_batch* b, cudaStream_t s, int mode) {
     ap.ni = ni;
     ap.Nt = Nt;
     ap.seq_valid = ragged ? c->p_seq_valid : nullptr;
+    ap.split_tail = c->attn_split_tail ? 1 : 0;
+    ap.tail_ws = c->attn_tail_ws;
+    ap.tail_cnt = c->attn_tail_cnt;
     if (fused) {   // O rows straight to their owners' buffers
       ap.split = 3;
       ap.out_split = split;
@@ -2853,8 +2872,8 @@ extern "C" int dit_debug_gemm_resid(const void* A, const void* W, const void* bi
 
 // Test/bench-only: one attention launch on head-major q/k/v [B][H][N][d] (bf16),
 // O written joint-row-major [B*N][H*d] (d = 128 -> tcgen05 kernel).
-extern "C" int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N,
-                                   int32_t d, void* out, void* stream) {
+extern "C" int dit_debug_attention_ex(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N,
+                                      int32_t d, void* out, int32_t split_tail, void* stream) {
   if (!q || !k || !v || !out || B < 1 || H < 1 || N < 1) return DIT_EINVAL;
   AttnParams ap;
   memset(&ap, 0, sizeof(ap));
@@ -2869,7 +2888,27 @@ extern "C" int dit_debug_attention(const void* q, const void* k, const void* v, 
   ap.out = out;
   ap.ld_out = H * d;
   ap.split = 0;
+  static float* tail_ws = nullptr;        // one process-wide tail workspace (debug / bench launches)
+  static uint32_t* tail_cnt = nullptr;
+  if (split_tail && d >= 64) {
+    if (!tail_ws && (cudaMalloc(&tail_ws, attn_tail_ws_bytes(128)) != cudaSuccess ||
+                     cudaMalloc(&tail_cnt, ATTN_TAIL_UNITS * 2 * 4) != cudaSuccess ||
+                     cudaMemset(tail_cnt, 0, ATTN_TAIL_UNITS * 2 * 4) != cudaSuccess))
+      return DIT_ENOMEM;
+    ap.split_tail = 1;
+    ap.tail_ws = tail_ws;
+    ap.tail_cnt = tail_cnt;
+  }
   return attention_launch(ap, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? DIT_OK : DIT_ECUDA;
+}
+
+extern "C" int dit_debug_attention(const void* q, const void* k, const void* v, int32_t B, int32_t H, int32_t N,
+                                   int32_t d, void* out, void* stream) {
+  static const bool split_tail = [] {   // DIT_ATTN_SPLIT_TAIL=1: the split tail for bench runs
+    const char* e = getenv("DIT_ATTN_SPLIT_TAIL");
+    return e && e[0] == '1';
+  }();
+  return dit_debug_attention_ex(q, k, v, B, H, N, d, out, split_tail ? 1 : 0, stream);
 }
 
 namespace dit { cudaError_t attention_set_trace(long long* buf); }

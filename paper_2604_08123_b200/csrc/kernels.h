@@ -145,7 +145,15 @@ struct AttnParams {
   void* out_peer[8];
   int out_split;
   int head_off;
+  // split tail (opt-in, attention_tc.cu TailSched): the last partial round's items split along the
+  // keys; tail_ws = device fp32 [ATTN_TAIL_UNITS][2][128][d + 4] partials, tail_cnt = device u32
+  // [ATTN_TAIL_UNITS * 2] merge counters (zero; the merging part resets them)
+  int split_tail;
+  float* tail_ws;
+  uint32_t* tail_cnt;
 };
+constexpr int ATTN_TAIL_UNITS = 160;   // >= SMs: tail units never exceed the grid
+inline size_t attn_tail_ws_bytes(int d) { return (size_t)ATTN_TAIL_UNITS * 2 * 128 * (d + 4) * 4; }
 // Output row of query token n (global joint order) of request b; SP mode also
 // returns the destination rank in *dest (rows are then [dest][B][N_loc]).
 __host__ __device__ inline long long attn_out_row(const AttnParams& p, int b, int n) {

@@ -97,6 +97,8 @@ EXPORTS = {
     "sp_init_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "dit_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "dit_debug_attention_trace": (C.c_int, [C.c_void_p]),
+    "dit_debug_attention_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "dit_debug_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  C.c_void_p]),
     "dit_debug_gemm_resid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
