@@ -238,4 +238,6 @@ cudaError_t attention_launch(const AttnParams& p, cudaStream_t s) {
   }
 }
 
+cudaError_t attention_mma_preload() { return preload_module_of(reinterpret_cast<const void*>(&attn_fwd_kernel<32>)); }
+
 }  // namespace dit

@@ -738,4 +738,6 @@ cudaError_t attention_tc_launch(const AttnParams& p, cudaStream_t s) {
   return p.d == 64 ? attention_tc_launch_hd<64, false>(p, s) : attention_tc_launch_hd<128, false>(p, s);
 }
 
+cudaError_t attention_tc_preload() { return preload_module_of(reinterpret_cast<const void*>(&attn_tc::attn_tc_kernel<128, false, false>)); }
+
 }  // namespace dit

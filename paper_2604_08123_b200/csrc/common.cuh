@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #define DEVI __device__ __forceinline__
 
 typedef __nv_bfloat16 bf16;
@@ -354,3 +356,44 @@ template <int kCols>
 DEVI void tmem_dealloc_2sm(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
 }
+
+// ------------------------------------------------------------------ eager module loading
+// Load every kernel of the module (translation unit) holding `kernel` now.  Under CUDA's lazy
+// loading (torch turns it on) a kernel's first launch loads its module, and a load that happens
+// while another kernel of the process spins waiting for it -- the fused SP exchange barrier, a
+// ControlNet flag, in-process ranks -- can stall until that spin gives up.  dit_create preloads
+// every libdit module once.
+inline cudaError_t preload_module_of(const void* kernel) {
+  typedef CUresult (*PFN_getmod)(CUmodule*, CUfunction);
+  typedef CUresult (*PFN_count)(unsigned int*, CUmodule);
+  typedef CUresult (*PFN_enum)(CUfunction*, unsigned int, CUmodule);
+  typedef CUresult (*PFN_load)(CUfunction);
+  static PFN_getmod getmod = nullptr;
+  static PFN_count count = nullptr;
+  static PFN_enum enumerate = nullptr;
+  static PFN_load load = nullptr;
+  if (!getmod) {
+    void* p[4] = {};
+    cudaDriverEntryPointQueryResult q;
+    const char* names[4] = {"cuFuncGetModule", "cuModuleGetFunctionCount", "cuModuleEnumerateFunctions", "cuFuncLoad"};
+    for (int i = 0; i < 4; ++i)
+      if (cudaGetDriverEntryPoint(names[i], &p[i], cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return cudaErrorNotSupported;
+    count = reinterpret_cast<PFN_count>(p[1]);
+    enumerate = reinterpret_cast<PFN_enum>(p[2]);
+    load = reinterpret_cast<PFN_load>(p[3]);
+    getmod = reinterpret_cast<PFN_getmod>(p[0]);
+  }
+  cudaFunction_t f;
+  if (cudaGetFuncBySymbol(&f, kernel) != cudaSuccess) return cudaErrorInvalidDeviceFunction;
+  CUmodule m;
+  unsigned int n = 0;
+  if (getmod(&m, reinterpret_cast<CUfunction>(f)) != CUDA_SUCCESS || count(&n, m) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  std::vector<CUfunction> fs(n);
+  if (n && enumerate(fs.data(), n, m) != CUDA_SUCCESS) return cudaErrorNotSupported;
+  for (CUfunction fn : fs)
+    if (load(fn) != CUDA_SUCCESS) return cudaErrorNotSupported;
+  return cudaSuccess;
+}
+

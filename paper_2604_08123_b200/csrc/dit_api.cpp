@@ -422,6 +422,18 @@ extern "C" int dit_create(const dit_config* cfg, int device, void* workspace, si
     return DIT_ENOMEM;
   }
   if (cudaSetDevice(device) != cudaSuccess) { g_create_error = "cudaSetDevice failed"; return DIT_ECUDA; }
+  {
+    // every libdit kernel loaded now, not at its first launch (common.cuh preload_module_of): a
+    // lazy load while a spinning kernel of this process waits on it (exchange barriers, ControlNet
+    // flags, in-process ranks) can stall until the spin gives up
+    static std::once_flag once;
+    std::call_once(once, [] {
+      const cudaError_t e[5] = {gemm_preload(), attention_tc_preload(), attention_mma_preload(), elementwise_preload(),
+                                merge_preload()};
+      for (cudaError_t x : e)
+        if (x != cudaSuccess) fprintf(stderr, "[libdit] eager kernel loading unavailable (%s)\n", cudaGetErrorString(x));
+    });
+  }
   dit_ctx* c = new dit_ctx();
   c->cfg = *cfg;
   c->device = device;

@@ -735,4 +735,6 @@ cudaError_t cfg_euler_launch(const float* vc, const float* vu, const float* g, c
       count / 4);
   return cudaGetLastError();
 }
+cudaError_t elementwise_preload() { return preload_module_of(reinterpret_cast<const void*>(&cast_bf16_kernel)); }
+
 }  // namespace dit

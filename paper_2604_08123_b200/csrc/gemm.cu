@@ -795,4 +795,6 @@ cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t gemm_preload() { return preload_module_of(reinterpret_cast<const void*>(&gemm_kernel)); }
+
 }  // namespace dit

@@ -121,6 +121,12 @@ bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uin
                   uint64_t stride2_bytes, uint32_t box0, uint32_t box1);
 
 cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s);
+// eager loading of each translation unit's kernels (common.cuh preload_module_of)
+cudaError_t gemm_preload();
+cudaError_t attention_tc_preload();
+cudaError_t attention_mma_preload();
+cudaError_t elementwise_preload();
+cudaError_t merge_preload();
 size_t gemm_smem_bytes();
 
 // ------------------------------------------------------------------ attention

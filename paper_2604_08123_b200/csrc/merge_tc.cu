@@ -308,4 +308,6 @@ cudaError_t restore_log_launch(const void* jobs_dev, int njobs, const unsigned l
   return cudaGetLastError();
 }
 
+cudaError_t merge_preload() { return preload_module_of(reinterpret_cast<const void*>(&merge_tc::restore_log_kernel)); }
+
 }  // namespace dit

@@ -3,7 +3,9 @@ round of work items is at most half full, each tail item's keys are split into S
 partial O / max / sum the last part merges in part order.  Checked against a plain PyTorch fp32
 reference over EVERY (request, head) -- the tail items are the last ones -- at S = 2, 3 and 4 and
 both head dims, run-to-run bitwise determinism, agreement with the unsplit kernel within rounding,
-and a dit_step with the split tail on against the fp64 oracle."""
+and a dit_step with the split tail on against the fp64 oracle.  (Named to run last: run before
+tests/test_gpu_bmax16.py in one process, the in-process two-rank sequence-parallel test there
+stalled in its flag barrier -- ranks spinning on one GPU, the hazard the profiling guide warns of.)"""
 import ctypes as C
 import dataclasses
 import os
