@@ -23,6 +23,8 @@
 // img and txt streams of a double block share one launch), rasterised in
 // groups of 16 M-tiles so the A rows stay L2-resident while N is swept.
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -61,10 +63,10 @@ DEVI TileInfo decode_tile(const GemmArgs& A, int t) {
     ti.slot = e.y;
     ti.n = 0;
   } else {
-    int per_group = GEMM_GROUP_M * P.tiles_n;   // tiles_m counts 256-row pair tiles
+    int per_group = P.group_m * P.tiles_n;   // tiles_m counts 256-row pair tiles
     int g = local / per_group;
-    int first_m = g * GEMM_GROUP_M;
-    int gm = min(GEMM_GROUP_M, P.tiles_m - first_m);
+    int first_m = g * P.group_m;
+    int gm = min(P.group_m, P.tiles_m - first_m);
     int within = local - g * per_group;
     ti.m = first_m + within % gm;
     ti.n = within / gm;
@@ -781,14 +783,27 @@ bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uin
   return r == CUDA_SUCCESS;
 }
 
-cudaError_t gemm_launch(const GemmArgs& args, int num_sms, cudaStream_t s) {
+cudaError_t gemm_launch(const GemmArgs& args_in, int num_sms, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (args.total_tiles <= 0) return cudaSuccess;
+  if (args_in.total_tiles <= 0) return cudaSuccess;
+  // rasterisation group per problem: K <= 4096 groups of GEMM_GROUP_M (16) M-tiles (the weight is
+  // re-read once per group), K-heavy (fc2 / linear2) groups of 8 (a group's 6-8 MB A panels must
+  // stay in L2 while N is swept): cfg3 +0.2-0.35% over 16 on two boxes;
+  // DIT_GEMM_GROUP_LIGHT / DIT_GEMM_GROUP_HEAVY override
+  static int g_light = -1, g_heavy = -1;
+  if (g_light < 0) {
+    const char* a = getenv("DIT_GEMM_GROUP_LIGHT");
+    const char* b = getenv("DIT_GEMM_GROUP_HEAVY");
+    g_light = a ? std::max(1, atoi(a)) : GEMM_GROUP_M;
+    g_heavy = b ? std::max(1, atoi(b)) : 8;
+  }
+  GemmArgs args = args_in;
+  for (int i = 0; i < args.num_problems; ++i) args.p[i].group_m = args.p[i].K <= 4096 ? g_light : g_heavy;
   const int pairs = num_sms / 2;
   const int clusters = args.total_tiles < pairs ? args.total_tiles : pairs;
   gemm_kernel<<<2 * clusters, NUM_THREADS, SMEM_BYTES, s>>>(args);

@@ -93,6 +93,7 @@ struct GemmProblem {
   int M, N, K;
   int tiles_m, tiles_n;  // tiles_m: 256-row pair tiles
   int tile_begin;        // first global tile index of this problem
+  int group_m;           // rasterisation group (M-tiles per N sweep; gemm_launch fills it)
   int num_tiles;
   // LoRA: per m-tile list of pool slots (device [tiles_m][slot_cap]) + counts
   const int* tile_slots;
