@@ -89,3 +89,27 @@ def test_split_tail_dit_step_vs_oracle(torch_cuda):
     x_o, v_o = O.dit_step(cfg, W, batch, {2: oracle_adapter(cfg, 16, 0)[0]}, {}, n_res=0)
     check(v, v_o, "v")
     check(lat, x_o, "latents")
+
+
+def test_split_tail_nccl_sp_layout_world1_bitwise(torch_cuda):
+    """The split tail's merged rows written through the sequence-parallel output layout (a 1-rank
+    NCCL communicator, DIT_FORCE_SP: send layout + ncclAlltoAll + scatter) equal the plain split-tail
+    step bitwise -- the merge writes every row where the unsplit epilogue would."""
+    from paper_2604_08123_b200 import SyntheticDiT
+    from paper_2604_08123_b200.dit import nccl_unique_id
+    cfg = dataclasses.replace(synth.TINY_SINGLE, hidden=512, heads=4, depth_single=1, rope_axes=(16, 56, 56))
+    B, hh, ww, nt = 3, 64, 64, 512          # 18 query blocks x 4 heads x 3 = 216 items: a 68-item tail
+    batch = synth.make_batch(cfg, B, hh, ww, nt)
+    os.environ["DIT_ATTN_SPLIT_TAIL"] = "1"
+    try:
+        ref = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt)
+        _, v1 = ref.step(batch)
+        os.environ["DIT_FORCE_SP"] = "1"
+        m = SyntheticDiT(cfg, max_batch=B, max_img_tokens=hh * ww, max_txt_tokens=nt)
+        m.sp_init(1, 0, nccl_unique_id())
+        _, v2 = m.step(batch)
+    finally:
+        os.environ.pop("DIT_FORCE_SP", None)
+        del os.environ["DIT_ATTN_SPLIT_TAIL"]
+    np.testing.assert_array_equal(v2, v1)
+    assert np.isfinite(v1).all()
