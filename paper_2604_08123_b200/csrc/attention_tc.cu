@@ -49,10 +49,18 @@ constexpr int PANEL = 128 * 64 * 2;              // 16 KB: 128 rows x 64 bf16 (o
 #ifndef ATTN_VST
 #define ATTN_VST 2
 #endif
-constexpr int KST = ATTN_KST, VST = ATTN_VST;   // K / V ring stages (the kv-tile counter g indexes both)
+#ifndef ATTN_KST64
+#define ATTN_KST64 3
+#endif
+// K / V ring stages (the kv-tile counter g indexes both); d = 64: a 3-stage K ring (+2.5% with the
+// {64, 96} P releases below)
+template <int HD> __host__ __device__ constexpr int kst_of() { return HD == 64 ? ATTN_KST64 : ATTN_KST; }
+template <int HD> __host__ __device__ constexpr int vst_of() { return ATTN_VST; }
 // per head dim: 128 rows x HD bf16 per tile (HD / 64 swizzle panels)
 template <int HD> __host__ __device__ constexpr int tile_bytes() { return 128 * HD * 2; }
-template <int HD> __host__ __device__ constexpr int smem_bytes() { return tile_bytes<HD>() * (NQ + KST + VST) + 1024 + 256; }
+template <int HD> __host__ __device__ constexpr int smem_bytes() {
+  return tile_bytes<HD>() * (NQ + kst_of<HD>() + vst_of<HD>()) + 1024 + 256;
+}
 constexpr int SM_WARPS_PER_TILE = 4;
 // 12 warps = 3 warpgroups: softmax WG0/WG1, WG2 = 2 idle + producer + MMA (highest ids).
 // setmaxnreg moves registers from WG2 to the softmax warpgroups (S row in registers).
@@ -90,7 +98,10 @@ constexpr uint32_t COL_S = 0, COL_O = 256;
 #ifndef ATTN_PMASK
 #define ATTN_PMASK 4
 #endif
-constexpr int PMASK = ATTN_PMASK & 7;
+#ifndef ATTN_PMASK64
+#define ATTN_PMASK64 6
+#endif
+template <int HD> __host__ __device__ constexpr int pmask_of() { return (HD == 64 ? ATTN_PMASK64 : ATTN_PMASK) & 7; }
 constexpr float RESCALE_THRESH = 8.0f;
 
 DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -274,6 +285,7 @@ template <int HD, bool RAGGED, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ AttnParams p) {
   constexpr int TILE_BYTES = tile_bytes<HD>();
   constexpr int NPANEL = HD / 64;
+  constexpr int KST = kst_of<HD>(), VST = vst_of<HD>(), PMASK = pmask_of<HD>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                              // [NQ] tiles
