@@ -52,10 +52,13 @@ constexpr int PANEL = 128 * 64 * 2;              // 16 KB: 128 rows x 64 bf16 (o
 #ifndef ATTN_KST64
 #define ATTN_KST64 3
 #endif
-// K / V ring stages (the kv-tile counter g indexes both); d = 64: a 3-stage K ring (+2.5% with the
-// {64, 96} P releases below)
+#ifndef ATTN_VST128
+#define ATTN_VST128 3
+#endif
+// K / V ring stages (the kv-tile counter g indexes both), with the {64, 96} P releases below:
+// d = 64 a 3-stage K ring (+2.5%), d = 128 a 3-stage V ring (+1.1-1.2%)
 template <int HD> __host__ __device__ constexpr int kst_of() { return HD == 64 ? ATTN_KST64 : ATTN_KST; }
-template <int HD> __host__ __device__ constexpr int vst_of() { return ATTN_VST; }
+template <int HD> __host__ __device__ constexpr int vst_of() { return HD == 128 ? ATTN_VST128 : ATTN_VST; }
 // per head dim: 128 rows x HD bf16 per tile (HD / 64 swizzle panels)
 template <int HD> __host__ __device__ constexpr int tile_bytes() { return 128 * HD * 2; }
 template <int HD> __host__ __device__ constexpr int smem_bytes() {
@@ -96,7 +99,7 @@ constexpr uint32_t COL_S = 0, COL_O = 256;
 // split P arrive: bit c set = the softmax warps release P columns of kv [0, 32 (c + 1)) after
 // chunk c (the MMA warp starts the PV on them); the last chunk is always released at the end
 #ifndef ATTN_PMASK
-#define ATTN_PMASK 4
+#define ATTN_PMASK 6
 #endif
 #ifndef ATTN_PMASK64
 #define ATTN_PMASK64 6
