@@ -1,7 +1,8 @@
 cd $GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -m gpu -q -rs -p no:cacheprovider > gpurun_out/att_full.log 2>&1; tail -1 gpurun_out/att_full.log
+V=$GRAFT_REPO_ROOT/paper_2604_08123_b200/build/variants
 for r in 1 2; do
-  timeout 120 python tools/attn_bench.py 2>&1 | tail -1
-  timeout 120 python tools/attn_bench.py 8 24 4429 64 2>&1 | tail -1
+for v in base p6 p10 p16 r216 r200; do
+  L=""; if [ $v != base ]; then L=$V/libdit_$v.so; fi
+  echo "== $v run $r: $(DIT_LIB_OVERRIDE=$L timeout 120 python tools/attn_bench.py 2>&1 | tail -1 | awk "{print \$8}") / d64: $(DIT_LIB_OVERRIDE=$L timeout 120 python tools/attn_bench.py 8 24 4429 64 2>&1 | tail -1 | awk "{print \$8}")"
 done
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/att_cfg3.json 2>/dev/null; python tools/bench_brief.py gpurun_out/att_cfg3.json 2>/dev/null | head -2
+done
