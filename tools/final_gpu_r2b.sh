@@ -1,6 +1,6 @@
 set -x
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2final2
+O=gpurun_out/r2final5
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit,temperature.gpu,driver_version --format=csv > $O/nvsmi.txt
 timeout 1500 python -m pytest tests -m gpu -q -rs > $O/pytest_gpu.log 2>&1
