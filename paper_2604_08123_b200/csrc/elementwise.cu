@@ -93,6 +93,9 @@ __global__ void __launch_bounds__(LN_THREADS) lnmod_kernel(const LnModParams p, 
 // reads stay in flight independently of the reductions (the one-block-per-row
 // kernel is limited by register occupancy to ~120 KB in flight per SM).
 constexpr int LNP_STAGES = 2;
+#ifndef LNP_CTAS_PER_SM
+#define LNP_CTAS_PER_SM 8
+#endif
 constexpr int LNP_MAXD = 3072;
 
 DEVI int ln_row_of(const LnModParams& p, int r, int& seg, int& b, int& n, int& out_row) {
@@ -188,8 +191,8 @@ cudaError_t lnmod_launch(const LnModParams& p, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const bool aligned = (reinterpret_cast<uintptr_t>(p.h) & 15) == 0 && (p.D * 4) % 16 == 0;
-  if (p.D <= LNP_MAXD && aligned && total >= 8 * sms) {
-    lnmod_persistent_kernel<<<8 * sms, LN_THREADS, 0, s>>>(p, total);
+  if (p.D <= LNP_MAXD && aligned && total >= LNP_CTAS_PER_SM * sms) {
+    lnmod_persistent_kernel<<<LNP_CTAS_PER_SM * sms, LN_THREADS, 0, s>>>(p, total);
   } else {
     lnmod_kernel<<<total, LN_THREADS, 0, s>>>(p, total);
   }
